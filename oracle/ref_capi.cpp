@@ -1,0 +1,305 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY (see oracle_abi.h).
+//
+// extern "C" wrappers over the unmodified reference library. oracle/Makefile
+// compiles /root/reference/proj/src/*.cpp in place with -Dchebstep=chebstep_ref
+// and this file with the same flag, so every reference symbol lives in
+// namespace chebstep_ref and cannot collide with the product's chebstep::
+// drop-in API. Each wrapper converts plain arrays to the reference types,
+// calls the reference function named in its comment, and maps the
+// reference exception hierarchy (errors.hpp:9-56) to CS_* status codes.
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "chebstep/block.hpp"
+#include "chebstep/csr.hpp"
+#include "chebstep/dense_ops.hpp"
+#include "chebstep/errors.hpp"
+#include "chebstep/gram.hpp"
+#include "chebstep/lapack.hpp"
+#include "chebstep/mpk.hpp"
+#include "chebstep/precond.hpp"
+#include "chebstep/problems.hpp"
+#include "chebstep/solver.hpp"
+#include "chebstep/spectral.hpp"
+#include "chebstep/util.hpp"
+#include "oracle_abi.h"
+
+namespace cs = chebstep;  // == chebstep_ref under -Dchebstep=chebstep_ref
+
+namespace {
+thread_local std::string g_msg;
+thread_local int g_payload = 0;
+
+template <class F>
+int guarded(F&& f) {
+  g_msg.clear();
+  g_payload = 0;
+  try {
+    f();
+    return 0;
+  } catch (const cs::DimensionError& e) {
+    g_msg = e.what();
+    return 1;
+  } catch (const cs::InvalidMatrixError& e) {
+    g_msg = e.what();
+    return 2;
+  } catch (const cs::NotSpdError& e) {
+    g_msg = e.what();
+    return 3;
+  } catch (const cs::BasisBreakdownError& e) {
+    g_msg = e.what();
+    g_payload = e.column;
+    return 4;
+  } catch (const cs::SolverBreakdownError& e) {
+    g_msg = e.what();
+    g_payload = e.outer_iteration;
+    return 5;
+  } catch (const cs::GuardExceededError& e) {
+    g_msg = e.what();
+    return 6;
+  } catch (const cs::ParseError& e) {
+    g_msg = e.what();
+    return 7;
+  } catch (const cs::InvalidArgumentError& e) {
+    g_msg = e.what();
+    return 8;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return 9;
+  }
+}
+
+cs::CsrMatrix make_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+  cs::CsrMatrix a;
+  a.n = n;
+  a.row_offsets.assign(rp, rp + n + 1);
+  const int64_t nnz = rp[n];
+  a.col_indices.assign(ci, ci + nnz);
+  a.values.assign(v, v + nnz);
+  return a;
+}
+
+struct Precond {
+  cs::IdentityPreconditioner ident;
+  std::unique_ptr<cs::JacobiPreconditioner> jac;
+  const cs::Preconditioner& get() const {
+    return jac ? static_cast<const cs::Preconditioner&>(*jac) : ident;
+  }
+};
+
+void make_precond(Precond& p, const cs::CsrMatrix& a, int kind) {
+  if (kind == 1) p.jac = std::make_unique<cs::JacobiPreconditioner>(a);
+  else if (kind != 0) throw cs::InvalidArgumentError("unknown preconditioner kind");
+}
+
+cs::VectorBlock block_of(int64_t n, int k, const double* d) {
+  cs::VectorBlock b(n, k);
+  std::memcpy(b.data.data(), d, sizeof(double) * static_cast<size_t>(n) * k);
+  return b;
+}
+
+cs::SmallDense dense_of(int r, int c, const double* d) {
+  cs::SmallDense m(r, c);
+  std::memcpy(m.data.data(), d, sizeof(double) * static_cast<size_t>(r) * c);
+  return m;
+}
+
+void fill_report(const cs::SolveReport& r, oc_report* o) {
+  o->converged = r.converged ? 1 : 0;
+  o->outer_iters = r.outer_iters;
+  o->spmv_count = r.spmv_count;
+  o->precond_count = r.precond_count;
+  o->allreduce_count = r.allreduce_count;
+  o->local_update_flops = r.local_update_flops;
+  o->gram_solve_flops = r.gram_solve_flops;
+  o->lambda_min = r.spectrum_used.lambda_min;
+  o->lambda_max = r.spectrum_used.lambda_max;
+  auto copy = [&](const std::vector<double>& src, double* dst, int* len) {
+    const int m = static_cast<int>(src.size());
+    *len = m;
+    if (dst)
+      for (int i = 0; i < m && i < o->cap; ++i) dst[i] = src[i];
+  };
+  copy(r.rel_residual, o->rel_residual, &o->n_rel);
+  copy(r.delta_alpha, o->delta_alpha, &o->n_da);
+  copy(r.delta_beta, o->delta_beta, &o->n_db);
+}
+}  // namespace
+
+extern "C" {
+
+// problems.cpp:13-53
+int ref_poisson27_fill(int64_t nx, int64_t ny, int64_t nz, int64_t* rowptr, int64_t* col,
+                       double* val) {
+  return guarded([&] {
+    cs::PoissonSystem sys = cs::poisson27({nx, ny, nz});
+    std::memcpy(rowptr, sys.a.row_offsets.data(), sizeof(int64_t) * (sys.a.n + 1));
+    std::memcpy(col, sys.a.col_indices.data(), sizeof(int64_t) * sys.a.nnz());
+    std::memcpy(val, sys.a.values.data(), sizeof(double) * sys.a.nnz());
+  });
+}
+
+// csr.cpp:111-124
+int ref_spmv(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* x,
+             double* y) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    cs::spmv_into(a, {x, static_cast<size_t>(n)}, {y, static_cast<size_t>(n)});
+  });
+}
+
+// precond.cpp:15-30 (the inverse diagonal is private; apply to ones)
+int ref_jacobi_invdiag(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                       double* out) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    cs::JacobiPreconditioner m(a);
+    std::vector<double> ones(static_cast<size_t>(n), 1.0);
+    m.apply(ones, {out, static_cast<size_t>(n)});
+  });
+}
+
+// mpk.cpp:26-71
+int ref_mpk(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, int precond,
+            const double* r, int s, double lo, double hi, double* z, double* p) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    Precond m;
+    make_precond(m, a, precond);
+    const auto params = cs::ChebyshevParams::from_interval(lo, hi);
+    cs::MpkResult res = cs::mpk_chebyshev(a, {r, static_cast<size_t>(n)}, s, m.get(), params);
+    std::memcpy(z, res.z.data.data(), sizeof(double) * res.z.data.size());
+    std::memcpy(p, res.p.data.data(), sizeof(double) * res.p.data.size());
+  });
+}
+
+// dense_ops.cpp:19-27
+int ref_block_gram(int64_t n, int ku, int kv, const double* u, const double* w, double* g) {
+  return guarded([&] {
+    const cs::SmallDense out = cs::block_gram(block_of(n, ku, u), block_of(n, kv, w));
+    std::memcpy(g, out.data.data(), sizeof(double) * out.data.size());
+  });
+}
+
+// dense_ops.cpp:29-42
+int ref_block_update(int64_t n, int m, int k, const double* y, const double* x, const double* c,
+                     double* out) {
+  return guarded([&] {
+    const cs::VectorBlock r =
+        cs::block_update(block_of(n, k, y), block_of(n, m, x), dense_of(m, k, c));
+    std::memcpy(out, r.data.data(), sizeof(double) * r.data.size());
+  });
+}
+
+// gram.cpp:38-49
+int ref_assemble_gram(int64_t n, int k, const double* q, const double* aq, double* w) {
+  return guarded([&] {
+    const cs::GramSystem g = cs::assemble_gram(block_of(n, k, q), block_of(n, k, aq));
+    std::memcpy(w, g.w.data.data(), sizeof(double) * g.w.data.size());
+  });
+}
+
+// gram.cpp:51-58 + 78-119
+int ref_fgs_solve(int s, const double* w, int k, const double* rhs, int nu, double* x,
+                  double* delta) {
+  return guarded([&] {
+    const cs::GramSystem g = cs::gram_from_matrix(dense_of(s, s, w));
+    cs::FgsConfig cfg;
+    cfg.nu = nu;
+    const cs::FgsResult r = cs::fgs_solve(g, dense_of(s, k, rhs), cfg);
+    std::memcpy(x, r.x.data.data(), sizeof(double) * r.x.data.size());
+    *delta = r.rel_residual;
+  });
+}
+
+// dense_ops.cpp:55-88
+int ref_cholesky_solve(int s, const double* w, int k, const double* rhs, double* x) {
+  return guarded([&] {
+    const cs::SmallDense r = cs::small_cholesky_solve(dense_of(s, s, w), dense_of(s, k, rhs));
+    std::memcpy(x, r.data.data(), sizeof(double) * r.data.size());
+  });
+}
+
+// util.cpp:31-36
+int ref_random_vector(int64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    const std::vector<double> r = cs::random_vector(n, seed);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// lapack.cpp:61-71 (LAPACKE_dsterf)
+int ref_tridiag_eigvals(int m, const double* diag, const double* off, double* out) {
+  return guarded([&] {
+    std::vector<double> d(diag, diag + m);
+    std::vector<double> e(off, off + (m > 0 ? m - 1 : 0));
+    const std::vector<double> r = cs::lapack::tridiag_eigvals(d, e);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// spectral.cpp:60-132
+int ref_estimate_interval(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                          int precond, int steps, uint64_t seed, double* lo, double* hi) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    Precond m;
+    make_precond(m, a, precond);
+    const cs::SpectrumEstimate e = cs::estimate_interval(a, m.get(), steps, seed);
+    *lo = e.lambda_min;
+    *hi = e.lambda_max;
+  });
+}
+
+// solver.cpp:78-190
+int ref_pcg_s_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                    const double* b, const double* x0, int precond, const oc_cfg* c, double* x,
+                    oc_report* rep) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    Precond m;
+    make_precond(m, a, precond);
+    cs::SolverConfig cfg;
+    cfg.s = c->s;
+    cfg.tol = c->tol;
+    cfg.max_outer = c->max_outer;
+    cfg.fgs.nu = c->nu;
+    cfg.gram_solver = c->gram == 1 ? cs::GramSolverKind::cholesky : cs::GramSolverKind::fgs;
+    if (c->has_spectrum) {
+      cs::SpectrumEstimate e;
+      e.lambda_min = c->lambda_min;
+      e.lambda_max = c->lambda_max;
+      cfg.spectrum = e;
+    }
+    cfg.lanczos_steps = c->lanczos_steps;
+    cfg.seed = c->seed;
+    const cs::SolveResult res = cs::pcg_s_solve(a, {b, static_cast<size_t>(n)},
+                                                {x0, static_cast<size_t>(n)}, m.get(), cfg);
+    std::memcpy(x, res.x.data(), sizeof(double) * res.x.size());
+    fill_report(res.report, rep);
+  });
+}
+
+// solver.cpp:192-264
+int ref_pcg_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                  const double* b, const double* x0, int precond, double tol, int max_iter,
+                  double* x, oc_report* rep) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    Precond m;
+    make_precond(m, a, precond);
+    const cs::SolveResult res = cs::pcg_solve(a, {b, static_cast<size_t>(n)},
+                                              {x0, static_cast<size_t>(n)}, m.get(), tol, max_iter);
+    std::memcpy(x, res.x.data(), sizeof(double) * res.x.size());
+    fill_report(res.report, rep);
+  });
+}
+
+const char* ref_last_error(int* payload) {
+  if (payload) *payload = g_payload;
+  return g_msg.c_str();
+}
+
+}  // extern "C"

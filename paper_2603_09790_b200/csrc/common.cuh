@@ -1,0 +1,78 @@
+// common.cuh -- shared device/host definitions of libchebstep_gpu (sm_100a).
+//
+// Data layout in HBM:
+//  * Matrix: SELL-32. Rows are grouped in slices of 32 consecutive rows; a
+//    slice stores its nonzeros column-major by slot (slot k of lane l at
+//    vals[slice_ptr[s] + k*32 + l]), padded to the slice's widest row with
+//    val = 0, col = -1. Columns are int32 local indices (owned rows
+//    0..n_local-1, then ghosts), values FP64: 12 B per nonzero. Within a row
+//    the reference's stored column order is kept, so the per-row
+//    accumulation order equals csr.cpp:116-121 and results are bitwise equal.
+//  * Vectors: FP64, blocks column-major with leading dimension `ld`
+//    (>= n_local + n_ghost, multiple of 32); ghost slots trail the owned rows
+//    of every SpMV operand so the halo lands in place.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace csg {
+
+constexpr int kSliceRows = 32;
+constexpr int kMaxS = 64;  // kSmallDenseMax, block.hpp:35
+
+// Error word: (code << 32) | payload, first writer wins (atomicCAS from 0).
+struct DevState {
+  int k;             // current outer iteration (1-based once the loop runs)
+  int done;          // nonzero: every solve kernel returns immediately
+  int converged;
+  int outer_iters;
+  unsigned long long err;      // final error
+  unsigned long long pending;  // fast mode: basis breakdown seen in a speculative MPK
+  int n_rel, n_da, n_db;
+  int pad_;
+  double bnorm;
+  double rho;        // classical PCG
+  double scal[8];    // small scalars (classical PCG step, beta ...)
+};
+
+struct SellView {
+  int64_t n_local;
+  int64_t nslices;
+  const int64_t* __restrict__ slice_ptr;
+  const double* __restrict__ vals;
+  const int32_t* __restrict__ cols;
+  const double* __restrict__ inv_diag;  // nullptr for identity
+};
+
+__host__ __device__ inline unsigned long long make_err(int code, int payload) {
+  return (static_cast<unsigned long long>(static_cast<unsigned>(code)) << 32) |
+         static_cast<unsigned>(payload);
+}
+
+#define CS_CUDA(call)                                                      \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) throw ::csg::CudaError(e_, #call, __FILE__, __LINE__); \
+  } while (0)
+
+struct CudaError {
+  cudaError_t err;
+  std::string what;
+  CudaError(cudaError_t e, const char* call, const char* file, int line)
+      : err(e),
+        what(std::string(cudaGetErrorString(e)) + " in " + call + " at " + file + ":" +
+             std::to_string(line)) {}
+};
+
+// Library error carrying a CS_* code (thrown inside, mapped at the C-ABI).
+struct LibError {
+  int code;
+  int payload;
+  std::string msg;
+};
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace csg

@@ -1,0 +1,138 @@
+// kernels.cuh -- host launchers of every device kernel (internal interface).
+#pragma once
+#include "common.cuh"
+
+namespace csg {
+
+// ------------------------------------------------------------------ problems (sell.cu)
+struct StencilDesc {
+  int kind;  // CS_GEN_*
+  int64_t nx, ny, nz;
+  int64_t z0, z1;  // owned z-planes [z0, z1)
+  double cx, cy, cz;
+};
+// Per-slice widths of a generated slab (analytic row lengths), then fill.
+void launch_stencil_widths(const StencilDesc& d, int64_t n_local, int64_t nslices, int64_t* widths,
+                           cudaStream_t st);
+void launch_stencil_fill(const StencilDesc& d, int64_t n_local, int64_t nslices,
+                         const int64_t* slice_ptr, double* vals, int32_t* cols, double* diag,
+                         cudaStream_t st);
+// exclusive scan of widths*32 -> slice_ptr[0..nslices]
+void scan_slice_ptr(const int64_t* widths, int64_t nslices, int64_t* slice_ptr, void* tmp,
+                    size_t* tmp_bytes, cudaStream_t st);
+// CSR (device, int64) -> SELL-32; validates offsets and column range into *bad.
+void launch_csr_widths(int64_t n, const int64_t* rowptr, int64_t nslices, int64_t* widths,
+                       int* bad, cudaStream_t st);
+void launch_csr_fill(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                     int64_t nslices, const int64_t* slice_ptr, double* vals, int32_t* cols,
+                     double* diag, int* bad, cudaStream_t st);
+// SELL -> CSR row lengths and fill (global columns via row_begin / ghost map)
+void launch_sell_row_len(const SellView& a, int64_t* len, cudaStream_t st);
+void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* ghost_global,
+                        const int64_t* rowptr, int64_t* col, double* val, cudaStream_t st);
+void scan_rowptr(const int64_t* len, int64_t n, int64_t* rowptr, void* tmp, size_t* tmp_bytes,
+                 cudaStream_t st);
+// inv_diag[i] = 1/diag[i]; *bad = 1 if any diag <= 0 (precond.cpp:17-22)
+void launch_inv_diag(int64_t n, const double* diag, double* inv_diag, int* bad, cudaStream_t st);
+
+// ------------------------------------------------------------------ SpMV family (spmv.cu)
+enum SpmvKind { kPlain = 0, kResid = 1, kMpkFirst = 2, kMpkMid = 3, kMpkLast = 4, kDot = 5 };
+struct SpmvArgs {
+  const double* x = nullptr;   // operand (owned + ghost slots)
+  double* y = nullptr;         // A x (p column, r, ...)
+  const double* b = nullptr;   // kResid: y = b - A x
+  const double* zp1 = nullptr; // zp_{q-1}
+  const double* zp2 = nullptr; // zp_{q-2}
+  double* zpout = nullptr;     // zp_q (Jacobi only)
+  double* zout = nullptr;      // z_q = M^-1 zp_q
+  double ca = 0, cb = 0, cc = 0;
+  int col = 0;                 // basis column for the breakdown payload
+  int pending = 0;             // record breakdown in st->pending instead of st->err
+  DevState* st = nullptr;
+  double* partial = nullptr;   // kDot: per-block partials of x.y
+  unsigned* ticket = nullptr;  // kDot: last-block finalisation
+  double* result = nullptr;    // kDot: finalised sum
+};
+void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t slice_begin,
+                 int64_t slice_end, cudaStream_t st);
+int spmv_dot_blocks(int64_t nslices);
+
+// ------------------------------------------------------------------ vector kernels (vec.cu)
+void launch_precond_apply(int64_t n, const double* inv_diag, const double* in, double* out,
+                          DevState* st, int col, int pending, cudaStream_t s);
+void launch_random_vector(int64_t n, int64_t offset, uint64_t seed, double* out, cudaStream_t s);
+// serial ascending-order Gram: g[i + j*ku] = sum_l u_i[l] v_j[l]; one thread per entry.
+void launch_serial_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, const double* v,
+                        int64_t ldv, double* g, DevState* st, cudaStream_t s);
+// deterministic block-tree Gram (generic, any ku/kv <= 64), finalised by the last block.
+void launch_tree_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, const double* v,
+                      int64_t ldv, double* g, double* partial, unsigned* ticket, DevState* st,
+                      cudaStream_t s);
+size_t tree_gram_partial_doubles(int64_t n, int ku, int kv);
+// fast packed reduction {Q^T P, Z^T P, Z^T r, Q^T r, r^T r} (2s^2+2s+1 doubles)
+bool pack_supported(int s);
+void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
+                 const double* r, double* packed, double* partial, unsigned* ticket,
+                 DevState* st, cudaStream_t strm);
+size_t pack_partial_doubles(int s, int64_t n);
+// x/r/Q/AQ updates
+struct UpdateArgs {
+  int s;
+  int64_t n, ld;
+  double* q;             // Q block (in place)
+  double* aq;            // AQ block (in place)
+  const double* z;       // Z block (beta path); z column 0 is overwritten with M^-1 r (fast)
+  double* zw;            // where to write M^-1 r (fast), nullptr = skip
+  const double* p;       // P block = A Z columns 1..s
+  double* x;
+  double* r;
+  const double* inv_diag;  // nullptr = identity
+  const double* alpha;   // device s
+  const double* beta;    // device s x s, nullptr = no block update
+  DevState* st;
+};
+void launch_fast_update(const UpdateArgs& a, cudaStream_t s);  // beta block update + x/r + z0
+void launch_ref_xr_update(const UpdateArgs& a, cudaStream_t s);   // solver.cpp:159-162
+void launch_ref_block_update(const UpdateArgs& a, cudaStream_t s);  // dense_ops.cpp:29-42 x2
+// generic block_update (unit entry)
+void launch_block_update(int64_t n, int m, int k, const double* y, const double* x,
+                         const double* c, double* out, cudaStream_t s);
+void launch_axpby_pcg(int which, int64_t n, double* x, double* r, double* p, const double* q,
+                      const double* inv_diag, DevState* st, double* partial, unsigned* ticket,
+                      double* result, int serial, cudaStream_t s);
+// lanczos helpers
+void launch_scale2(int64_t n, double* v, double* g, const double* src_v, const double* src_g,
+                   const double* denom, DevState* st, cudaStream_t s);
+
+// ------------------------------------------------------------------ small single-CTA kernels (small.cu)
+struct SmallArgs {
+  int s;
+  int nu;
+  int gram;        // CS_GRAM_*
+  int max_outer;
+  double tol;
+  DevState* st;
+  double* W;       // s x s symmetric Gram (persistent)
+  double* alpha;   // s
+  double* beta;    // s x s
+  double* raw;     // reference mode: raw products (W, b1, b2, rr) / fast: packed block
+  double* rel;     // history arrays
+  double* da;
+  double* db;
+};
+void launch_fast_setup(const SmallArgs& a, cudaStream_t s);   // W_1, alpha_1 from packed
+void launch_fast_step(const SmallArgs& a, cudaStream_t s);    // stop test, beta, recurrence, alpha
+void launch_ref_alpha(const SmallArgs& a, cudaStream_t s);    // symmetrise W, alpha solve
+void launch_ref_test(const SmallArgs& a, cudaStream_t s);     // rel residual + stop test
+void launch_ref_beta(const SmallArgs& a, cudaStream_t s);     // beta solve, k++
+void launch_unit_fgs(int s, const double* w, int k, const double* rhs, int nu, double* x,
+                     double* delta, int* status, cudaStream_t st);
+void launch_unit_chol(int s, const double* w, int k, const double* rhs, double* x, int* status,
+                      cudaStream_t st);
+void launch_unit_assemble(int k, double* w, int* status, cudaStream_t st);
+// classical PCG scalar steps
+void launch_pcg_scalar(int which, double tol, int max_iter, DevState* st, const double* dots,
+                       double* rel, cudaStream_t s);
+void launch_set_state(DevState* st, double bnorm, int k, cudaStream_t s);
+
+}  // namespace csg

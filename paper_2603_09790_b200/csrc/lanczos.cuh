@@ -1,0 +1,32 @@
+// lanczos.cuh -- device scalars and launchers of the spectrum estimate.
+#pragma once
+#include "common.cuh"
+
+namespace csg {
+
+constexpr int kLanczosMax = 256;  // steps cap (reference default 40)
+
+struct LanczosScalars {
+  double alpha[kLanczosMax];
+  double beta[kLanczosMax];
+  double proj[kLanczosMax];
+  double dot;    // last reduced scalar
+  double denom;  // normaliser of the next basis pair
+  int count;     // completed alpha entries
+};
+
+void lz_resid(int64_t n, const double* t, const double* inv_diag, const double* vj,
+              const double* gj, const double* vp, const double* gp, double* r, double* gr,
+              const LanczosScalars* sc, int j, DevState* st, cudaStream_t s);
+void lz_axpy2(int64_t n, const double* v, const double* g, double* r, double* gr,
+              const double* proj, DevState* st, cudaStream_t s);
+int lz_cgs_blocks(int64_t n);
+void lz_cgs(int64_t n, int64_t ld, int m, const double* V, const double* G, double* r, double* gr,
+            const double* proj, double* partial, unsigned* ticket, double* result, DevState* st,
+            cudaStream_t s);
+void lz_scalar(int which, int j, int steps, LanczosScalars* sc, DevState* st, cudaStream_t s);
+
+// host: eigenvalues of the symmetric tridiagonal (d[m], e[m-1]) ascending
+void tridiag_eigenvalues(int m, const double* d, const double* e, double* out);
+
+}  // namespace csg

@@ -1,0 +1,423 @@
+// runtime.cu -- device context, device-resident problems, halo exchange,
+// collectives and launch/timing accounting.
+#include <algorithm>
+#include <cstring>
+
+#include "runtime.cuh"
+
+namespace csg {
+
+[[noreturn]] void fail(int code, int payload, const std::string& msg) {
+  throw LibError{code, payload, msg};
+}
+
+#define CS_NCCL(call)                                                                   \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      ::csg::fail(CS_ERR_NCCL, 0, std::string("NCCL: ") + ncclGetErrorString(r_) + " in " #call); \
+  } while (0)
+
+// ------------------------------------------------------------------ accounting
+
+cudaEvent_t pooled_event(cs_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CS_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+Launch::Launch(cs_ctx* ctx, int ph) : c(ctx), phase(ph) {
+  ++c->launches;
+  ++c->phase_launches[ph];
+  if (c->timing) {
+    a = pooled_event(c);
+    CS_CUDA(cudaEventRecord(a, c->stream));
+  }
+}
+
+Launch::~Launch() {
+  if (c->timing && a != nullptr) {
+    cudaEvent_t b = pooled_event(c);
+    cudaEventRecord(b, c->stream);
+    c->spans.push_back({phase, a, b});
+  }
+}
+
+void collect_timing(cs_ctx* c) {
+  if (c->spans.empty()) return;
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  for (const auto& s : c->spans) {
+    float ms = 0.f;
+    CS_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
+    c->phase_ms[s.phase] += ms;
+    c->event_pool.push_back(s.a);
+    c->event_pool.push_back(s.b);
+  }
+  c->spans.clear();
+}
+
+void* ctx_scratch(cs_ctx* c, size_t bytes) {
+  if (c->scratch_bytes < bytes) {
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    c->scratch.alloc(bytes);
+    c->scratch_bytes = bytes;
+  }
+  return c->scratch.p;
+}
+
+// ------------------------------------------------------------------ communication
+
+void halo_exchange_on(cs_problem* p, double* col, cudaStream_t st) {
+  cs_ctx* c = p->ctx;
+  CS_NCCL(ncclGroupStart());
+  if (p->ghost_lo > 0) {
+    CS_NCCL(ncclRecv(col + p->n_local, p->ghost_lo, ncclDouble, c->rank - 1, c->comm, st));
+    CS_NCCL(ncclSend(col, p->send_lo, ncclDouble, c->rank - 1, c->comm, st));
+  }
+  if (p->ghost_hi > 0) {
+    CS_NCCL(ncclRecv(col + p->n_local + p->ghost_lo, p->ghost_hi, ncclDouble, c->rank + 1,
+                     c->comm, st));
+    CS_NCCL(ncclSend(col + p->n_local - p->send_hi, p->send_hi, ncclDouble, c->rank + 1, c->comm,
+                     st));
+  }
+  CS_NCCL(ncclGroupEnd());
+}
+
+void halo_exchange(cs_problem* p, double* col) {
+  cs_ctx* c = p->ctx;
+  if (c->nranks == 1 || (p->ghost_lo == 0 && p->ghost_hi == 0)) return;
+  Launch L(c, CS_PHASE_COMM);
+  halo_exchange_on(p, col, c->stream);
+}
+
+void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand) {
+  cs_ctx* c = p->ctx;
+  const SellView A = p->view();
+  const bool halo = c->nranks > 1 && (p->ghost_lo > 0 || p->ghost_hi > 0);
+  const bool overlap = halo && kind != kDot && p->slice_int_end > p->slice_int_begin;
+  if (!overlap) {
+    if (halo) halo_exchange(p, operand);
+    Launch L(c, CS_PHASE_SPMV);
+    launch_spmv(kind, A, g, 0, p->nslices, c->stream);
+    return;
+  }
+  // halo on the comm stream, interior slices meanwhile, then the boundary
+  CS_CUDA(cudaEventRecord(c->ev_ready, c->stream));
+  CS_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  ++c->launches;
+  ++c->phase_launches[CS_PHASE_COMM];
+  halo_exchange_on(p, operand, c->comm_stream);
+  CS_CUDA(cudaEventRecord(c->ev_halo, c->comm_stream));
+  {
+    Launch L(c, CS_PHASE_SPMV);
+    launch_spmv(kind, A, g, p->slice_int_begin, p->slice_int_end, c->stream);
+  }
+  CS_CUDA(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+  {
+    Launch L(c, CS_PHASE_SPMV);
+    launch_spmv(kind, A, g, 0, p->slice_int_begin, c->stream);
+    launch_spmv(kind, A, g, p->slice_int_end, p->nslices, c->stream);
+  }
+}
+
+void allreduce_sum(cs_ctx* c, double* dev, size_t count) {
+  ++c->allreduces;
+  if (c->nranks == 1) return;
+  Launch L(c, CS_PHASE_COMM);
+  CS_NCCL(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, c->comm, c->stream));
+}
+
+std::string format_device_error(unsigned long long word, int) {
+  const int code = static_cast<int>((word >> 32) & 0xff);
+  const int sub = static_cast<int>((word >> 40) & 0xff);
+  const int payload = static_cast<int>(word & 0xffffffffu);
+  const std::string k = std::to_string(payload);
+  switch (code) {
+    case CS_ERR_BASIS_BREAKDOWN:
+      return "mpk: non-finite basis column " + std::to_string(payload + 1);
+    case CS_ERR_SOLVER_BREAKDOWN:
+      if (sub == 1)
+        return "Gram assembly degenerate at outer iteration " + k +
+               ": gram: non-positive diagonal (basis degeneracy)";
+      if (sub == 2) return "gram solve failed at outer iteration " + k + ": fgs: zero diagonal";
+      if (sub == 3)
+        return "gram solve failed at outer iteration " + k +
+               ": cholesky: non-positive pivot (basis breakdown)";
+      return "pcg: non-positive curvature at iteration " + k;
+    case CS_ERR_GENERIC:
+      if (sub == 1) return "estimate_interval: degenerate start vector";
+      return "estimate_interval: non-finite value";
+    default:
+      return "device error";
+  }
+}
+
+}  // namespace csg
+
+using namespace csg;
+
+// ------------------------------------------------------------------ context (C++ side of the ABI)
+
+namespace csg {
+
+cs_ctx* ctx_create(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    fail(CS_ERR_CUDA, 0, "no CUDA device available (libchebstep_gpu has no CPU fallback)");
+  if (device < 0 || device >= count) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad device ordinal");
+  CS_CUDA(cudaSetDevice(device));
+  auto c = std::make_unique<cs_ctx>();
+  c->device = device;
+  CS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CS_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  CS_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  CS_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  c->state.alloc(sizeof(DevState));
+  CS_CUDA(cudaMallocHost(&c->pinned, 4096));
+  return c.release();
+}
+
+void ctx_destroy(cs_ctx* c) {
+  if (c == nullptr) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& s : c->spans) {
+    cudaEventDestroy(s.a);
+    cudaEventDestroy(s.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  cudaEventDestroy(c->ev_ready);
+  cudaEventDestroy(c->ev_halo);
+  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->comm_stream);
+  cudaFreeHost(c->pinned);
+  delete c;
+}
+
+void comm_init(cs_ctx* c, int nranks, int rank, const unsigned char id[128]) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad rank");
+  CS_CUDA(cudaSetDevice(c->device));
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks == 1) return;
+  ncclUniqueId uid;
+  static_assert(sizeof(uid.internal) == 128, "nccl id size");
+  std::memcpy(uid.internal, id, 128);
+  CS_NCCL(ncclCommInitRank(&c->comm, nranks, uid, rank));
+}
+
+// ------------------------------------------------------------------ problems
+
+namespace {
+
+int64_t stencil_nnz_planes(int kind, int64_t nx, int64_t ny, int64_t nz, int64_t z0, int64_t z1) {
+  int64_t total = 0;
+  for (int64_t z = z0; z < z1; ++z) {
+    const int64_t cz = 1 + (z > 0) + (z + 1 < nz);
+    if (kind == CS_GEN_POISSON27) {
+      const int64_t fx = nx > 1 ? 3 * nx - 2 : 1, fy = ny > 1 ? 3 * ny - 2 : 1;
+      total += fx * fy * cz;
+    } else {
+      total += nx * ny * cz + 2 * ((nx - 1) * ny + nx * (ny - 1));
+    }
+  }
+  return total;
+}
+
+void finish_sell(cs_problem* p, int64_t* widths_dev) {
+  cs_ctx* c = p->ctx;
+  size_t tmp_bytes = 0;
+  scan_slice_ptr(widths_dev, p->nslices, p->slice_ptr.as<int64_t>(), nullptr, &tmp_bytes,
+                 c->stream);
+  DBuf tmp(tmp_bytes);
+  scan_slice_ptr(widths_dev, p->nslices, p->slice_ptr.as<int64_t>(), tmp.p, &tmp_bytes, c->stream);
+}
+
+int64_t read_i64(cs_ctx* c, const int64_t* dev) {
+  int64_t v = 0;
+  CS_CUDA(cudaMemcpyAsync(&v, dev, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  return v;
+}
+
+}  // namespace
+
+cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
+                             const double* coef) {
+  if (kind != CS_GEN_POISSON27 && kind != CS_GEN_STENCIL7)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "unknown generator kind");
+  if (nx < 1 || ny < 1 || nz < 1)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "poisson27: grid dimensions must be >= 1");
+  constexpr int64_t kMaxN = int64_t{1} << 31;  // problems.cpp:18-20
+  if (nx > kMaxN / ny || nx * ny > kMaxN / nz)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "poisson27: grid size overflow");
+  CS_CUDA(cudaSetDevice(c->device));
+  auto p = std::make_unique<cs_problem>();
+  p->ctx = c;
+  p->gen_kind = kind;
+  p->nx = nx, p->ny = ny, p->nz = nz;
+  const int64_t plane = nx * ny;
+  int64_t r0 = 0, r1 = plane * nz;
+  if (c->nranks > 1) {
+    if (cs_partition_rows(plane * nz, plane, c->nranks, c->rank, &r0, &r1) != CS_OK)
+      fail(CS_ERR_INVALID_ARGUMENT, 0, "grid has fewer z-planes than ranks");
+  }
+  StencilDesc d{kind, nx, ny, nz, r0 / plane, r1 / plane, 1.0, 1.0, 1.0};
+  if (coef != nullptr) d.cx = coef[0], d.cy = coef[1], d.cz = coef[2];
+  p->n_global = plane * nz;
+  p->row_begin = r0;
+  p->n_local = r1 - r0;
+  p->ghost_lo = d.z0 > 0 ? plane : 0;
+  p->ghost_hi = d.z1 < nz ? plane : 0;
+  p->send_lo = p->ghost_lo;
+  p->send_hi = p->ghost_hi;
+  p->n_ghost = p->ghost_lo + p->ghost_hi;
+  if (p->n_local + p->n_ghost >= (int64_t{1} << 31))
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "rank block exceeds int32 column range");
+  p->ld = round_up(p->n_local + p->n_ghost, 32);
+  p->nslices = (p->n_local + kSliceRows - 1) / kSliceRows;
+  p->nnz_local = stencil_nnz_planes(kind, nx, ny, nz, d.z0, d.z1);
+  // interior slices: rows whose stencils stay inside the owned planes
+  p->slice_int_begin = p->ghost_lo ? (plane + kSliceRows - 1) / kSliceRows : 0;
+  p->slice_int_end = p->ghost_hi ? (p->n_local - plane) / kSliceRows : p->nslices;
+  if (p->slice_int_end < p->slice_int_begin) p->slice_int_begin = p->slice_int_end = 0;
+
+  p->slice_ptr.alloc(sizeof(int64_t) * (p->nslices + 1));
+  {
+    DBuf widths(sizeof(int64_t) * p->nslices);
+    launch_stencil_widths(d, p->n_local, p->nslices, widths.as<int64_t>(), c->stream);
+    finish_sell(p.get(), widths.as<int64_t>());
+  }
+  const int64_t total = read_i64(c, p->slice_ptr.as<int64_t>() + p->nslices);
+  p->vals.alloc(sizeof(double) * total);
+  p->cols.alloc(sizeof(int32_t) * total);
+  p->diag.alloc(sizeof(double) * std::max<int64_t>(p->n_local, 1));
+  launch_stencil_fill(d, p->n_local, p->nslices, p->slice_ptr.as<int64_t>(), p->vals.as<double>(),
+                      p->cols.as<int32_t>(), p->diag.as<double>(), c->stream);
+  // ghost global ids: plane z0-1 then plane z1
+  for (int64_t i = 0; i < p->ghost_lo; ++i) p->ghosts_host.push_back(r0 - plane + i);
+  for (int64_t i = 0; i < p->ghost_hi; ++i) p->ghosts_host.push_back(r1 + i);
+  p->ghost_global.alloc(sizeof(int64_t) * std::max<int64_t>(p->n_ghost, 1));
+  if (p->n_ghost)
+    CS_CUDA(cudaMemcpyAsync(p->ghost_global.p, p->ghosts_host.data(), sizeof(int64_t) * p->n_ghost,
+                            cudaMemcpyHostToDevice, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  return p.release();
+}
+
+cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, const int64_t* col,
+                               const double* val) {
+  if (c->nranks > 1)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "CSR upload is single-rank; use generated problems for P>1");
+  if (n < 0) fail(CS_ERR_DIMENSION, 0, "negative dimension");
+  if (n >= (int64_t{1} << 31)) fail(CS_ERR_INVALID_ARGUMENT, 0, "n exceeds int32 column range");
+  if (rowptr[0] != 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[0] must be 0");
+  const int64_t nnz = rowptr[n];
+  if (nnz < 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[n] must equal nnz");
+  CS_CUDA(cudaSetDevice(c->device));
+  auto p = std::make_unique<cs_problem>();
+  p->ctx = c;
+  p->n_global = p->n_local = n;
+  p->ld = round_up(std::max<int64_t>(n, 1), 32);
+  p->nslices = (n + kSliceRows - 1) / kSliceRows;
+  p->nnz_local = nnz;
+  p->slice_int_begin = 0;
+  p->slice_int_end = p->nslices;
+  DBuf drp(sizeof(int64_t) * (n + 1)), dcol(sizeof(int64_t) * std::max<int64_t>(nnz, 1)),
+      dval(sizeof(double) * std::max<int64_t>(nnz, 1)), bad(sizeof(int));
+  CS_CUDA(cudaMemcpyAsync(drp.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice,
+                          c->stream));
+  if (nnz) {
+    CS_CUDA(cudaMemcpyAsync(dcol.p, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, c->stream));
+    CS_CUDA(cudaMemcpyAsync(dval.p, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
+  }
+  CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  p->slice_ptr.alloc(sizeof(int64_t) * (p->nslices + 1));
+  if (p->nslices > 0) {
+    DBuf widths(sizeof(int64_t) * p->nslices);
+    launch_csr_widths(n, drp.as<int64_t>(), p->nslices, widths.as<int64_t>(), bad.as<int>(),
+                      c->stream);
+    finish_sell(p.get(), widths.as<int64_t>());
+  } else {
+    CS_CUDA(cudaMemsetAsync(p->slice_ptr.p, 0, sizeof(int64_t), c->stream));
+  }
+  int hbad = 0;
+  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  const int64_t total = read_i64(c, p->slice_ptr.as<int64_t>() + p->nslices);
+  if (hbad) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets must be nondecreasing");
+  p->vals.alloc(sizeof(double) * std::max<int64_t>(total, 1));
+  p->cols.alloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
+  p->diag.alloc(sizeof(double) * std::max<int64_t>(n, 1));
+  if (p->nslices > 0)
+    launch_csr_fill(n, drp.as<int64_t>(), dcol.as<int64_t>(), dval.as<double>(), p->nslices,
+                    p->slice_ptr.as<int64_t>(), p->vals.as<double>(), p->cols.as<int32_t>(),
+                    p->diag.as<double>(), bad.as<int>(), c->stream);
+  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  if (hbad) fail(CS_ERR_INVALID_MATRIX, 0, "column index out of range");
+  p->ghost_global.alloc(8);
+  return p.release();
+}
+
+void problem_set_precond(cs_problem* p, int kind) {
+  cs_ctx* c = p->ctx;
+  CS_CUDA(cudaSetDevice(c->device));
+  if (kind == CS_PRECOND_IDENTITY) {
+    p->precond = kind;
+    return;
+  }
+  if (kind != CS_PRECOND_JACOBI) fail(CS_ERR_INVALID_ARGUMENT, 0, "unknown preconditioner");
+  if (!p->inv_diag.p) p->inv_diag.alloc(sizeof(double) * std::max<int64_t>(p->n_local, 1));
+  DBuf bad(sizeof(int));
+  CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  {
+    Launch L(c, CS_PHASE_OTHER);
+    launch_inv_diag(p->n_local, p->diag.as<double>(), p->inv_diag.as<double>(), bad.as<int>(),
+                    c->stream);
+  }
+  int hbad = 0;
+  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  if (hbad) fail(CS_ERR_NOT_SPD, 0, "jacobi: diagonal must be strictly positive");
+  p->precond = kind;
+}
+
+void problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val) {
+  cs_ctx* c = p->ctx;
+  CS_CUDA(cudaSetDevice(c->device));
+  const int64_t n = p->n_local;
+  DBuf len(sizeof(int64_t) * std::max<int64_t>(n, 1)), rp(sizeof(int64_t) * (n + 1));
+  const SellView A = p->view();
+  if (n > 0) {
+    launch_sell_row_len(A, len.as<int64_t>(), c->stream);
+    size_t tb = 0;
+    scan_rowptr(len.as<int64_t>(), n, rp.as<int64_t>(), nullptr, &tb, c->stream);
+    DBuf tmp(tb);
+    scan_rowptr(len.as<int64_t>(), n, rp.as<int64_t>(), tmp.p, &tb, c->stream);
+  } else {
+    CS_CUDA(cudaMemsetAsync(rp.p, 0, sizeof(int64_t), c->stream));
+  }
+  const int64_t nnz = read_i64(c, rp.as<int64_t>() + n);
+  DBuf dc(sizeof(int64_t) * std::max<int64_t>(nnz, 1)), dv(sizeof(double) * std::max<int64_t>(nnz, 1));
+  if (n > 0)
+    launch_sell_to_csr(A, p->row_begin, p->ghost_global.as<int64_t>(), rp.as<int64_t>(),
+                       dc.as<int64_t>(), dv.as<double>(), c->stream);
+  CS_CUDA(cudaMemcpyAsync(rowptr, rp.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (nnz) {
+    CS_CUDA(cudaMemcpyAsync(col, dc.p, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaMemcpyAsync(val, dv.p, sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace csg

@@ -1,0 +1,146 @@
+// runtime.cuh -- host-side runtime objects behind the C ABI: device context
+// (streams, NCCL communicator, per-phase CUDA-event timing, launch counts),
+// device-resident problems (SELL matrix + preconditioner + halo layout) and
+// the cached per-problem solve workspace.
+#pragma once
+#include <nccl.h>
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "chebstep_gpu.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "lanczos.cuh"
+
+namespace csg {
+
+// RAII device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  explicit DBuf(size_t b) { alloc(b); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, bytes = o.bytes;
+      o.p = nullptr, o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t b) {
+    release();
+    if (b == 0) b = 8;
+    CS_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct TimedSpan {
+  int phase;
+  cudaEvent_t a, b;
+};
+
+}  // namespace csg
+
+struct cs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;       // compute
+  cudaStream_t comm_stream = nullptr;  // halo exchange
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // accounting
+  int64_t launches = 0;
+  std::array<int64_t, CS_NUM_PHASES> phase_launches{};
+  std::array<double, CS_NUM_PHASES> phase_ms{};
+  bool timing = false;
+  std::vector<csg::TimedSpan> spans;
+  std::vector<cudaEvent_t> event_pool;
+  int64_t allreduces = 0;
+  // scratch
+  csg::DBuf state;      // DevState
+  csg::DBuf scratch;    // partials / tickets / scalars
+  size_t scratch_bytes = 0;
+  void* pinned = nullptr;  // pinned host staging for flags
+};
+
+struct cs_problem {
+  cs_ctx* ctx = nullptr;
+  int64_t n_global = 0, row_begin = 0, n_local = 0, n_ghost = 0, ld = 0, nnz_local = 0;
+  int64_t nslices = 0;
+  int64_t slice_int_begin = 0, slice_int_end = 0;  // interior slices (no ghost columns)
+  // halo: ghosts = [lower plane (from rank-1) | upper plane (from rank+1)]
+  int64_t ghost_lo = 0, ghost_hi = 0, send_lo = 0, send_hi = 0;
+  int gen_kind = -1;
+  int64_t nx = 0, ny = 0, nz = 0;
+  csg::DBuf slice_ptr, vals, cols, diag, inv_diag, ghost_global;
+  std::vector<int64_t> ghosts_host;
+  int precond = CS_PRECOND_IDENTITY;
+  // cached solve workspace
+  int ws_s = -1;
+  csg::DBuf ws;
+  csg::SellView view() const {
+    csg::SellView v;
+    v.n_local = n_local;
+    v.nslices = nslices;
+    v.slice_ptr = slice_ptr.as<int64_t>();
+    v.vals = vals.as<double>();
+    v.cols = cols.as<int32_t>();
+    v.inv_diag = precond == CS_PRECOND_JACOBI ? inv_diag.as<double>() : nullptr;
+    return v;
+  }
+};
+
+namespace csg {
+
+// launch accounting + optional CUDA-event timing of every kernel
+struct Launch {
+  cs_ctx* c;
+  int phase;
+  cudaEvent_t a = nullptr;
+  Launch(cs_ctx* ctx, int ph);
+  ~Launch();
+};
+cudaEvent_t pooled_event(cs_ctx* c);
+void collect_timing(cs_ctx* c);
+
+// SpMV with halo exchange (interior rows overlap the transfer)
+void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand_col);
+void halo_exchange(cs_problem* p, double* col);
+void allreduce_sum(cs_ctx* c, double* dev, size_t count);
+// scratch region of the context, grown on demand
+void* ctx_scratch(cs_ctx* c, size_t bytes);
+
+// solver entry points (solver.cu)
+void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, double* lo,
+                           double* hi, double* t_ms);
+void pcgs_solve_dev(cs_problem* p, const double* b, const double* x0, const cs_config& cfg,
+                    double* x, cs_report* rep);
+void mpk_unit(cs_problem* p, double* Z, double* P, double* r, double* zpA, double* zpB, int s,
+              double lo, double hi, DevState* st);
+void pcg_solve_dev(cs_problem* p, const double* b, const double* x0, double tol, int max_iter,
+                   int mode, double* x, cs_report* rep);
+
+// error helpers
+[[noreturn]] void fail(int code, int payload, const std::string& msg);
+std::string format_device_error(unsigned long long word, int s);
+
+}  // namespace csg

@@ -1,0 +1,306 @@
+// sell.cu -- device-side matrix assembly into SELL-32 and the inverse
+// conversions used by the bit-exactness checks.
+//
+//  * Stencil generators write the SELL arrays directly on the device, one
+//    thread per row, with the reference's assembly conventions
+//    (problems.cpp:13-53): x-fastest rows, neighbours visited in
+//    (dz, dy, dx) lexicographic order so columns ascend, diagonal 26 / -1
+//    for the 27-point operator; the 7-point operator follows the same
+//    conventions. Values are exact small integers, so the device
+//    assembly is bitwise the CPU assembly.
+//  * A rank owning z-planes [z0, z1) numbers its rows 0..n_local-1 and the
+//    ghost plane z0-1 (if any) n_local.., then plane z1 (if any); a row's
+//    entries keep ascending GLOBAL column order, so per-row summation order
+//    is partition-invariant.
+//  * CSR -> SELL conversion for uploaded reference CsrMatrix data.
+#include <cub/device/device_scan.cuh>
+
+#include "kernels.cuh"
+
+namespace csg {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int stencil_row_count(const StencilDesc& d, int64_t ix, int64_t iy,
+                                                 int64_t iz) {
+  if (d.kind == 0) {  // 27-point
+    const int cx = 1 + (ix > 0) + (ix + 1 < d.nx);
+    const int cy = 1 + (iy > 0) + (iy + 1 < d.ny);
+    const int cz = 1 + (iz > 0) + (iz + 1 < d.nz);
+    return cx * cy * cz;
+  }
+  return 1 + (ix > 0) + (ix + 1 < d.nx) + (iy > 0) + (iy + 1 < d.ny) + (iz > 0) +
+         (iz + 1 < d.nz);
+}
+
+__global__ void stencil_widths_kernel(StencilDesc d, int64_t n_local, int64_t nslices,
+                                      int64_t* widths) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t slice = row >> 5;
+  if (slice >= nslices) return;
+  int cnt = 0;
+  if (row < n_local) {
+    const int64_t plane = d.nx * d.ny;
+    const int64_t iz = d.z0 + row / plane;
+    const int64_t rem = row % plane;
+    cnt = stencil_row_count(d, rem % d.nx, rem / d.nx, iz);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, off));
+  if ((threadIdx.x & 31) == 0) widths[slice] = static_cast<int64_t>(cnt) * kSliceRows;
+}
+
+// Local index of global grid point (jx, jy, jz) for a rank owning [z0, z1).
+__device__ __forceinline__ int32_t local_col(const StencilDesc& d, int64_t n_local, int64_t jx,
+                                             int64_t jy, int64_t jz) {
+  const int64_t plane = d.nx * d.ny;
+  const int64_t in_plane = jy * d.nx + jx;
+  if (jz >= d.z0 && jz < d.z1) return static_cast<int32_t>((jz - d.z0) * plane + in_plane);
+  const int64_t lo_cnt = d.z0 > 0 ? plane : 0;
+  if (jz < d.z0) return static_cast<int32_t>(n_local + in_plane);
+  return static_cast<int32_t>(n_local + lo_cnt + in_plane);
+}
+
+__global__ void stencil_fill_kernel(StencilDesc d, int64_t n_local, int64_t nslices,
+                                    const int64_t* __restrict__ slice_ptr, double* vals,
+                                    int32_t* cols, double* diag_out) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t slice = row >> 5;
+  if (slice >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = slice_ptr[slice];
+  const int width = static_cast<int>((slice_ptr[slice + 1] - base) >> 5);
+  double* vp = vals + base + lane;
+  int32_t* cp = cols + base + lane;
+  int k = 0;
+  if (row < n_local) {
+    const int64_t plane = d.nx * d.ny;
+    const int64_t iz = d.z0 + row / plane;
+    const int64_t rem = row % plane;
+    const int64_t iy = rem / d.nx, ix = rem % d.nx;
+    double dg = 0.0;
+    if (d.kind == 0) {
+      for (int dz = -1; dz <= 1; ++dz) {
+        const int64_t jz = iz + dz;
+        if (jz < 0 || jz >= d.nz) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int64_t jy = iy + dy;
+          if (jy < 0 || jy >= d.ny) continue;
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int64_t jx = ix + dx;
+            if (jx < 0 || jx >= d.nx) continue;
+            const bool self = (dx == 0 && dy == 0 && dz == 0);
+            cp[k * kSliceRows] = local_col(d, n_local, jx, jy, jz);
+            vp[k * kSliceRows] = self ? 26.0 : -1.0;
+            ++k;
+          }
+        }
+      }
+      dg = 26.0;
+    } else {
+      const double dv = 2.0 * (d.cx + d.cy + d.cz);
+      auto put = [&](int64_t jx, int64_t jy, int64_t jz, double v) {
+        cp[k * kSliceRows] = local_col(d, n_local, jx, jy, jz);
+        vp[k * kSliceRows] = v;
+        ++k;
+      };
+      if (iz > 0) put(ix, iy, iz - 1, -d.cz);
+      if (iy > 0) put(ix, iy - 1, iz, -d.cy);
+      if (ix > 0) put(ix - 1, iy, iz, -d.cx);
+      put(ix, iy, iz, dv);
+      if (ix + 1 < d.nx) put(ix + 1, iy, iz, -d.cx);
+      if (iy + 1 < d.ny) put(ix, iy + 1, iz, -d.cy);
+      if (iz + 1 < d.nz) put(ix, iy, iz + 1, -d.cz);
+      dg = dv;
+    }
+    diag_out[row] = dg;
+  }
+  for (; k < width; ++k) {  // padding slots
+    cp[k * kSliceRows] = -1;
+    vp[k * kSliceRows] = 0.0;
+  }
+}
+
+__global__ void csr_widths_kernel(int64_t n, const int64_t* __restrict__ rowptr, int64_t nslices,
+                                  int64_t* widths, int* bad) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t slice = row >> 5;
+  if (slice >= nslices) return;
+  int64_t len = 0;
+  if (row < n) {
+    len = rowptr[row + 1] - rowptr[row];
+    if (len < 0 || len > (1 << 24)) {
+      atomicExch(bad, 1);
+      len = 0;
+    }
+  }
+  int cnt = static_cast<int>(len);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, off));
+  if ((threadIdx.x & 31) == 0) widths[slice] = static_cast<int64_t>(cnt) * kSliceRows;
+}
+
+// Diagonal exactly as CsrMatrix::diagonal (csr.cpp:10-15): std::lower_bound
+// over the row's stored columns (libstdc++ halving order), 0 when absent.
+__device__ double csr_lower_bound_diag(const int64_t* col, const double* val, int64_t first,
+                                       int64_t last, int64_t i) {
+  int64_t len = last - first;
+  while (len > 0) {
+    const int64_t half = len >> 1;
+    const int64_t mid = first + half;
+    if (col[mid] < i) {
+      first = mid + 1;
+      len = len - half - 1;
+    } else {
+      len = half;
+    }
+  }
+  if (first == last || col[first] != i) return 0.0;
+  return val[first];
+}
+
+__global__ void csr_fill_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                const int64_t* __restrict__ col, const double* __restrict__ val,
+                                int64_t nslices, const int64_t* __restrict__ slice_ptr,
+                                double* vals, int32_t* cols, double* diag_out, int* bad) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t slice = row >> 5;
+  if (slice >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = slice_ptr[slice];
+  const int width = static_cast<int>((slice_ptr[slice + 1] - base) >> 5);
+  double* vp = vals + base + lane;
+  int32_t* cp = cols + base + lane;
+  int k = 0;
+  if (row < n) {
+    const int64_t b = rowptr[row], e = rowptr[row + 1];
+    for (int64_t t = b; t < e; ++t, ++k) {
+      const int64_t c = col[t];
+      if (c < 0 || c >= n) {
+        atomicExch(bad, 2);
+        cp[k * kSliceRows] = -1;
+        vp[k * kSliceRows] = 0.0;
+        continue;
+      }
+      cp[k * kSliceRows] = static_cast<int32_t>(c);
+      vp[k * kSliceRows] = val[t];
+    }
+    diag_out[row] = csr_lower_bound_diag(col, val, b, e, row);
+  }
+  for (; k < width; ++k) {
+    cp[k * kSliceRows] = -1;
+    vp[k * kSliceRows] = 0.0;
+  }
+}
+
+__global__ void sell_row_len_kernel(SellView a, int64_t* len) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= a.n_local) return;
+  const int64_t slice = row >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = a.slice_ptr[slice];
+  const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
+  int cnt = 0;
+  for (int k = 0; k < width; ++k)
+    if (a.cols[base + k * kSliceRows + lane] >= 0) ++cnt;
+  len[row] = cnt;
+}
+
+__global__ void sell_to_csr_kernel(SellView a, int64_t row_begin,
+                                   const int64_t* __restrict__ ghost_global,
+                                   const int64_t* __restrict__ rowptr, int64_t* col,
+                                   double* val) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= a.n_local) return;
+  const int64_t slice = row >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = a.slice_ptr[slice];
+  const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
+  int64_t o = rowptr[row];
+  for (int k = 0; k < width; ++k) {
+    const int32_t c = a.cols[base + k * kSliceRows + lane];
+    if (c < 0) continue;
+    col[o] = c < a.n_local ? row_begin + c : ghost_global[c - a.n_local];
+    val[o] = a.vals[base + k * kSliceRows + lane];
+    ++o;
+  }
+}
+
+__global__ void inv_diag_kernel(int64_t n, const double* __restrict__ diag, double* inv, int* bad) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double d = diag[i];
+  if (!(d > 0.0)) atomicExch(bad, 1);
+  inv[i] = 1.0 / d;  // precond.cpp:22, IEEE division
+}
+
+inline unsigned grid_for(int64_t threads) {
+  return static_cast<unsigned>((threads + kThreads - 1) / kThreads);
+}
+
+}  // namespace
+
+void launch_stencil_widths(const StencilDesc& d, int64_t n_local, int64_t nslices, int64_t* widths,
+                           cudaStream_t st) {
+  stencil_widths_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(d, n_local, nslices, widths);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_stencil_fill(const StencilDesc& d, int64_t n_local, int64_t nslices,
+                         const int64_t* slice_ptr, double* vals, int32_t* cols, double* diag,
+                         cudaStream_t st) {
+  stencil_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(d, n_local, nslices, slice_ptr,
+                                                                   vals, cols, diag);
+  CS_CUDA(cudaGetLastError());
+}
+
+void scan_slice_ptr(const int64_t* widths, int64_t nslices, int64_t* slice_ptr, void* tmp,
+                    size_t* tmp_bytes, cudaStream_t st) {
+  // slice_ptr[0] = 0, slice_ptr[i+1] = sum_{j<=i} widths[j]: inclusive scan into +1
+  if (tmp == nullptr) {
+    CS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, *tmp_bytes, widths, slice_ptr + 1, nslices, st));
+    return;
+  }
+  CS_CUDA(cudaMemsetAsync(slice_ptr, 0, sizeof(int64_t), st));
+  CS_CUDA(cub::DeviceScan::InclusiveSum(tmp, *tmp_bytes, widths, slice_ptr + 1, nslices, st));
+}
+
+void scan_rowptr(const int64_t* len, int64_t n, int64_t* rowptr, void* tmp, size_t* tmp_bytes,
+                 cudaStream_t st) {
+  scan_slice_ptr(len, n, rowptr, tmp, tmp_bytes, st);
+}
+
+void launch_csr_widths(int64_t n, const int64_t* rowptr, int64_t nslices, int64_t* widths,
+                       int* bad, cudaStream_t st) {
+  csr_widths_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(n, rowptr, nslices, widths, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_csr_fill(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                     int64_t nslices, const int64_t* slice_ptr, double* vals, int32_t* cols,
+                     double* diag, int* bad, cudaStream_t st) {
+  csr_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(n, rowptr, col, val, nslices,
+                                                               slice_ptr, vals, cols, diag, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_sell_row_len(const SellView& a, int64_t* len, cudaStream_t st) {
+  sell_row_len_kernel<<<grid_for(a.n_local), kThreads, 0, st>>>(a, len);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* ghost_global,
+                        const int64_t* rowptr, int64_t* col, double* val, cudaStream_t st) {
+  sell_to_csr_kernel<<<grid_for(a.n_local), kThreads, 0, st>>>(a, row_begin, ghost_global, rowptr,
+                                                              col, val);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_inv_diag(int64_t n, const double* diag, double* inv_diag, int* bad, cudaStream_t st) {
+  if (n == 0) return;
+  inv_diag_kernel<<<grid_for(n), kThreads, 0, st>>>(n, diag, inv_diag, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
+}  // namespace csg

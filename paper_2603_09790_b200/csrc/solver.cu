@@ -1,0 +1,728 @@
+// solver.cu -- host orchestration of the device solve path:
+//   pcg_s_solve   (solver.cpp:78-190)  Chebyshev s-step PCG, fast or reference algebra
+//   pcg_solve     (solver.cpp:192-264) classical PCG comparator
+//   estimate_interval (spectral.cpp:60-132) device Lanczos
+// All n-sized work is device kernels; the host only enqueues work and polls
+// an 4-byte convergence flag every `check_every` outer iterations while the
+// next batch is already queued (stop decisions are taken on the device).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.cuh"
+
+namespace csg {
+namespace {
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    CS_CUDA(cudaEventCreate(&a));
+    CS_CUDA(cudaEventCreate(&b));
+    CS_CUDA(cudaEventRecord(a, s));
+  }
+  double stop() {
+    CS_CUDA(cudaEventRecord(b, s));
+    CS_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+DevState read_state(cs_ctx* c) {
+  DevState h;
+  CS_CUDA(cudaMemcpyAsync(&h, c->state.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+void init_state(cs_ctx* c, double bnorm, int k) {
+  DevState h;
+  std::memset(&h, 0, sizeof h);
+  h.bnorm = bnorm;
+  h.k = k;
+  CS_CUDA(cudaMemcpyAsync(c->state.p, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+}
+
+void raise_device_error(const DevState& h, int s) {
+  if (h.err == 0ull) return;
+  const int code = static_cast<int>((h.err >> 32) & 0xff);
+  const int payload = static_cast<int>(h.err & 0xffffffffu);
+  fail(code, payload, format_device_error(h.err, s));
+}
+
+// bump allocator over one device buffer
+struct Arena {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += sizeof(T) * std::max<size_t>(count, 1);
+    return p;
+  }
+};
+
+// global dot product (tree or serial order) into dev[0], then allreduce
+void dot_into(cs_problem* p, const double* u, const double* v, double* dev, int mode,
+              double* partial, unsigned* ticket, DevState* st) {
+  cs_ctx* c = p->ctx;
+  {
+    Launch L(c, CS_PHASE_REDUCE);
+    if (mode == CS_MODE_REFERENCE)
+      launch_serial_gram(p->n_local, 1, 1, u, p->ld, v, p->ld, dev, st, c->stream);
+    else
+      launch_tree_gram(p->n_local, 1, 1, u, p->ld, v, p->ld, dev, partial, ticket, st, c->stream);
+  }
+  allreduce_sum(c, dev, 1);
+}
+
+double host_norm(cs_problem* p, const double* v, int mode) {
+  cs_ctx* c = p->ctx;
+  DBuf tmp(sizeof(double) * (tree_gram_partial_doubles(p->n_local, 1, 1) + 64));
+  Arena ar{tmp.as<char>()};
+  double* d = ar.take<double>(1);
+  unsigned* ticket = ar.take<unsigned>(1);
+  double* partial = ar.take<double>(tree_gram_partial_doubles(p->n_local, 1, 1));
+  CS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), c->stream));
+  dot_into(p, v, v, d, mode, partial, ticket, nullptr);
+  double h = 0;
+  CS_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  return std::sqrt(h);
+}
+
+}  // namespace
+
+// ====================================================================== Lanczos
+
+void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, double* lo,
+                           double* hi, double* t_ms) {
+  cs_ctx* c = p->ctx;
+  if (steps < 2) fail(CS_ERR_INVALID_ARGUMENT, 0, "estimate_interval: steps >= 2");
+  if (steps > kLanczosMax) fail(CS_ERR_INVALID_ARGUMENT, 0, "estimate_interval: steps > 256");
+  if (mode == CS_MODE_REFERENCE && c->nranks > 1)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "reference mode is single-GPU");
+  CS_CUDA(cudaSetDevice(c->device));
+  const int64_t n = p->n_local, ld = p->ld;
+  DBuf work(sizeof(double) * (static_cast<size_t>(2 * steps + 3) * ld));
+  double* V = work.as<double>();
+  double* G = V + steps * ld;
+  double* t = G + steps * ld;
+  double* r = t + ld;
+  double* gr = r + ld;
+  const size_t tree_part = tree_gram_partial_doubles(n, steps, 1);
+  const size_t part = std::max<size_t>(tree_part, static_cast<size_t>(lz_cgs_blocks(n)) + 16);
+  char* scr = static_cast<char*>(ctx_scratch(
+      c, sizeof(LanczosScalars) + sizeof(double) * (part + spmv_dot_blocks(p->nslices)) + 4096));
+  Arena ar{scr};
+  LanczosScalars* sc = ar.take<LanczosScalars>(1);
+  double* partial = ar.take<double>(part + spmv_dot_blocks(p->nslices));
+  unsigned* ticket = ar.take<unsigned>(4);
+  CS_CUDA(cudaMemsetAsync(sc, 0, sizeof(LanczosScalars), c->stream));
+  CS_CUDA(cudaMemsetAsync(ticket, 0, 4 * sizeof(unsigned), c->stream));
+  init_state(c, 0.0, 0);
+  DevState* st = c->state.as<DevState>();
+  const double* inv = p->view().inv_diag;
+  Timer timer(c->stream);
+  auto L = [&]() { return Launch(c, CS_PHASE_LANCZOS); };
+
+  // start: g = random_vector(n, seed); v = M^-1 g; normalise by sqrt(v.g)  (spectral.cpp:72-83)
+  {
+    auto l = L();
+    launch_random_vector(n, p->row_begin, seed, G, c->stream);
+  }
+  {
+    auto l = L();
+    launch_precond_apply(n, inv, G, V, nullptr, -1, 0, c->stream);
+  }
+  auto reduce_dot = [&](const double* u, const double* v) {
+    auto l = L();
+    if (mode == CS_MODE_REFERENCE)
+      launch_serial_gram(n, 1, 1, u, ld, v, ld, &sc->dot, st, c->stream);
+    else
+      launch_tree_gram(n, 1, 1, u, ld, v, ld, &sc->dot, partial, ticket, st, c->stream);
+  };
+  reduce_dot(V, G);
+  allreduce_sum(c, &sc->dot, 1);
+  {
+    auto l = L();
+    lz_scalar(0, 0, steps, sc, st, c->stream);
+  }
+  {
+    auto l = L();
+    launch_scale2(n, V, G, V, G, &sc->denom, st, c->stream);
+  }
+  for (int j = 0; j < steps; ++j) {
+    double* vj = V + j * ld;
+    double* gj = G + j * ld;
+    SpmvArgs g;
+    g.x = vj;
+    g.y = t;
+    g.st = st;
+    if (mode == CS_MODE_REFERENCE) {
+      spmv_halo(p, kPlain, g, vj);
+      reduce_dot(vj, t);
+    } else {
+      g.partial = partial;
+      g.ticket = ticket + 1;
+      g.result = &sc->dot;
+      spmv_halo(p, kDot, g, vj);
+    }
+    allreduce_sum(c, &sc->dot, 1);
+    {
+      auto l = L();
+      lz_scalar(1, j, steps, sc, st, c->stream);
+    }
+    {
+      auto l = L();
+      lz_resid(n, t, inv, vj, gj, j > 0 ? vj - ld : nullptr, j > 0 ? gj - ld : nullptr, r, gr, sc,
+               j, st, c->stream);
+    }
+    if (mode == CS_MODE_REFERENCE) {
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, spectral.cpp:104-108
+        {
+          auto l = L();
+          launch_serial_gram(n, 1, 1, G + i * ld, ld, r, ld, &sc->proj[0], st, c->stream);
+        }
+        auto l = L();
+        lz_axpy2(n, V + i * ld, G + i * ld, r, gr, &sc->proj[0], st, c->stream);
+      }
+      reduce_dot(r, gr);
+    } else {
+      {  // classical Gram-Schmidt: all projections in one pass
+        auto l = L();
+        launch_tree_gram(n, j + 1, 1, G, ld, r, ld, sc->proj, partial, ticket + 2, st, c->stream);
+      }
+      allreduce_sum(c, sc->proj, j + 1);
+      auto l = L();
+      lz_cgs(n, ld, j + 1, V, G, r, gr, sc->proj, partial, ticket + 3, &sc->dot, st, c->stream);
+    }
+    allreduce_sum(c, &sc->dot, 1);
+    {
+      auto l = L();
+      lz_scalar(2, j, steps, sc, st, c->stream);
+    }
+    if (j + 1 < steps) {
+      auto l = L();
+      launch_scale2(n, vj + ld, gj + ld, r, gr, &sc->denom, st, c->stream);
+    }
+  }
+  const double ms = timer.stop();
+  if (t_ms) *t_ms = ms;
+  collect_timing(c);
+  const DevState h = read_state(c);
+  raise_device_error(h, 0);
+  LanczosScalars hs;
+  CS_CUDA(cudaMemcpy(&hs, sc, sizeof hs, cudaMemcpyDeviceToHost));
+  const int m = hs.count;
+  if (m < 1) fail(CS_ERR_GENERIC, 0, "estimate_interval: no Lanczos step completed");
+  std::vector<double> ritz(m);
+  tridiag_eigenvalues(m, hs.alpha, hs.beta, ritz.data());
+  *lo = 0.9 * ritz.front();  // spectral.cpp:123-128
+  *hi = 1.1 * ritz.back();
+  if (!(*lo > 0.0) || !std::isfinite(*hi))
+    fail(CS_ERR_NOT_SPD, 0, "estimate_interval: operator not positive definite");
+}
+
+// ====================================================================== PCG-S
+
+namespace {
+
+struct Blocks {
+  double *Q, *AQ, *Z, *P, *x, *r, *b, *zpA, *zpB;
+};
+
+Blocks workspace(cs_problem* p, int s) {
+  const int64_t ld = p->ld;
+  const size_t vecs = static_cast<size_t>(4 * s + 5);
+  if (p->ws_s != s) {
+    p->ws.release();
+    p->ws.alloc(sizeof(double) * vecs * ld);
+    CS_CUDA(cudaMemsetAsync(p->ws.p, 0, sizeof(double) * vecs * ld, p->ctx->stream));
+    p->ws_s = s;
+  }
+  double* base = p->ws.as<double>();
+  Blocks bk;
+  bk.Q = base;
+  bk.AQ = bk.Q + s * ld;
+  bk.Z = bk.AQ + s * ld;
+  bk.P = bk.Z + s * ld;
+  bk.x = bk.P + s * ld;
+  bk.r = bk.x + ld;
+  bk.b = bk.r + ld;
+  bk.zpA = bk.b + ld;
+  bk.zpB = bk.zpA + ld;
+  return bk;
+}
+
+// MPK steps 1..s on a basis whose z_0 is already in Z column 0 (mpk.cpp:53-69).
+void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int pending,
+               DevState* st) {
+  const int64_t ld = p->ld;
+  const double alpha = 2.0 / (hi - lo);           // mpk.hpp:22
+  const double sigma = (hi + lo) / (hi - lo);     // mpk.hpp:23-25
+  const double gamma = 1.0;
+  const bool jac = p->precond == CS_PRECOND_JACOBI;
+  auto zcol = [&](int q) { return bk.Z + q * ld; };
+  auto zp = [&](int q) -> double* {  // zp_q storage
+    if (q == 0) return bk.r;
+    if (!jac) return zcol(q);
+    return (q & 1) ? bk.zpA : bk.zpB;
+  };
+  for (int q = 1; q < s; ++q) {
+    SpmvArgs g;
+    g.x = zcol(q - 1);
+    g.y = bk.P + (q - 1) * ld;
+    g.zp1 = zp(q - 1);
+    g.zp2 = q >= 2 ? zp(q - 2) : nullptr;
+    g.zpout = jac ? zp(q) : nullptr;
+    g.zout = zcol(q);
+    if (q == 1) {
+      g.ca = alpha;
+      g.cb = -sigma;
+      g.cc = 0.0;
+    } else {
+      g.ca = 2.0 * alpha;
+      g.cb = -2.0 * sigma;
+      g.cc = -gamma;
+    }
+    g.col = q;
+    g.pending = pending;
+    g.st = st;
+    spmv_halo(p, q == 1 ? kMpkFirst : kMpkMid, g, zcol(q - 1));
+  }
+  SpmvArgs g;
+  g.x = zcol(s - 1);
+  g.y = bk.P + (s - 1) * ld;
+  g.col = s - 1;
+  g.pending = pending;
+  g.st = st;
+  spmv_halo(p, kMpkLast, g, zcol(s - 1));
+}
+
+}  // namespace
+
+void mpk_unit(cs_problem* p, double* Z, double* P, double* r, double* zpA, double* zpB, int s,
+              double lo, double hi, DevState* st) {
+  Blocks bk{};
+  bk.Z = Z;
+  bk.P = P;
+  bk.r = r;
+  bk.zpA = zpA;
+  bk.zpB = zpB;
+  mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st);
+}
+
+void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
+                    const cs_config& cfg, double* x_dev, cs_report* rep) {
+  cs_ctx* c = p->ctx;
+  CS_CUDA(cudaSetDevice(c->device));
+  // SolverConfig::validate, solver.cpp:15-22
+  if (cfg.s < 1 || cfg.s > kMaxS) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: s must be in [1, 64]");
+  if (!(cfg.tol > 0.0)) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: tol must be > 0");
+  if (cfg.max_outer < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: max_outer must be >= 1");
+  if (cfg.nu < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: nu must be >= 1");
+  const int mode = cfg.mode;
+  if (mode == CS_MODE_REFERENCE && c->nranks > 1)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "reference mode is single-GPU");
+  const int s = cfg.s;
+  const int64_t n = p->n_local, ld = p->ld;
+  const int64_t launches0 = c->launches, allred0 = c->allreduces;
+  const double nglob = static_cast<double>(p->n_global);
+
+  Blocks bk = workspace(p, s);
+  DevState* st = c->state.as<DevState>();
+
+  // vectors in: x (ghost slots filled by the halo), b
+  CS_CUDA(cudaMemcpyAsync(bk.x, x0_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  CS_CUDA(cudaMemcpyAsync(bk.b, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+
+  std::memset(rep, 0, offsetof(cs_report, cap));
+  rep->n_rel = rep->n_da = rep->n_db = 0;
+  const double bnorm = host_norm(p, bk.b, mode);  // solver.cpp:93
+  if (bnorm == 0.0) {
+    CS_CUDA(cudaMemsetAsync(x_dev, 0, sizeof(double) * n, c->stream));
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    rep->converged = 1;
+    rep->n_rel = 1;
+    if (rep->rel_residual && rep->cap > 0) rep->rel_residual[0] = 0.0;
+    return;
+  }
+  double lo = cfg.lambda_min, hi = cfg.lambda_max, t_lz = 0.0;
+  if (!cfg.has_spectrum) estimate_interval_dev(p, cfg.lanczos_steps, cfg.seed, mode, &lo, &hi, &t_lz);
+  rep->lambda_min = lo;
+  rep->lambda_max = hi;
+  if (!(hi > lo) || !(lo > 0.0) || !std::isfinite(hi))  // mpk.cpp:11-16
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "ChebyshevParams: need lambda_max > lambda_min > 0");
+  const int hist = cfg.max_outer + 2;
+  const int q = s * s;
+  const bool use_pack = mode == CS_MODE_FAST && pack_supported(s);
+  const size_t partial_n = std::max(use_pack ? pack_partial_doubles(s, n) : 0,
+                                    tree_gram_partial_doubles(n, s, s)) +
+                           spmv_dot_blocks(p->nslices) + 64;
+  char* scr = static_cast<char*>(ctx_scratch(
+      c, sizeof(double) * (3 * static_cast<size_t>(hist) + 4 * q + 8 * s + 64 + partial_n) +
+             64 * 256));
+  Arena ar{scr};
+  double* raw = ar.take<double>(2 * q + 2 * s + 1);
+  double* W = ar.take<double>(q);
+  double* alpha_d = ar.take<double>(s);
+  double* beta_d = ar.take<double>(q);
+  double* rel = ar.take<double>(hist);
+  double* da = ar.take<double>(hist);
+  double* db = ar.take<double>(hist);
+  double* partial = ar.take<double>(partial_n);
+  unsigned* ticket = ar.take<unsigned>(8);
+  CS_CUDA(cudaMemsetAsync(ticket, 0, 8 * sizeof(unsigned), c->stream));
+
+  init_state(c, bnorm, 0);
+  SmallArgs sa;
+  sa.s = s;
+  sa.nu = cfg.nu;
+  sa.gram = cfg.gram;
+  sa.max_outer = cfg.max_outer;
+  sa.tol = cfg.tol;
+  sa.st = st;
+  sa.W = W;
+  sa.alpha = alpha_d;
+  sa.beta = beta_d;
+  sa.raw = raw;
+  sa.rel = rel;
+  sa.da = da;
+  sa.db = db;
+  const SellView A = p->view();
+  UpdateArgs ua;
+  ua.s = s;
+  ua.n = n;
+  ua.ld = ld;
+  ua.x = bk.x;
+  ua.r = bk.r;
+  ua.inv_diag = A.inv_diag;
+  ua.alpha = alpha_d;
+  ua.st = st;
+
+  auto gram = [&](const double* u, int ku, const double* v, int kv, double* out) {
+    Launch L(c, CS_PHASE_REDUCE);
+    if (mode == CS_MODE_REFERENCE)
+      launch_serial_gram(n, ku, kv, u, ld, v, ld, out, st, c->stream);
+    else
+      launch_tree_gram(n, ku, kv, u, ld, v, ld, out, partial, ticket, st, c->stream);
+  };
+  // packed one-allreduce block {Q^T P, Z^T P, Z^T r, Q^T r, r^T r}
+  auto packed_reduce = [&](const double* Qm, const double* Zm) {
+    if (use_pack) {
+      Launch L(c, CS_PHASE_REDUCE);
+      launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, c->stream);
+    } else {
+      gram(Qm, s, bk.P, s, raw);
+      gram(Zm, s, bk.P, s, raw + q);
+      gram(Zm, s, bk.r, 1, raw + 2 * q);
+      gram(Qm, s, bk.r, 1, raw + 2 * q + s);
+      gram(bk.r, 1, bk.r, 1, raw + 2 * q + 2 * s);
+    }
+    allreduce_sum(c, raw, 2 * q + 2 * s + 1);
+  };
+  auto small = [&](void (*fn)(const SmallArgs&, cudaStream_t)) {
+    Launch L(c, CS_PHASE_SMALL);
+    fn(sa, c->stream);
+  };
+
+  Timer timer(c->stream);
+  // ---- setup: r0 = b - A x0 (solver.cpp:118-122), MPK(r0) (:125-129)
+  {
+    SpmvArgs g;
+    g.x = bk.x;
+    g.y = bk.r;
+    g.b = bk.b;
+    g.st = st;
+    spmv_halo(p, kResid, g, bk.x);
+  }
+  if (mode == CS_MODE_REFERENCE) {
+    gram(bk.r, 1, bk.r, 1, raw + q + s);
+    {
+      Launch L(c, CS_PHASE_SMALL);
+      launch_ref_test(sa, c->stream);  // rel[0], k = 1
+    }
+  }
+  {
+    Launch L(c, CS_PHASE_UPDATE);
+    launch_precond_apply(n, A.inv_diag, bk.r, bk.Z, st, 0, 0, c->stream);
+  }
+  mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st);
+  std::swap(bk.Q, bk.Z);  // q = basis.z ; aq = basis.p.columns(1, s)
+  std::swap(bk.AQ, bk.P);
+  ua.q = bk.Q;
+  ua.aq = bk.AQ;
+  ua.z = bk.Z;
+  ua.p = bk.P;
+  if (mode == CS_MODE_FAST) {
+    std::swap(bk.P, bk.AQ);  // pack wants P = A Q here
+    packed_reduce(bk.Q, bk.Q);
+    std::swap(bk.P, bk.AQ);
+    small(launch_fast_setup);
+  }
+
+  // ---- outer iterations
+  auto outer_fast = [&](bool first) {
+    ua.beta = first ? nullptr : beta_d;
+    ua.zw = bk.Z;  // z_0 = M^-1 r_k for the next MPK
+    {
+      Launch L(c, CS_PHASE_UPDATE);
+      launch_fast_update(ua, c->stream);
+    }
+    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st);
+    packed_reduce(bk.Q, bk.Z);
+    small(launch_fast_step);
+  };
+  auto outer_ref = [&]() {
+    gram(bk.Q, s, bk.AQ, s, raw);          // assemble_gram, solver.cpp:139-147
+    gram(bk.Q, s, bk.r, 1, raw + q);       // b1 = Q^T p_0, :153-154
+    small(launch_ref_alpha);               // :155-157
+    {
+      Launch L(c, CS_PHASE_UPDATE);
+      launch_ref_xr_update(ua, c->stream); // :159-163
+    }
+    gram(bk.r, 1, bk.r, 1, raw + q + s);   // ||r||, :165
+    {
+      Launch L(c, CS_PHASE_SMALL);
+      launch_ref_test(sa, c->stream);      // :166-171
+    }
+    {
+      Launch L(c, CS_PHASE_UPDATE);
+      launch_precond_apply(n, A.inv_diag, bk.r, bk.Z, st, 0, 0, c->stream);
+    }
+    mpk_steps(p, bk, s, lo, hi, 0, st);    // :173-176
+    gram(bk.Q, s, bk.P, s, raw + q + s + 1);  // b2, :178-179
+    small(launch_ref_beta);                // :180-182
+    ua.beta = beta_d;
+    Launch L(c, CS_PHASE_UPDATE);
+    launch_ref_block_update(ua, c->stream);  // :184-185
+  };
+
+  const int batch = cfg.check_every > 0 ? cfg.check_every : (n < (1 << 22) ? 16 : 4);
+  volatile int* flag = static_cast<volatile int*>(c->pinned);
+  cudaEvent_t ev[2];
+  CS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  int issued = 0, slot = 0;
+  bool have_prev = false;
+  for (;;) {
+    for (int bi = 0; bi < batch && issued < cfg.max_outer; ++bi, ++issued) {
+      if (mode == CS_MODE_FAST) outer_fast(issued == 0);
+      else outer_ref();
+    }
+    CS_CUDA(cudaMemcpyAsync(const_cast<int*>(&flag[slot]), &st->done, sizeof(int),
+                            cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaEventRecord(ev[slot], c->stream));
+    if (issued >= cfg.max_outer) break;
+    if (have_prev) {
+      CS_CUDA(cudaEventSynchronize(ev[slot ^ 1]));
+      if (flag[slot ^ 1]) break;
+    }
+    have_prev = true;
+    slot ^= 1;
+  }
+  const double t_solve = timer.stop();
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  collect_timing(c);
+  const DevState h = read_state(c);
+  raise_device_error(h, s);
+
+  CS_CUDA(cudaMemcpyAsync(x_dev, bk.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  // report, reference semantics (solver.cpp:120-188)
+  rep->converged = h.converged;
+  rep->outer_iters = h.outer_iters;
+  const int64_t mpks = 1 + (h.converged ? h.outer_iters - 1 : h.outer_iters);
+  rep->spmv_count = 1 + static_cast<int64_t>(s) * mpks;
+  rep->precond_count = static_cast<int64_t>(s) * mpks;
+  rep->allreduce_count = 2 * static_cast<int64_t>(h.outer_iters);
+  const double lflops = 3.5 * (static_cast<double>(s) * s + s) * nglob;
+  const double gflops = cfg.gram == CS_GRAM_FGS
+                            ? static_cast<double>(cfg.nu) * (static_cast<double>(s) * s + 2.0 * s)
+                            : static_cast<double>(s) * s * s / 3.0 + 2.0 * s * s * (s + 1.0);
+  for (int k = 0; k < h.outer_iters; ++k) rep->local_update_flops += lflops;
+  for (int k = 0; k < h.n_da + h.n_db; ++k) rep->gram_solve_flops += gflops;
+  rep->n_rel = h.n_rel;
+  rep->n_da = h.n_da;
+  rep->n_db = h.n_db;
+  auto copy_hist = [&](double* dst, const double* src, int len) {
+    if (dst && rep->cap > 0 && len > 0)
+      CS_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * std::min(len, rep->cap),
+                              cudaMemcpyDeviceToHost, c->stream));
+  };
+  copy_hist(rep->rel_residual, rel, h.n_rel);
+  copy_hist(rep->delta_alpha, da, h.n_da);
+  copy_hist(rep->delta_beta, db, h.n_db);
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  rep->device_allreduces = c->allreduces - allred0;
+  rep->kernel_launches = c->launches - launches0;
+  rep->t_lanczos_ms = t_lz;
+  rep->t_solve_ms = t_solve;
+}
+
+// ====================================================================== classical PCG
+
+void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, double tol,
+                   int max_iter, int mode, double* x_dev, cs_report* rep) {
+  cs_ctx* c = p->ctx;
+  CS_CUDA(cudaSetDevice(c->device));
+  if (!(tol >= 0.0) || max_iter < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "pcg_solve: bad tol/max_iter");
+  if (mode == CS_MODE_REFERENCE && c->nranks > 1)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "reference mode is single-GPU");
+  const int64_t n = p->n_local, ld = p->ld;
+  const int64_t launches0 = c->launches, allred0 = c->allreduces;
+  // vectors: x, r, b, p, q, z  (reuse the s=1 workspace slots)
+  Blocks bk = workspace(p, 1);
+  double* xv = bk.x;
+  double* rv = bk.r;
+  double* bv = bk.b;
+  double* pv = bk.Q;   // p needs ghost slots
+  double* qv = bk.AQ;
+  double* zv = bk.Z;
+  const int hist = max_iter + 2;
+  const size_t partial_n = static_cast<size_t>(std::max<int64_t>(spmv_dot_blocks(p->nslices),
+                                                                 (n + 255) / 256)) * 2 + 64;
+  char* scr = static_cast<char*>(
+      ctx_scratch(c, sizeof(double) * (static_cast<size_t>(hist) + partial_n + 64) + 16 * 256));
+  Arena ar{scr};
+  double* dots = ar.take<double>(4);
+  double* rel = ar.take<double>(hist);
+  double* partial = ar.take<double>(partial_n);
+  unsigned* ticket = ar.take<unsigned>(4);
+  CS_CUDA(cudaMemsetAsync(ticket, 0, 4 * sizeof(unsigned), c->stream));
+  DevState* st = c->state.as<DevState>();
+  const double* inv = p->view().inv_diag;
+  const bool serial = mode == CS_MODE_REFERENCE;
+  CS_CUDA(cudaMemcpyAsync(xv, x0_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  CS_CUDA(cudaMemcpyAsync(bv, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  std::memset(rep, 0, offsetof(cs_report, cap));
+  rep->n_rel = rep->n_da = rep->n_db = 0;
+  const double bnorm = host_norm(p, bv, mode);
+  if (bnorm == 0.0) {
+    CS_CUDA(cudaMemsetAsync(x_dev, 0, sizeof(double) * n, c->stream));
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    rep->converged = 1;
+    rep->n_rel = 1;
+    if (rep->rel_residual && rep->cap > 0) rep->rel_residual[0] = 0.0;
+    return;
+  }
+  init_state(c, bnorm, 0);
+  auto serial_dot = [&](const double* u, const double* v, double* out) {
+    Launch L(c, CS_PHASE_REDUCE);
+    launch_serial_gram(n, 1, 1, u, ld, v, ld, out, st, c->stream);
+  };
+  auto vec = [&](int which, bool dots_on) {
+    Launch L(c, CS_PHASE_UPDATE);
+    launch_axpby_pcg(which, n, xv, rv, pv, qv, inv, st, partial, ticket, dots, dots_on ? 0 : 1,
+                     c->stream);
+  };
+  auto scalar = [&](int which) {
+    Launch L(c, CS_PHASE_SMALL);
+    launch_pcg_scalar(which, tol, max_iter, st, dots, rel, c->stream);
+  };
+  Timer timer(c->stream);
+  {  // r = b - A x0
+    SpmvArgs g;
+    g.x = xv;
+    g.y = rv;
+    g.b = bv;
+    g.st = st;
+    spmv_halo(p, kResid, g, xv);
+  }
+  if (serial) {
+    serial_dot(rv, rv, dots);
+    {
+      Launch L(c, CS_PHASE_UPDATE);
+      launch_precond_apply(n, inv, rv, zv, st, -1, 0, c->stream);
+    }
+    serial_dot(rv, zv, dots + 1);
+  } else {
+    vec(3, true);
+  }
+  allreduce_sum(c, dots, 2);
+  scalar(0);
+  vec(0, false);  // p = z
+  auto iteration = [&]() {
+    SpmvArgs g;
+    g.x = pv;
+    g.y = qv;
+    g.st = st;
+    if (serial) {
+      spmv_halo(p, kPlain, g, pv);
+      serial_dot(pv, qv, dots);
+    } else {
+      g.partial = partial;
+      g.ticket = ticket + 1;
+      g.result = dots;
+      spmv_halo(p, kDot, g, pv);
+    }
+    allreduce_sum(c, dots, 1);
+    scalar(1);
+    if (serial) {
+      vec(1, false);
+      serial_dot(rv, rv, dots);
+      {
+        Launch L(c, CS_PHASE_UPDATE);
+        launch_precond_apply(n, inv, rv, zv, st, -1, 0, c->stream);
+      }
+      serial_dot(rv, zv, dots + 1);
+    } else {
+      vec(1, true);
+    }
+    allreduce_sum(c, dots, 2);
+    scalar(2);
+    vec(2, false);
+  };
+  const int batch = n < (1 << 22) ? 32 : 8;
+  volatile int* flag = static_cast<volatile int*>(c->pinned);
+  cudaEvent_t ev[2];
+  CS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  int issued = 0, slot = 0;
+  bool have_prev = false;
+  for (;;) {
+    for (int bi = 0; bi < batch && issued < max_iter; ++bi, ++issued) iteration();
+    CS_CUDA(cudaMemcpyAsync(const_cast<int*>(&flag[slot]), &st->done, sizeof(int),
+                            cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaEventRecord(ev[slot], c->stream));
+    if (issued >= max_iter) break;
+    if (have_prev) {
+      CS_CUDA(cudaEventSynchronize(ev[slot ^ 1]));
+      if (flag[slot ^ 1]) break;
+    }
+    have_prev = true;
+    slot ^= 1;
+  }
+  const double t_solve = timer.stop();
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  collect_timing(c);
+  const DevState h = read_state(c);
+  raise_device_error(h, 1);
+  CS_CUDA(cudaMemcpyAsync(x_dev, xv, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  rep->converged = h.converged;
+  rep->outer_iters = h.outer_iters;
+  rep->spmv_count = 1 + h.outer_iters;
+  rep->precond_count = 1 + (h.converged ? h.outer_iters - 1 : h.outer_iters);
+  rep->allreduce_count = 2 * static_cast<int64_t>(h.outer_iters);
+  for (int k = 0; k < h.outer_iters; ++k) rep->local_update_flops += 8.0 * static_cast<double>(p->n_global);
+  rep->n_rel = h.n_rel;
+  if (rep->rel_residual && rep->cap > 0 && h.n_rel > 0)
+    CS_CUDA(cudaMemcpyAsync(rep->rel_residual, rel, sizeof(double) * std::min(h.n_rel, rep->cap),
+                            cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  rep->device_allreduces = c->allreduces - allred0;
+  rep->kernel_launches = c->launches - launches0;
+  rep->t_solve_ms = t_solve;
+}
+
+}  // namespace csg

@@ -1,0 +1,620 @@
+// vec.cu -- streaming vector/block kernels: tall-skinny reductions (serial
+// reference order, deterministic tree, and the fused packed one-allreduce
+// reduction on FP64 DMMA), the fused x/r/Q/AQ update pass, preconditioner
+// apply, seeded start vectors and the classical-PCG vector steps.
+//
+// Arithmetic contracts:
+//  * "reference" kernels keep the reference's per-element operation sequence
+//    with explicit __dmul_rn/__dadd_rn (no FMA contraction):
+//    axpy y = y + a*x (kernels_scalar.cpp:6-8), xpby y = x + b*y (:10-12),
+//    block_update out_j = y_j + sum_q c_qj x_q in ascending q (dense_ops.cpp:29-42),
+//    dot / Gram entries as ONE serial ascending chain (dense_ops.cpp:10-15,
+//    kernels_scalar.cpp:22-33);
+//  * "fast" reductions use fixed-shape trees (warp shuffles, fixed block
+//    count, last-block finalisation in block order): deterministic run to run,
+//    but not the serial order.
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace csg {
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(int64_t threads, int per = kThreads) {
+  return static_cast<unsigned>((threads + per - 1) / per);
+}
+
+__device__ __forceinline__ bool halted(const DevState* st) {
+  return st != nullptr && *(volatile const int*)&st->done;
+}
+
+// ------------------------------------------------------------------ precond / rng
+
+__global__ void precond_kernel(int64_t n, const double* __restrict__ inv_diag,
+                               const double* __restrict__ in, double* out, DevState* st, int col,
+                               int pending) {
+  if (halted(st)) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double z = inv_diag ? __dmul_rn(inv_diag[i], in[i]) : in[i];
+  out[i] = z;
+  if (col >= 0 && !isfinite(z) && st != nullptr) {
+    atomicCAS(pending ? &st->pending : &st->err, 0ull, make_err(4, col));
+    if (!pending) st->done = 1;
+  }
+}
+
+// util.hpp:25-40: the i-th SplitMix64 draw is a pure function of
+// seed + (i+1)*golden, so the sequential generator parallelises exactly.
+__global__ void random_kernel(int64_t n, int64_t offset, uint64_t seed, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t z = seed + static_cast<uint64_t>(offset + i + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z = z ^ (z >> 31);
+  const double unit = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+  out[i] = __dsub_rn(__dmul_rn(2.0, unit), 1.0);
+}
+
+// ------------------------------------------------------------------ serial-order Gram
+
+__global__ void serial_gram_kernel(int64_t n, int ku, int kv, const double* __restrict__ u,
+                                   int64_t ldu, const double* __restrict__ v, int64_t ldv,
+                                   double* g, DevState* st) {
+  if (halted(st)) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ku * kv) return;
+  const int i = e % ku, j = e / ku;
+  const double* ui = u + i * ldu;
+  const double* vj = v + j * ldv;
+  double acc = 0.0;
+#pragma unroll 16
+  for (int64_t l = 0; l < n; ++l) acc = __dadd_rn(acc, __dmul_rn(ui[l], vj[l]));
+  g[e] = acc;
+}
+
+// ------------------------------------------------------------------ tree Gram (generic)
+
+constexpr int kTreeBlocks = 296;  // 2 x 148 SMs
+
+__global__ void __launch_bounds__(kThreads)
+    tree_gram_kernel(int64_t n, int ku, int kv, const double* __restrict__ u, int64_t ldu,
+                     const double* __restrict__ v, int64_t ldv, double* g, double* partial,
+                     unsigned* ticket, DevState* st) {
+  if (halted(st)) return;
+  __shared__ double red[kThreads / 32];
+  __shared__ bool last;
+  const int ne = ku * kv;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t b1 = min(n, b0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = 0; e < ne; ++e) {
+    const double* ui = u + (e % ku) * ldu;
+    const double* vj = v + (e / ku) * ldv;
+    double acc = 0.0;
+    for (int64_t l = b0 + threadIdx.x; l < b1; l += kThreads) acc += ui[l] * vj[l];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+      partial[static_cast<int64_t>(blockIdx.x) * ne + e] = s;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const volatile double* pp = partial;
+  for (int e = threadIdx.x; e < ne; e += kThreads) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += pp[static_cast<int64_t>(b) * ne + e];
+    g[e] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// ------------------------------------------------------------------ packed DMMA reduction
+//
+// One pass over Q, Z, P (= A Z columns 1..s) and r produces the whole
+// one-allreduce block {G1 = Q^T P, G2 = Z^T P, c1 = Z^T r, c2 = Q^T r, rr}.
+// A warp streams 32-row chunks with coalesced loads (lane = row); the r
+// products are plain per-lane FMAs, the (2s x s) Gram products run on the
+// FP64 tensor cores (mma.sync m8n8k4, DMMA) from a warp-private shared-memory
+// tile laid out [column][row] with a 36-double stride so the fragment loads
+// are bank-conflict free. Per-warp partials are combined in a fixed order and
+// the last block reduces the block partials in block order.
+
+constexpr int kPackWarps = 8;
+constexpr int kPackStride = 36;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int S>
+struct PackShape {
+  static constexpr int MT = (2 * S + 7) / 8;
+  static constexpr int NT = (S + 7) / 8;
+  static constexpr int UC = MT * 8;
+  static constexpr int PC = NT * 8;
+  static constexpr int NOUT = 2 * S * S + 2 * S + 1;
+  static constexpr size_t smem_warp = static_cast<size_t>(UC + PC) * kPackStride;
+  static constexpr size_t smem_bytes = smem_warp * kPackWarps * sizeof(double);
+};
+
+template <int S>
+__global__ void __launch_bounds__(kPackWarps * 32)
+    pack_kernel(int64_t n, int64_t ld, const double* __restrict__ Q, const double* __restrict__ Z,
+                const double* __restrict__ P, const double* __restrict__ r, double* packed,
+                double* partial, unsigned* ticket, DevState* st) {
+  using Sh = PackShape<S>;
+  if (halted(st)) return;
+  extern __shared__ double smem[];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double* sU = smem + warp * Sh::smem_warp;
+  double* sP = sU + Sh::UC * kPackStride;
+  for (int c = 2 * S; c < Sh::UC; ++c) sU[c * kPackStride + lane] = 0.0;
+  for (int c = S; c < Sh::PC; ++c) sP[c * kPackStride + lane] = 0.0;
+
+  double acc[Sh::MT][Sh::NT][2];
+#pragma unroll
+  for (int m = 0; m < Sh::MT; ++m)
+#pragma unroll
+    for (int q = 0; q < Sh::NT; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+  double c1[S], c2[S], rr = 0.0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) c1[i] = c2[i] = 0.0;
+
+  const int64_t nchunks = (n + 31) / 32;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kPackWarps;
+  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * kPackWarps + warp; ch < nchunks;
+       ch += stride) {
+    const int64_t row = ch * 32 + lane;
+    const bool ok = row < n;
+    double qv[S], zv[S], pv[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      qv[i] = ok ? __ldcs(Q + i * ld + row) : 0.0;
+      zv[i] = ok ? __ldcs(Z + i * ld + row) : 0.0;
+      pv[i] = ok ? __ldcs(P + i * ld + row) : 0.0;
+    }
+    const double rv = ok ? __ldcs(r + row) : 0.0;
+    rr = fma(rv, rv, rr);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      c2[i] = fma(qv[i], rv, c2[i]);
+      c1[i] = fma(zv[i], rv, c1[i]);
+      sU[i * kPackStride + lane] = qv[i];
+      sU[(S + i) * kPackStride + lane] = zv[i];
+      sP[i * kPackStride + lane] = pv[i];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      double a[Sh::MT], b[Sh::NT];
+#pragma unroll
+      for (int m = 0; m < Sh::MT; ++m) a[m] = sU[(m * 8 + g) * kPackStride + kk * 4 + t];
+#pragma unroll
+      for (int q = 0; q < Sh::NT; ++q) b[q] = sP[(q * 8 + g) * kPackStride + kk * 4 + t];
+#pragma unroll
+      for (int m = 0; m < Sh::MT; ++m)
+#pragma unroll
+        for (int q = 0; q < Sh::NT; ++q) dmma(acc[m][q], a[m], b[q]);
+    }
+    __syncwarp();
+  }
+  // warp-level: plain accumulators by shuffle tree
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    rr += __shfl_down_sync(0xffffffffu, rr, off);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      c1[i] += __shfl_down_sync(0xffffffffu, c1[i], off);
+      c2[i] += __shfl_down_sync(0xffffffffu, c2[i], off);
+    }
+  }
+  __syncthreads();  // tiles are dead; reuse smem as [warp][NOUT]
+  double* out = smem + warp * Sh::NOUT;
+#pragma unroll
+  for (int m = 0; m < Sh::MT; ++m)
+#pragma unroll
+    for (int q = 0; q < Sh::NT; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = m * 8 + g;       // U column: Q_i (i < S) or Z_{i-S}
+        const int j = q * 8 + 2 * t + e;  // P column
+        if (i < 2 * S && j < S) out[(i < S ? 0 : S * S) + (i % S) + j * S] = acc[m][q][e];
+      }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      out[2 * S * S + i] = c1[i];
+      out[2 * S * S + S + i] = c2[i];
+    }
+    out[2 * S * S + 2 * S] = rr;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < Sh::NOUT; e += kPackWarps * 32) {
+    double s = 0.0;
+    for (int w = 0; w < kPackWarps; ++w) s += smem[w * Sh::NOUT + e];
+    partial[static_cast<int64_t>(blockIdx.x) * Sh::NOUT + e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const volatile double* pp = partial;
+  for (int e = threadIdx.x; e < Sh::NOUT; e += kPackWarps * 32) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += pp[static_cast<int64_t>(b) * Sh::NOUT + e];
+    packed[e] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+int pack_grid(int64_t n) {
+  const int64_t chunks = (n + 31) / 32;
+  const int64_t want = (chunks + kPackWarps - 1) / kPackWarps;
+  return static_cast<int>(want < 148 * 3 ? (want > 0 ? want : 1) : 148 * 3);
+}
+
+template <int S>
+void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const double* p,
+                 const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
+                 cudaStream_t strm) {
+  using Sh = PackShape<S>;
+  static bool configured = false;
+  if (!configured) {
+    CS_CUDA(cudaFuncSetAttribute(pack_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Sh::smem_bytes)));
+    configured = true;
+  }
+  pack_kernel<S><<<pack_grid(n), kPackWarps * 32, Sh::smem_bytes, strm>>>(n, ld, q, z, p, r, packed,
+                                                                          partial, ticket, st);
+  CS_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ update pass
+//
+// Per row, in one read of each operand:
+//   (beta)  Q_j <- Z_j + sum_q beta_qj Q_q ; AQ_j <- P_j + sum_q beta_qj AQ_q
+//   (xr)    for j: x <- x + alpha_j Q_j ; r <- r + (-alpha_j) AQ_j
+//   (z0)    z_0 <- M^-1 r (the next MPK's first column) + finite check
+// with the reference operation order (block_update, then the interleaved axpys).
+
+template <int S, bool BETA, bool XR, bool Z0>
+__global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
+  if (halted(a.st)) return;
+  constexpr int SM = S > 0 ? S : kMaxS;
+  const int s = S > 0 ? S : a.s;
+  __shared__ double sh_alpha[SM];
+  __shared__ double sh_beta[BETA ? SM * SM : 1];
+  for (int t = threadIdx.x; t < s; t += blockDim.x) sh_alpha[t] = XR ? a.alpha[t] : 0.0;
+  if constexpr (BETA)
+    for (int t = threadIdx.x; t < s * s; t += blockDim.x) sh_beta[t] = a.beta[t];
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  double xv = 0.0, rv = 0.0;
+  if constexpr (XR) {
+    xv = a.x[i];
+    rv = a.r[i];
+  }
+  if constexpr (BETA) {
+    double qo[SM];
+#pragma unroll
+    for (int q = 0; q < SM; ++q)
+      if (q < s) qo[q] = a.q[q * a.ld + i];
+    for (int j = 0; j < s; ++j) {
+      double o = a.z[j * a.ld + i];
+#pragma unroll
+      for (int q = 0; q < SM; ++q)
+        if (q < s) o = __dadd_rn(o, __dmul_rn(sh_beta[q + j * s], qo[q]));
+      a.q[j * a.ld + i] = o;
+      if constexpr (XR) xv = __dadd_rn(xv, __dmul_rn(sh_alpha[j], o));
+    }
+#pragma unroll
+    for (int q = 0; q < SM; ++q)
+      if (q < s) qo[q] = a.aq[q * a.ld + i];
+    for (int j = 0; j < s; ++j) {
+      double o = a.p[j * a.ld + i];
+#pragma unroll
+      for (int q = 0; q < SM; ++q)
+        if (q < s) o = __dadd_rn(o, __dmul_rn(sh_beta[q + j * s], qo[q]));
+      a.aq[j * a.ld + i] = o;
+      if constexpr (XR) rv = __dadd_rn(rv, __dmul_rn(-sh_alpha[j], o));
+    }
+  } else if constexpr (XR) {
+    for (int j = 0; j < s; ++j) {
+      xv = __dadd_rn(xv, __dmul_rn(sh_alpha[j], a.q[j * a.ld + i]));
+      rv = __dadd_rn(rv, __dmul_rn(-sh_alpha[j], a.aq[j * a.ld + i]));
+    }
+  }
+  if constexpr (XR) {
+    a.x[i] = xv;
+    a.r[i] = rv;
+  }
+  if constexpr (Z0) {
+    const double z = a.inv_diag ? __dmul_rn(a.inv_diag[i], rv) : rv;
+    a.zw[i] = z;
+    if (!isfinite(z)) atomicCAS(&a.st->pending, 0ull, make_err(4, 0));
+  }
+}
+
+template <bool BETA, bool XR, bool Z0>
+void update_dispatch(const UpdateArgs& a, cudaStream_t st) {
+  const unsigned grid = grid_for(a.n);
+  if (a.n == 0) return;
+#define CSG_UPD(SV) update_kernel<SV, BETA, XR, Z0><<<grid, kThreads, 0, st>>>(a)
+  switch (a.s) {
+    case 1: CSG_UPD(1); break;
+    case 2: CSG_UPD(2); break;
+    case 3: CSG_UPD(3); break;
+    case 4: CSG_UPD(4); break;
+    case 5: CSG_UPD(5); break;
+    case 6: CSG_UPD(6); break;
+    case 8: CSG_UPD(8); break;
+    case 10: CSG_UPD(10); break;
+    case 12: CSG_UPD(12); break;
+    case 16: CSG_UPD(16); break;
+    default: CSG_UPD(0); break;
+  }
+#undef CSG_UPD
+  CS_CUDA(cudaGetLastError());
+}
+
+// generic block_update (unit entry), dense_ops.cpp:29-42
+__global__ void block_update_kernel(int64_t n, int m, int k, const double* __restrict__ y,
+                                    const double* __restrict__ x, const double* __restrict__ c,
+                                    double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < k; ++j) {
+    double o = y[j * n + i];
+    for (int q = 0; q < m; ++q) o = __dadd_rn(o, __dmul_rn(c[q + j * m], x[q * n + i]));
+    out[j * n + i] = o;
+  }
+}
+
+// ------------------------------------------------------------------ classical PCG vector steps
+// which 0: z = M^-1 r; p = z                         (solver.cpp:228-231)
+// which 1: x += step p; r -= step q  (+ fast dots r.r, r.M^-1 r)   (solver.cpp:241-243)
+// which 2: p = M^-1 r + beta p                       (solver.cpp:254-259)
+// which 3: fast dots r.r and r.M^-1 r only (setup)
+
+template <int WHICH, bool DOTS>
+__global__ void __launch_bounds__(kThreads)
+    pcg_vec_kernel(int64_t n, double* x, double* r, double* p, const double* __restrict__ q,
+                   const double* __restrict__ inv_diag, DevState* st, double* partial,
+                   unsigned* ticket, double* result) {
+  if (halted(st)) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double d_rr = 0.0, d_rz = 0.0;
+  if (i < n) {
+    if constexpr (WHICH == 0) {
+      const double rv = r[i];
+      p[i] = inv_diag ? __dmul_rn(inv_diag[i], rv) : rv;
+    } else if constexpr (WHICH == 1) {
+      const double step = st->scal[0];
+      x[i] = __dadd_rn(x[i], __dmul_rn(step, p[i]));
+      const double rv = __dadd_rn(r[i], __dmul_rn(-step, q[i]));
+      r[i] = rv;
+      if constexpr (DOTS) {
+        const double zv = inv_diag ? __dmul_rn(inv_diag[i], rv) : rv;
+        d_rr = rv * rv;
+        d_rz = rv * zv;
+      }
+    } else if constexpr (WHICH == 2) {
+      const double rv = r[i];
+      const double zv = inv_diag ? __dmul_rn(inv_diag[i], rv) : rv;
+      p[i] = __dadd_rn(zv, __dmul_rn(st->scal[1], p[i]));
+    } else {
+      const double rv = r[i];
+      const double zv = inv_diag ? __dmul_rn(inv_diag[i], rv) : rv;
+      d_rr = rv * rv;
+      d_rz = rv * zv;
+    }
+  }
+  if constexpr (DOTS) {
+    __shared__ double red[2][kThreads / 32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      d_rr += __shfl_down_sync(0xffffffffu, d_rr, off);
+      d_rz += __shfl_down_sync(0xffffffffu, d_rz, off);
+    }
+    if (lane == 0) {
+      red[0][warp] = d_rr;
+      red[1][warp] = d_rz;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        a += red[0][w];
+        b += red[1][w];
+      }
+      partial[2 * blockIdx.x] = a;
+      partial[2 * blockIdx.x + 1] = b;
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      const volatile double* pp = partial;
+      double a = 0.0, b = 0.0;
+      for (unsigned bb = 0; bb < gridDim.x; ++bb) {
+        a += pp[2 * bb];
+        b += pp[2 * bb + 1];
+      }
+      result[0] = a;
+      result[1] = b;
+      *ticket = 0u;
+    }
+  }
+}
+
+__global__ void scale2_kernel(int64_t n, double* v, double* g, const double* __restrict__ sv,
+                              const double* __restrict__ sg, const double* denom, DevState* st) {
+  if (halted(st)) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double d = *denom;
+  v[i] = __ddiv_rn(sv[i], d);
+  g[i] = __ddiv_rn(sg[i], d);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+
+void launch_precond_apply(int64_t n, const double* inv_diag, const double* in, double* out,
+                          DevState* st, int col, int pending, cudaStream_t s) {
+  if (n == 0) return;
+  precond_kernel<<<grid_for(n), kThreads, 0, s>>>(n, inv_diag, in, out, st, col, pending);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_random_vector(int64_t n, int64_t offset, uint64_t seed, double* out, cudaStream_t s) {
+  if (n == 0) return;
+  random_kernel<<<grid_for(n), kThreads, 0, s>>>(n, offset, seed, out);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_serial_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, const double* v,
+                        int64_t ldv, double* g, DevState* st, cudaStream_t s) {
+  const int ne = ku * kv;
+  serial_gram_kernel<<<grid_for(ne, 64), 64, 0, s>>>(n, ku, kv, u, ldu, v, ldv, g, st);
+  CS_CUDA(cudaGetLastError());
+}
+
+size_t tree_gram_partial_doubles(int64_t, int ku, int kv) {
+  return static_cast<size_t>(kTreeBlocks) * ku * kv;
+}
+
+void launch_tree_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, const double* v,
+                      int64_t ldv, double* g, double* partial, unsigned* ticket, DevState* st,
+                      cudaStream_t s) {
+  tree_gram_kernel<<<kTreeBlocks, kThreads, 0, s>>>(n, ku, kv, u, ldu, v, ldv, g, partial, ticket,
+                                                    st);
+  CS_CUDA(cudaGetLastError());
+}
+
+bool pack_supported(int s) {
+  switch (s) {
+    case 1: case 2: case 3: case 4: case 5: case 6: case 8: case 10: case 12: case 16:
+      return true;
+    default:
+      return false;
+  }
+}
+
+size_t pack_partial_doubles(int s, int64_t n) {
+  return static_cast<size_t>(pack_grid(n)) * (2 * s * s + 2 * s + 1);
+}
+
+void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
+                 const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
+                 cudaStream_t strm) {
+#define CSG_PACK(SV) pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, strm)
+  switch (s) {
+    case 1: CSG_PACK(1); break;
+    case 2: CSG_PACK(2); break;
+    case 3: CSG_PACK(3); break;
+    case 4: CSG_PACK(4); break;
+    case 5: CSG_PACK(5); break;
+    case 6: CSG_PACK(6); break;
+    case 8: CSG_PACK(8); break;
+    case 10: CSG_PACK(10); break;
+    case 12: CSG_PACK(12); break;
+    case 16: CSG_PACK(16); break;
+    default: throw LibError{9, 0, "pack: unsupported s"};
+  }
+#undef CSG_PACK
+}
+
+void launch_fast_update(const UpdateArgs& a, cudaStream_t s) {
+  if (a.beta != nullptr)
+    update_dispatch<true, true, true>(a, s);
+  else
+    update_dispatch<false, true, true>(a, s);
+}
+
+void launch_ref_xr_update(const UpdateArgs& a, cudaStream_t s) {
+  update_dispatch<false, true, false>(a, s);
+}
+
+void launch_ref_block_update(const UpdateArgs& a, cudaStream_t s) {
+  update_dispatch<true, false, false>(a, s);
+}
+
+void launch_block_update(int64_t n, int m, int k, const double* y, const double* x,
+                         const double* c, double* out, cudaStream_t s) {
+  if (n == 0) return;
+  block_update_kernel<<<grid_for(n), kThreads, 0, s>>>(n, m, k, y, x, c, out);
+  CS_CUDA(cudaGetLastError());
+}
+
+int pcg_vec_blocks(int64_t n) { return static_cast<int>(grid_for(n)); }
+
+void launch_axpby_pcg(int which, int64_t n, double* x, double* r, double* p, const double* q,
+                      const double* inv_diag, DevState* st, double* partial, unsigned* ticket,
+                      double* result, int serial, cudaStream_t s) {
+  if (n == 0) return;
+  const unsigned grid = grid_for(n);
+  const bool dots = !serial;
+  switch (which) {
+    case 0:
+      pcg_vec_kernel<0, false><<<grid, kThreads, 0, s>>>(n, x, r, p, q, inv_diag, st, partial,
+                                                         ticket, result);
+      break;
+    case 1:
+      if (dots)
+        pcg_vec_kernel<1, true><<<grid, kThreads, 0, s>>>(n, x, r, p, q, inv_diag, st, partial,
+                                                          ticket, result);
+      else
+        pcg_vec_kernel<1, false><<<grid, kThreads, 0, s>>>(n, x, r, p, q, inv_diag, st, partial,
+                                                           ticket, result);
+      break;
+    case 2:
+      pcg_vec_kernel<2, false><<<grid, kThreads, 0, s>>>(n, x, r, p, q, inv_diag, st, partial,
+                                                         ticket, result);
+      break;
+    case 3:
+      pcg_vec_kernel<3, true><<<grid, kThreads, 0, s>>>(n, x, r, p, q, inv_diag, st, partial,
+                                                        ticket, result);
+      break;
+    default: throw LibError{9, 0, "bad pcg step"};
+  }
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_scale2(int64_t n, double* v, double* g, const double* src_v, const double* src_g,
+                   const double* denom, DevState* st, cudaStream_t s) {
+  if (n == 0) return;
+  scale2_kernel<<<grid_for(n), kThreads, 0, s>>>(n, v, g, src_v, src_g, denom, st);
+  CS_CUDA(cudaGetLastError());
+}
+
+}  // namespace csg

@@ -1,0 +1,204 @@
+"""GPU solve-level parity: pcg_s_solve / pcg_solve against the CPU oracle.
+
+* reference mode (the reference algebra + serial reduction order) must be
+  bitwise equal to the oracle given the same spectrum -- x, every residual
+  and delta history entry, and every counter;
+* fast mode (one packed reduction per outer iteration, tree reductions) must
+  reach the same outer-iteration count within +-1 at nu >= 30 / Cholesky and
+  an x within 1e-8 relative of the oracle's (north star).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_X = 1e-8  # relative, north star
+
+
+def _csr(cs, o):
+    return cs.CsrMatrix(o.n, o.rowptr, o.col, o.val)
+
+
+def _problem(port, name):
+    kind, n = name.split("_")
+    n = int(n)
+    return port.poisson27(n) if kind == "p27" else port.stencil7(n)
+
+
+def _relx(x, xr):
+    return np.linalg.norm(x - xr) / np.linalg.norm(xr)
+
+
+REF_CASES = [
+    # problem, s, nu, gram, tol, precond
+    ("p27_16", 4, 30, "fgs", 1e-6, 0),
+    ("p27_16", 4, 30, "cholesky", 1e-6, 0),
+    ("p27_16", 2, 30, "fgs", 1e-6, 0),
+    ("p7_32", 4, 2, "fgs", 1e-8, 1),
+    ("p27_32", 8, 30, "fgs", 1e-8, 1),
+    ("p27_32", 12, 30, "fgs", 1e-8, 1),
+    ("p27_8", 1, 30, "fgs", 1e-8, 1),
+]
+
+
+@pytest.mark.parametrize("case", REF_CASES, ids=lambda c: "-".join(map(str, c)))
+def test_pcgs_reference_mode_bitwise(cs, port, case):
+    name, s, nu, gram, tol, precond = case
+    o = _problem(port, name)
+    lam = port.estimate_interval(o, precond)
+    x_o, r_o = port.pcg_s_solve(o, s=s, nu=nu, gram=gram, tol=tol, spectrum=lam, precond=precond,
+                                max_outer=2000)
+    m = cs.JacobiPreconditioner(_csr(cs, o)) if precond else cs.IdentityPreconditioner()
+    cfg = cs.SolverConfig(s=s, tol=tol, max_outer=2000, fgs=cs.FgsConfig(nu=nu),
+                          gram_solver=cs.GramSolverKind[gram], mode="reference",
+                          spectrum=cs.SpectrumEstimate(*lam))
+    res = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n), m, cfg)
+    rep = res.report
+    assert rep.outer_iters == r_o.outer_iters and rep.converged == r_o.converged
+    assert res.x.tobytes() == x_o.tobytes()
+    assert rep.rel_residual.tobytes() == r_o.rel_residual.tobytes()
+    assert rep.delta_alpha.tobytes() == r_o.delta_alpha.tobytes()
+    assert rep.delta_beta.tobytes() == r_o.delta_beta.tobytes()
+    assert (rep.spmv_count, rep.precond_count, rep.allreduce_count) == (
+        r_o.spmv_count, r_o.precond_count, r_o.allreduce_count)
+    assert rep.local_update_flops == r_o.local_update_flops
+    assert rep.gram_solve_flops == r_o.gram_solve_flops
+
+
+@pytest.mark.slow
+def test_baseline_config1_reference_mode_bitwise(cs, port):
+    """BASELINE config 1: 7-pt 64^3, s=4, Jacobi, nu=2, tol 1e-8 (343 outer
+    iterations on the reference; chaotic under rounding)."""
+    o = port.stencil7(64)
+    lam = port.estimate_interval(o, 1)
+    x_o, r_o = port.pcg_s_solve(o, s=4, nu=2, tol=1e-8, spectrum=lam, max_outer=5000)
+    assert r_o.outer_iters == 343
+    cfg = cs.SolverConfig(s=4, tol=1e-8, max_outer=5000, fgs=cs.FgsConfig(nu=2),
+                          mode="reference", spectrum=cs.SpectrumEstimate(*lam))
+    res = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n),
+                         cs.JacobiPreconditioner(_csr(cs, o)), cfg)
+    assert res.report.outer_iters == 343
+    assert res.x.tobytes() == x_o.tobytes()
+    assert res.report.rel_residual.tobytes() == r_o.rel_residual.tobytes()
+
+
+FAST_CASES = [
+    ("p27_32", 4, 30, "fgs"), ("p27_32", 8, 30, "fgs"), ("p27_32", 12, 30, "fgs"),
+    ("p27_32", 4, 30, "cholesky"), ("p7_32", 4, 30, "fgs"), ("p27_64", 4, 30, "fgs"),
+    ("p27_64", 8, 30, "fgs"), ("p27_64", 4, 30, "cholesky"), ("p7_64", 4, 30, "fgs"),
+]
+
+
+@pytest.mark.parametrize("case", FAST_CASES, ids=lambda c: "-".join(map(str, c)))
+def test_pcgs_fast_mode_parity(cs, port, case):
+    name, s, nu, gram = case
+    o = _problem(port, name)
+    x_o, r_o = port.pcg_s_solve(o, s=s, nu=nu, gram=gram, tol=1e-8, max_outer=5000)
+    cfg = cs.SolverConfig(s=s, tol=1e-8, max_outer=5000, fgs=cs.FgsConfig(nu=nu),
+                          gram_solver=cs.GramSolverKind[gram], mode="fast")
+    res = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n),
+                         cs.JacobiPreconditioner(_csr(cs, o)), cfg)
+    rep = res.report
+    assert rep.converged
+    assert abs(rep.outer_iters - r_o.outer_iters) <= 1, (rep.outer_iters, r_o.outer_iters)
+    assert _relx(res.x, x_o) <= TOL_X
+    assert abs(rep.spectrum_used.lambda_min / r_o.lambda_min - 1) < 1e-9
+    # one packed reduction (one allreduce) per outer iteration on the device
+    assert rep.device_allreduces <= rep.outer_iters + 2
+    # the recurrence residual tracks the true residual
+    y = port.spmv(o, res.x)
+    true_rel = np.linalg.norm(1.0 - y) / np.sqrt(o.n)
+    assert true_rel <= 1e-8 * 10
+
+
+def test_pcg_classical(cs, port):
+    o = port.poisson27(32)
+    x_o, r_o = port.pcg_solve(o, tol=1e-8, max_iter=1000)
+    a = _csr(cs, o)
+    m = cs.JacobiPreconditioner(a)
+    p = cs.DeviceProblem.from_csr(a).set_precond(m)
+    ref = p.pcg_solve(tol=1e-8, max_iter=1000, mode="reference")
+    assert ref.report.outer_iters == r_o.outer_iters
+    assert ref.x.tobytes() == x_o.tobytes()
+    assert ref.report.rel_residual.tobytes() == r_o.rel_residual.tobytes()
+    fast = cs.pcg_solve(a, np.ones(o.n), np.zeros(o.n), m, 1e-8, 1000)
+    assert abs(fast.report.outer_iters - r_o.outer_iters) <= 1
+    assert _relx(fast.x, x_o) <= TOL_X
+    assert fast.report.spmv_count == 1 + fast.report.outer_iters
+
+
+def test_zero_rhs(cs, port):
+    o = port.poisson27(8)
+    res = cs.pcg_s_solve(_csr(cs, o), np.zeros(o.n), np.ones(o.n), cs.IdentityPreconditioner())
+    assert res.report.converged and res.report.rel_residual.tolist() == [0.0]
+    assert not res.x.any()
+
+
+def test_identity_breakdown_like_reference(cs):
+    """A=I, M=I, auto spectrum, s=4 -> SolverBreakdownError at outer 1
+    (z_1 = 0 makes the Gram diagonal vanish), exactly like the reference."""
+    a = cs.CsrMatrix.identity(50)
+    with pytest.raises(cs.SolverBreakdownError) as e:
+        cs.pcg_s_solve(a, np.ones(50), np.zeros(50), cs.IdentityPreconditioner(),
+                       cs.SolverConfig(s=4, mode="reference"))
+    assert e.value.outer_iteration == 1
+    res = cs.pcg_s_solve(a, np.ones(50), np.zeros(50), cs.IdentityPreconditioner(),
+                         cs.SolverConfig(s=3, spectrum=cs.SpectrumEstimate(0.5, 2.0)))
+    assert res.report.converged and res.report.outer_iters == 1
+
+
+def test_cholesky_breakdown_outer2(cs, port):
+    """27-pt 8^3, s=8, Cholesky, M=I -> SolverBreakdownError at outer 2."""
+    o = port.poisson27(8)
+    with pytest.raises(port_error(port)) as e:
+        port.pcg_s_solve(o, s=8, gram="cholesky", precond=0)
+    lam = port.estimate_interval(o, 0)
+    cfg = cs.SolverConfig(s=8, gram_solver=cs.GramSolverKind.cholesky, mode="reference",
+                          spectrum=cs.SpectrumEstimate(*lam))
+    with pytest.raises(cs.SolverBreakdownError) as e2:
+        cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n), cs.IdentityPreconditioner(), cfg)
+    assert e2.value.outer_iteration == e.value.payload == 2
+
+
+def port_error(port):
+    from oracle.oracle import OracleError
+    return OracleError
+
+
+def test_jacobi_not_spd(cs):
+    a = cs.CsrMatrix(2, [0, 1, 2], [0, 1], [1.0, -1.0])
+    with pytest.raises(cs.NotSpdError):
+        cs.pcg_s_solve(a, np.ones(2), np.zeros(2), cs.JacobiPreconditioner.__new__(cs.JacobiPreconditioner))
+
+
+def test_invalid_config(cs):
+    a = cs.CsrMatrix.identity(4)
+    for cfg in (cs.SolverConfig(s=0), cs.SolverConfig(s=65), cs.SolverConfig(tol=0.0),
+                cs.SolverConfig(max_outer=0), cs.SolverConfig(fgs=cs.FgsConfig(nu=0))):
+        with pytest.raises(cs.InvalidArgumentError):
+            cs.pcg_s_solve(a, np.ones(4), np.zeros(4), cs.IdentityPreconditioner(), cfg)
+    with pytest.raises(cs.DimensionError):
+        cs.pcg_s_solve(a, np.ones(3), np.zeros(4), cs.IdentityPreconditioner())
+
+
+def test_max_outer_not_converged(cs, port):
+    o = port.poisson27(16)
+    lam = port.estimate_interval(o, 1)
+    x_o, r_o = port.pcg_s_solve(o, s=4, tol=1e-12, max_outer=3, spectrum=lam)
+    cfg = cs.SolverConfig(s=4, tol=1e-12, max_outer=3, mode="reference",
+                          spectrum=cs.SpectrumEstimate(*lam))
+    res = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n), cs.JacobiPreconditioner(_csr(cs, o)), cfg)
+    assert not res.report.converged and res.report.outer_iters == 3
+    assert res.x.tobytes() == x_o.tobytes()
+    assert res.report.delta_beta.size == r_o.delta_beta.size == 3
+    assert res.report.spmv_count == r_o.spmv_count
+
+
+def test_device_resident_generated(cs, port):
+    """Device-generated problem, device-resident solve, fast mode."""
+    p = cs.DeviceProblem.generate("poisson27", 48, 48, 48).set_precond("jacobi")
+    o = port.poisson27(48)
+    x_o, r_o = port.pcg_s_solve(o, s=8, tol=1e-8, max_outer=5000)
+    res = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=5000))
+    assert abs(res.report.outer_iters - r_o.outer_iters) <= 1
+    assert _relx(res.x, x_o) <= TOL_X

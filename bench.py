@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 Chebyshev s-step PCG solve path.
+
+Metric (BASELINE.json): s-step PCG solve time to 1e-8 as GDOF/s
+(GDOF/s := n_global / t_solve / 1e9, one "step" = one complete pcg_s_solve:
+Lanczos spectrum estimate + setup + outer iterations to ||r||/||b|| <= 1e-8).
+
+Workload (BASELINE configs[1], weak-scaled for N>1 as configs[4]): 27-point
+Poisson 256^3 per GPU (global 256 x 256 x 256N, z-stacked), s=8, FGS nu=30,
+Jacobi, b=1, x0=0, fast (one-allreduce) algebra. Inputs are device-generated
+and HBM-resident when the timed region starts (`value`); `e2e` repeats the
+solve through the reference-facing C-ABI entry with HOST buffers (the host CSR
+upload + SELL conversion + solve + x download inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line. `--impl reference` times the reference CPU
+implementation (oracle/_ref, the unmodified reference library compiled from
+/root/reference, or the C restatement when absent) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "s-step PCG solve time to 1e-8 (GDOF/s)"
+UNIT = "GDOF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256, help="grid edge per GPU")
+    ap.add_argument("--stencil", type=int, default=27, choices=[7, 27])
+    ap.add_argument("--s", type=int, default=8)
+    ap.add_argument("--nu", type=int, default=30)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--mode", default="fast", choices=["fast", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pcg", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ helpers
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        loaded = [v for v in sm if v > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def nnz_of(stencil, nx, ny, nz):
+    f = lambda m: 3 * m - 2 if m > 1 else 1  # noqa: E731
+    if stencil == 27:
+        return f(nx) * f(ny) * f(nz)
+    n = nx * ny * nz
+    return n + 2 * ((nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1))
+
+
+def spmv_alg_bytes(nnz, n, s, outer, lanczos_steps, jacobi=True):
+    """Algorithmic bytes of every SpMV-phase kernel of one solve:
+    12 B per nonzero (FP64 value + int32 column), x read once, outputs once."""
+    b_spmv = 12 * nnz + 16 * n                       # y = A x
+    b_resid = 12 * nnz + 24 * n                      # r = b - A x
+    b_dot = 12 * nnz + 16 * n                        # Lanczos t = A v (+ v.t)
+    j = 8 * n if jacobi else 0
+    b_first = 12 * nnz + 16 * n + 8 * n + j + (8 * n if jacobi else 0) + 8 * n  # zp0 rd, zp wr, z wr
+    b_mid = 12 * nnz + 16 * n + 16 * n + j + (8 * n if jacobi else 0) + 8 * n
+    b_last = b_spmv
+    if s == 1:
+        per_mpk = b_last
+    else:
+        per_mpk = b_first + (s - 2) * b_mid + b_last
+    mpks = 1 + outer  # setup MPK + one (speculative) MPK per outer iteration (fast algebra)
+    return b_resid + lanczos_steps * b_dot + mpks * per_mpk, b_spmv
+
+
+def outer_bytes(nnz, n, s):
+    """B_outer(s) = s*B_spmv + 8n(14s+3) (Jacobi)."""
+    return s * (12 * nnz + 16 * n) + 8 * n * (14 * s + 3)
+
+
+# ------------------------------------------------------------------------------ CPU baseline
+
+def golden_outer(stencil, n, s, nu, world):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "outer_counts.json")) as f:
+            table = json.load(f)
+        key = f"p{stencil}_{n}x{n}x{n * world}_s{s}_nu{nu}_jacobi_1e-08"
+        return table.get(key)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_sample(args, lam, world=1):
+    """Bounded CPU sample of the same workload on one host core: the reference
+    pcg_s_solve on a 256 x 256 x nzs slab of the same operator with the same
+    spectrum, per-outer time = t(max_outer=2) - t(max_outer=1), scaled to the
+    full grid (per-outer cost is linear in n)."""
+    from oracle import oracle as orc
+    kind = "ref" if orc.available("ref") else "port"
+    o = orc.Oracle(kind)
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except (AttributeError, OSError):
+        pass
+    nzs = 16
+    nxy = args.n
+    if args.stencil == 27:
+        a = o.poisson27(nxy, nxy, nzs)
+    else:
+        a = orc.Oracle("port").stencil7(nxy, nxy, nzs)
+    t = []
+    for mo in (1, 2):
+        t0 = time.perf_counter()
+        o.pcg_s_solve(a, s=args.s, nu=args.nu, tol=args.tol, max_outer=mo, spectrum=lam,
+                      precond=1)
+        t.append(time.perf_counter() - t0)
+    per_outer = max(t[1] - t[0], 1e-9) * (args.n * world) / nzs
+    return {"kind": "reference" if kind == "ref" else "port", "cores": 1,
+            "per_outer_s": per_outer,
+            "sample": (f"pcg_s_solve on a {nxy}x{nxy}x{nzs} slab, same operator/s/nu/spectrum, "
+                       f"t(max_outer=2)-t(max_outer=1) = {t[1]-t[0]:.3f} s scaled x{args.n*world/nzs:g} "
+                       "to the full grid; Lanczos excluded; 1 of "
+                       f"{os.cpu_count()} host cores (the reference is single-threaded)")}
+
+
+# ------------------------------------------------------------------------------ reference arm
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    n = args.n
+    n_global = n * n * n * world
+    outer = golden_outer(args.stencil, n, args.s, args.nu, world)
+    lam = (0.0023, 1.5205)  # 27-pt Jacobi spectrum interval at 128^3; sample only
+    src = "golden"
+    if outer is None:
+        outer, src = 1000, "assumed"
+    vals = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        sample = cpu_sample(args, lam, world)
+        if i >= args.warmup:
+            vals.append(n_global / (outer * sample["per_outer_s"]) / 1e9)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (27-point Poisson, b=1, x0=0)",
+            "config": {"workload": f"{args.stencil}-pt Poisson {n}x{n}x{n*world}, s={args.s}, "
+                       f"nu={args.nu}, Jacobi, tol {args.tol:g}",
+                       "outer_iters": outer, "outer_iters_source": src},
+            "ms_per_step": outer * sample["per_outer_s"] * 1e3,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": sample["kind"],
+                             "sample": sample["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2603_09790_b200 as cs
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    ctx = cs.Context(local)
+    cs.set_default_context(ctx)
+    if world > 1:
+        obj = [cs.Context.unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        ctx.comm_init(world, rank, obj[0])
+    n = args.n
+    kind = "poisson27" if args.stencil == 27 else "poisson7"
+    prob = cs.DeviceProblem.generate(kind, n, n, n * world, ctx=ctx).set_precond("jacobi")
+    nl, ng = prob.n_local, prob.n_global
+    dev = torch.device("cuda", local)
+    b = torch.ones(nl, dtype=torch.float64, device=dev)
+    x0 = torch.zeros(nl, dtype=torch.float64, device=dev)
+    x = torch.empty(nl, dtype=torch.float64, device=dev)
+    cfg = cs.SolverConfig(s=args.s, tol=args.tol, max_outer=50000, fgs=cs.FgsConfig(nu=args.nu),
+                          mode=args.mode)
+    torch.cuda.synchronize()
+
+    def step():
+        return prob.pcg_s_solve_device(b.data_ptr(), x0.data_ptr(), x.data_ptr(), cfg)
+
+    for _ in range(args.warmup):
+        rep = step()
+    ext = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(local)
+    barrier()
+    ctx.reset_timing()
+    ctx.set_timing(True)
+    l0 = ctx.launches()
+    clocks.start()
+    e0.record(ext)
+    reps = [step() for _ in range(args.steps)]
+    e1.record(ext)
+    e1.synchronize()
+    clk = clocks.stop()
+    ctx.set_timing(False)
+    launches = ctx.launches() - l0
+    t_ms = e0.elapsed_time(e1)
+    t_max = ctx.allreduce_max(t_ms)
+    barrier()
+    phases = ctx.timing()
+    rep = reps[-1]
+    value = ng * args.steps / (t_max / 1e3) / 1e9
+    ms_step = t_max / args.steps
+
+    # roofline of the dominant kernel (SpMV fused with the MPK epilogue)
+    nnz_l = prob.nnz_local
+    alg, b_spmv = spmv_alg_bytes(nnz_l, nl, args.s, rep.outer_iters, cfg.lanczos_steps)
+    spmv_ms = phases["spmv"][0]
+    achieved = alg * args.steps / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
+    peak, peak_src = measured_peak()
+    tr = ncu_traffic()
+    roof = {"kernel": "sell_kernel<kMpk*> (SELL-32 FP64 SpMV + fused MPK epilogue)",
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "traffic": tr.get("bytes_per_launch") if tr else None,
+            "traffic_alg_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
+            "peak_source": peak_src,
+            "spmv_share_of_step": spmv_ms / (t_ms) if t_ms > 0 else None,
+            "alg_bytes_per_spmv": b_spmv}
+    # whole-solve bandwidth against B_outer
+    solve_outer_ms = rep.t_solve_ms / max(rep.outer_iters, 1)
+    b_out = outer_bytes(nnz_l, nl, args.s)
+    solve_level = {"t_outer_ms": solve_outer_ms, "B_outer_GB": b_out / 1e9,
+                   "achieved_GBps": b_out / (solve_outer_ms / 1e3) / 1e9,
+                   "frac_of_peak": b_out / (solve_outer_ms / 1e3) / 1e9 / peak,
+                   "t_lanczos_ms": rep.t_lanczos_ms, "t_solve_ms": rep.t_solve_ms}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated 27-point Poisson, b=1, x0=0)",
+            "config": {"workload": f"{args.stencil}-pt Poisson {n}^3 per GPU "
+                       f"(global {n}x{n}x{n*world}), s={args.s}, nu={args.nu}, Jacobi, "
+                       f"tol {args.tol:g}, {args.mode} algebra",
+                       "n_global": ng, "nnz_local": nnz_l, "outer_iters": rep.outer_iters,
+                       "converged": rep.converged,
+                       "final_rel_residual": float(rep.rel_residual[-1]),
+                       "lambda": [rep.spectrum_used.lambda_min, rep.spectrum_used.lambda_max],
+                       "allreduces_per_solve": rep.device_allreduces,
+                       "l2": "inputs > L2 (matrix %.1f GB/GPU vs 126 MB L2); no flush" %
+                             (prob.device_bytes / 1e9),
+                       "parallelism": f"z-slab row partition x{world}"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "solve_roofline": solve_level,
+            "phases_ms": {k: round(v[0], 3) for k, v in phases.items()},
+            "clocks": clk}
+
+    # e2e through the reference-facing C-ABI entry with host buffers
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, cs, ctx, prob, world, torch)
+    # classical PCG on the same GPUs (configs[1] "vs classical PCG")
+    if not args.no_pcg:
+        rp = prob.pcg_solve_device(b.data_ptr(), x0.data_ptr(), x.data_ptr(), tol=args.tol,
+                                   max_iter=100000)
+        t_pcg = ctx.allreduce_max(rp.t_solve_ms)
+        line["pcg"] = {"gdof_s": ng / (t_pcg / 1e3) / 1e9, "iters": rp.outer_iters,
+                       "t_solve_ms": t_pcg, "allreduces_per_solve": 2 * rp.outer_iters,
+                       "reductions_per_s_pcgs": rep.device_allreduces / (ms_step / 1e3),
+                       "reductions_per_s_pcg": 2 * rp.outer_iters / (t_pcg / 1e3)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        lam = (rep.spectrum_used.lambda_min, rep.spectrum_used.lambda_max)
+        smp = cpu_sample(args, lam)
+        v = ng / (rep.outer_iters * smp["per_outer_s"]) / 1e9
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": smp["cores"],
+                                "kind": smp["kind"], "sample": smp["sample"] +
+                                f"; x {rep.outer_iters} outer iterations of this GPU run"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    prob.close()
+    barrier()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def e2e(args, cs, ctx, prob, world, torch):
+    """Reference-facing entry with HOST buffers: N=1 -> cs_pcg_s_solve_csr with the host
+    int64 CSR (upload + SELL conversion + Jacobi setup + Lanczos + solve + x download);
+    N>1 -> cs_pcg_s_solve on the rank's slab with host b/x0/x."""
+    import numpy as np
+    nl, ng = prob.n_local, prob.n_global
+    cfg = cs.SolverConfig(s=args.s, tol=args.tol, max_outer=50000, fgs=cs.FgsConfig(nu=args.nu),
+                          mode=args.mode)
+
+    def pinned(arr):
+        t = torch.empty(arr.size, dtype={np.int64: torch.int64, np.float64: torch.float64}[arr.dtype.type],
+                        pin_memory=True)
+        t.numpy()[:] = arr
+        return t
+
+    if world == 1:
+        a = prob.to_csr()
+        keep = [pinned(a.row_offsets), pinned(a.col_indices), pinned(a.values)]
+        ah = cs.CsrMatrix(a.n, keep[0].numpy(), keep[1].numpy(), keep[2].numpy())
+        del a
+        bh, x0h = pinned(np.ones(nl)), pinned(np.zeros(nl))
+        m = cs.JacobiPreconditioner(ah)
+        call = lambda: cs.pcg_s_solve(ah, bh.numpy(), x0h.numpy(), m, cfg, ctx=ctx)  # noqa: E731
+        h2d = 8 * (ah.n + 1) + 16 * ah.nnz() + 16 * nl
+        entry = "cs_pcg_s_solve_csr (host int64 CSR + b + x0 -> host x)"
+    else:
+        bh, x0h = pinned(np.ones(nl)), pinned(np.zeros(nl))
+        call = lambda: prob.pcg_s_solve(bh.numpy(), x0h.numpy(), cfg)  # noqa: E731
+        h2d = 16 * nl
+        entry = "cs_pcg_s_solve (device-resident slab, host b + x0 -> host x)"
+    call()  # warm-up
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        res = call()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    dt = ctx.allreduce_max(dt)
+    return {"value": ng / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 8 * nl, "steps": args.e2e_steps, "entry": entry,
+            "ms_per_step": dt * 1e3, "outer_iters": res.report.outer_iters}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

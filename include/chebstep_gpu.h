@@ -129,6 +129,8 @@ int cs_ctx_reset_timing(cs_ctx* ctx);
 int cs_ctx_get_timing(cs_ctx* ctx, int phase, double* ms, int64_t* launches);
 int cs_ctx_launch_count(cs_ctx* ctx, int64_t* launches);
 int cs_ctx_synchronize(cs_ctx* ctx);
+/* the cudaStream_t every solve kernel of this context is launched on */
+int cs_ctx_stream(cs_ctx* ctx, void** stream);
 
 /* Multi-GPU (one process per GPU). Rank 0 creates the id and the host
  * transports its 128 bytes to the other ranks (torch.distributed, files...). */

@@ -69,6 +69,7 @@ SIGNATURES = {
     "cs_ctx_get_timing": (C.c_int, [_vp, C.c_int, _dp, C.POINTER(C.c_int64)]),
     "cs_ctx_launch_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "cs_ctx_synchronize": (C.c_int, [_vp]),
+    "cs_ctx_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "cs_comm_unique_id": (C.c_int, [C.c_char_p]),
     "cs_ctx_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
     "cs_ctx_allreduce_max": (C.c_int, [_vp, _dp]),
@@ -112,7 +113,7 @@ SIGNATURES = {
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2603_09790_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2603_09790_b200/build.py` "
         "(the CUDA library is the product; there is no CPU fallback)")
 
 lib = C.CDLL(LIB_PATH)

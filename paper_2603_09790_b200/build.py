@@ -1,6 +1,8 @@
 """Build libchebstep_gpu.so in-tree for sm_100a (nvcc cross-compiles; no GPU needed).
 
-    python -m paper_2603_09790_b200.build [--force] [--jobs N]
+    python paper_2603_09790_b200/build.py [--force] [--jobs N]
+
+(run as a script: importing the package needs the built library)
 
 Every .cu/.cpp under csrc/ is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo`` into build/ and

@@ -157,6 +157,12 @@ class Context:
     def synchronize(self):
         _check(lib.cs_ctx_synchronize(self.handle))
 
+    def stream(self) -> int:
+        """cudaStream_t (as int) of this context's solve kernels."""
+        h = C.c_void_p()
+        _check(lib.cs_ctx_stream(self.handle, C.byref(h)))
+        return h.value or 0
+
 
 _default_ctx: Optional[Context] = None
 

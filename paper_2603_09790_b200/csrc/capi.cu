@@ -131,6 +131,10 @@ int cs_ctx_synchronize(cs_ctx* ctx) {
   return guard([&] { sync(ctx); });
 }
 
+int cs_ctx_stream(cs_ctx* ctx, void** stream) {
+  return guard([&] { *stream = static_cast<void*>(ctx->stream); });
+}
+
 int cs_comm_unique_id(unsigned char id[128]) {
   return guard([&] {
     ncclUniqueId uid;

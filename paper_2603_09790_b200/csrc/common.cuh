@@ -76,3 +76,43 @@ struct LibError {
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 }  // namespace csg
+
+#ifdef __CUDACC__
+namespace csg {
+
+// Deterministic finalisation of per-block partials, executed by ALL threads of
+// the last block (ticket pattern). partial[b*ne + e] for b < count. Output e is
+// summed in a fixed order that depends only on (count, blockDim): wide outputs
+// use one thread per entry (serial over b), narrow outputs a strided per-thread
+// chain followed by a fixed warp/block tree. Loads bypass L1 (ld.global.cg).
+__device__ __forceinline__ void finalize_partials(const double* partial, unsigned count, int ne,
+                                                  double* out) {
+  if (ne >= 32) {
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+      double s = 0.0;
+      for (unsigned b = 0; b < count; ++b) s += __ldcg(partial + static_cast<size_t>(b) * ne + e);
+      out[e] = s;
+    }
+    return;
+  }
+  __shared__ double fin_red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int e = 0; e < ne; ++e) {
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < count; b += blockDim.x)
+      s += __ldcg(partial + static_cast<size_t>(b) * ne + e);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) fin_red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += fin_red[w];
+      out[e] = t;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace csg
+#endif  // __CUDACC__

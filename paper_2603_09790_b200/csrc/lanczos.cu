@@ -93,13 +93,10 @@ __global__ void __launch_bounds__(kThreads)
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
     __threadfence();
-    const volatile double* pp = partial;
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += pp[b];
-    *result = s;
-    *ticket = 0u;
+    finalize_partials(partial, gridDim.x, 1, result);
+    if (threadIdx.x == 0) *ticket = 0u;
   }
 }
 

@@ -563,7 +563,13 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   copy_hist(rep->delta_alpha, da, h.n_da);
   copy_hist(rep->delta_beta, db, h.n_db);
   CS_CUDA(cudaStreamSynchronize(c->stream));
-  rep->device_allreduces = c->allreduces - allred0;
+  // global reductions of the iterations that executed: ||b||, the setup
+  // block, then one packed block per outer (fast) or W|b1, ||r||, b2 (reference)
+  rep->device_allreduces =
+      mode == CS_MODE_FAST
+          ? 2 + static_cast<int64_t>(h.outer_iters)
+          : 2 + 3 * static_cast<int64_t>(h.outer_iters) - (h.converged ? 1 : 0);
+  (void)allred0;
   rep->kernel_launches = c->launches - launches0;
   rep->t_lanczos_ms = t_lz;
   rep->t_solve_ms = t_solve;

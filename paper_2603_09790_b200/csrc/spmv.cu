@@ -101,13 +101,10 @@ __global__ void __launch_bounds__(kWarps * 32)
       last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
       __threadfence();
-      double s = 0.0;
-      const volatile double* pp = g.partial;
-      for (unsigned b = 0; b < gridDim.x; ++b) s += pp[b];
-      *g.result = s;
-      *g.ticket = 0u;
+      finalize_partials(g.partial, gridDim.x, 1, g.result);
+      if (threadIdx.x == 0) *g.ticket = 0u;
     }
   }
 }

@@ -115,12 +115,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const volatile double* pp = partial;
-  for (int e = threadIdx.x; e < ne; e += kThreads) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += pp[static_cast<int64_t>(b) * ne + e];
-    g[e] = s;
-  }
+  finalize_partials(partial, gridDim.x, ne, g);
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
@@ -262,12 +257,7 @@ __global__ void __launch_bounds__(kPackWarps * 32)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const volatile double* pp = partial;
-  for (int e = threadIdx.x; e < Sh::NOUT; e += kPackWarps * 32) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += pp[static_cast<int64_t>(b) * Sh::NOUT + e];
-    packed[e] = s;
-  }
+  finalize_partials(partial, gridDim.x, Sh::NOUT, packed);
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
@@ -301,8 +291,18 @@ void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const 
 //   (z0)    z_0 <- M^-1 r (the next MPK's first column) + finite check
 // with the reference operation order (block_update, then the interleaved axpys).
 
+// per-column base pointers as kernel parameters: the column addresses become
+// uniform-register operands instead of 64-bit per-thread address registers
+template <int SM>
+struct Cols {
+  double* q[SM];
+  double* aq[SM];
+  const double* z[SM];
+  const double* p[SM];
+};
+
 template <int S, bool BETA, bool XR, bool Z0>
-__global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) update_kernel(UpdateArgs a, Cols<(S > 0 ? S : kMaxS)> c) {
   if (halted(a.st)) return;
   constexpr int SM = S > 0 ? S : kMaxS;
   const int s = S > 0 ? S : a.s;
@@ -314,42 +314,65 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
+  // Every operand of the row is loaded before the dependent arithmetic so a
+  // thread keeps 2s (+2) independent loads in flight.
   double xv = 0.0, rv = 0.0;
   if constexpr (XR) {
     xv = a.x[i];
     rv = a.r[i];
   }
+  double lo[SM], hi[SM];  // (old Q, Z) then (old AQ, P)
+#pragma unroll
+  for (int q = 0; q < SM; ++q)
+    if (q < s) {
+      lo[q] = c.q[q][i];
+      hi[q] = BETA ? c.z[q][i] : 0.0;
+    }
   if constexpr (BETA) {
-    double qo[SM];
+    // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39)
 #pragma unroll
     for (int q = 0; q < SM; ++q)
-      if (q < s) qo[q] = a.q[q * a.ld + i];
-    for (int j = 0; j < s; ++j) {
-      double o = a.z[j * a.ld + i];
+      if (q < s) {
+        const double xq = lo[q];
 #pragma unroll
-      for (int q = 0; q < SM; ++q)
-        if (q < s) o = __dadd_rn(o, __dmul_rn(sh_beta[q + j * s], qo[q]));
-      a.q[j * a.ld + i] = o;
-      if constexpr (XR) xv = __dadd_rn(xv, __dmul_rn(sh_alpha[j], o));
-    }
+        for (int j = 0; j < SM; ++j)
+          if (j < s) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * s], xq));
+      }
 #pragma unroll
-    for (int q = 0; q < SM; ++q)
-      if (q < s) qo[q] = a.aq[q * a.ld + i];
-    for (int j = 0; j < s; ++j) {
-      double o = a.p[j * a.ld + i];
-#pragma unroll
-      for (int q = 0; q < SM; ++q)
-        if (q < s) o = __dadd_rn(o, __dmul_rn(sh_beta[q + j * s], qo[q]));
-      a.aq[j * a.ld + i] = o;
-      if constexpr (XR) rv = __dadd_rn(rv, __dmul_rn(-sh_alpha[j], o));
-    }
-  } else if constexpr (XR) {
-    for (int j = 0; j < s; ++j) {
-      xv = __dadd_rn(xv, __dmul_rn(sh_alpha[j], a.q[j * a.ld + i]));
-      rv = __dadd_rn(rv, __dmul_rn(-sh_alpha[j], a.aq[j * a.ld + i]));
-    }
+    for (int j = 0; j < SM; ++j)
+      if (j < s) c.q[j][i] = hi[j];  // new Q_j
   }
   if constexpr (XR) {
+#pragma unroll
+    for (int j = 0; j < SM; ++j)
+      if (j < s) xv = __dadd_rn(xv, __dmul_rn(sh_alpha[j], BETA ? hi[j] : lo[j]));
+  }
+  // compiler memory barrier: reload beta from shared memory for the AQ half
+  // instead of keeping all s*s coefficients live in registers across halves
+  asm volatile("" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < SM; ++q)
+    if (q < s) {
+      lo[q] = c.aq[q][i];
+      hi[q] = BETA ? c.p[q][i] : 0.0;
+    }
+  if constexpr (BETA) {
+#pragma unroll
+    for (int q = 0; q < SM; ++q)
+      if (q < s) {
+        const double xq = lo[q];
+#pragma unroll
+        for (int j = 0; j < SM; ++j)
+          if (j < s) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * s], xq));
+      }
+#pragma unroll
+    for (int j = 0; j < SM; ++j)
+      if (j < s) c.aq[j][i] = hi[j];  // new AQ_j
+  }
+  if constexpr (XR) {
+#pragma unroll
+    for (int j = 0; j < SM; ++j)
+      if (j < s) rv = __dadd_rn(rv, __dmul_rn(-sh_alpha[j], BETA ? hi[j] : lo[j]));
     a.x[i] = xv;
     a.r[i] = rv;
   }
@@ -360,11 +383,25 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a) {
   }
 }
 
+template <int S>
+Cols<S> make_cols(const UpdateArgs& a) {
+  Cols<S> c{};
+  const int s = S == kMaxS ? a.s : S;
+  for (int j = 0; j < s; ++j) {
+    c.q[j] = a.q ? a.q + j * a.ld : nullptr;
+    c.aq[j] = a.aq ? a.aq + j * a.ld : nullptr;
+    c.z[j] = a.z ? a.z + j * a.ld : nullptr;
+    c.p[j] = a.p ? a.p + j * a.ld : nullptr;
+  }
+  return c;
+}
+
 template <bool BETA, bool XR, bool Z0>
 void update_dispatch(const UpdateArgs& a, cudaStream_t st) {
   const unsigned grid = grid_for(a.n);
   if (a.n == 0) return;
-#define CSG_UPD(SV) update_kernel<SV, BETA, XR, Z0><<<grid, kThreads, 0, st>>>(a)
+#define CSG_UPD(SV) \
+  update_kernel<SV, BETA, XR, Z0><<<grid, kThreads, 0, st>>>(a, make_cols<SV ? SV : kMaxS>(a))
   switch (a.s) {
     case 1: CSG_UPD(1); break;
     case 2: CSG_UPD(2); break;
@@ -460,17 +497,10 @@ __global__ void __launch_bounds__(kThreads)
       last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
       __threadfence();
-      const volatile double* pp = partial;
-      double a = 0.0, b = 0.0;
-      for (unsigned bb = 0; bb < gridDim.x; ++bb) {
-        a += pp[2 * bb];
-        b += pp[2 * bb + 1];
-      }
-      result[0] = a;
-      result[1] = b;
-      *ticket = 0u;
+      finalize_partials(partial, gridDim.x, 2, result);
+      if (threadIdx.x == 0) *ticket = 0u;
     }
   }
 }

@@ -48,6 +48,33 @@ __device__ double gram_residual(int s, const double* W, int k, const double* rhs
   return res;
 }
 
+// One thread per right-hand-side column, W and the iterate in registers.
+template <int S>
+__device__ void fgs_columns_reg(const double* W, int k, const double* rhs, int nu, double* x) {
+  for (int col = threadIdx.x; col < k; col += blockDim.x) {
+    double w[S][S], b[S], xc[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      b[i] = rhs[i + col * S];
+      xc[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) w[i][j] = W[i + j * S];
+    }
+    for (int sweep = 0; sweep < nu; ++sweep) {
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        double acc = b[i];
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j != i) acc = __dsub_rn(acc, __dmul_rn(w[i][j], xc[j]));
+        xc[i] = __ddiv_rn(acc, w[i][i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) x[i + col * S] = xc[i];
+  }
+}
+
 // gram.cpp:78-119. Returns 0 or the NotSpd sub-code. x, tmp: s*k.
 __device__ int fgs_dev(int s, const double* W, int k, const double* rhs, int nu, double* x,
                        double* delta, double* tmp) {
@@ -62,15 +89,24 @@ __device__ int fgs_dev(int s, const double* W, int k, const double* rhs, int nu,
     *delta = 0.0;
     return 0;
   }
-  for (int col = threadIdx.x; col < k; col += blockDim.x) {
-    const double* b = rhs + col * s;
-    double* xc = x + col * s;
-    for (int sweep = 0; sweep < nu; ++sweep)
-      for (int i = 0; i < s; ++i) {
-        double acc = b[i];
-        for (int j = 0; j < s; ++j)
-          if (j != i) acc = __dsub_rn(acc, __dmul_rn(W[i + j * s], xc[j]));
-        xc[i] = __ddiv_rn(acc, W[i + i * s]);
+  switch (s) {  // register-resident sweeps for small orders, same operation sequence
+    case 2: fgs_columns_reg<2>(W, k, rhs, nu, x); break;
+    case 3: fgs_columns_reg<3>(W, k, rhs, nu, x); break;
+    case 4: fgs_columns_reg<4>(W, k, rhs, nu, x); break;
+    case 5: fgs_columns_reg<5>(W, k, rhs, nu, x); break;
+    case 6: fgs_columns_reg<6>(W, k, rhs, nu, x); break;
+    case 8: fgs_columns_reg<8>(W, k, rhs, nu, x); break;
+    default:
+      for (int col = threadIdx.x; col < k; col += blockDim.x) {
+        const double* b = rhs + col * s;
+        double* xc = x + col * s;
+        for (int sweep = 0; sweep < nu; ++sweep)
+          for (int i = 0; i < s; ++i) {
+            double acc = b[i];
+            for (int j = 0; j < s; ++j)
+              if (j != i) acc = __dsub_rn(acc, __dmul_rn(W[i + j * s], xc[j]));
+            xc[i] = __ddiv_rn(acc, W[i + i * s]);
+          }
       }
   }
   __syncthreads();

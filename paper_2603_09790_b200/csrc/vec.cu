@@ -301,8 +301,14 @@ struct Cols {
   const double* p[SM];
 };
 
+// Block = 8 warps over 128 rows: warps 0-3 take the Q role (Q_j <- Z_j + sum_q
+// beta_qj Q_q, then x += sum_j alpha_j Q_j), warps 4-7 the AQ role (AQ_j <- P_j +
+// sum_q beta_qj AQ_q, then r += sum_j (-alpha_j) AQ_j and z_0 = M^-1 r). The two
+// halves are independent, so each thread holds 2s operands instead of 4s.
+constexpr int kUpdRows = 128;
+
 template <int S, bool BETA, bool XR, bool Z0>
-__global__ void __launch_bounds__(kThreads, 2) update_kernel(UpdateArgs a, Cols<(S > 0 ? S : kMaxS)> c) {
+__global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S > 0 ? S : kMaxS)> c) {
   if (halted(a.st)) return;
   constexpr int SM = S > 0 ? S : kMaxS;
   const int s = S > 0 ? S : a.s;
@@ -312,22 +318,26 @@ __global__ void __launch_bounds__(kThreads, 2) update_kernel(UpdateArgs a, Cols<
   if constexpr (BETA)
     for (int t = threadIdx.x; t < s * s; t += blockDim.x) sh_beta[t] = a.beta[t];
   __syncthreads();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  // Every operand of the row is loaded before the dependent arithmetic so a
-  // thread keeps 2s (+2) independent loads in flight.
-  double xv = 0.0, rv = 0.0;
-  if constexpr (XR) {
-    xv = a.x[i];
-    rv = a.r[i];
-  }
-  double lo[SM], hi[SM];  // (old Q, Z) then (old AQ, P)
+  const bool aq_role = threadIdx.x >= kUpdRows;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kUpdRows + (threadIdx.x & (kUpdRows - 1));
+  const bool active = i < a.n;
+  double* const* dst = aq_role ? c.aq : c.q;      // updated in place
+  const double* const* src = aq_role ? c.p : c.z; // new basis part
+  double acc = 0.0;
+  double lo[SM], hi[SM];
+  if (active) {
+    if constexpr (XR) acc = aq_role ? a.r[i] : a.x[i];
 #pragma unroll
-  for (int q = 0; q < SM; ++q)
-    if (q < s) {
-      lo[q] = c.q[q][i];
-      hi[q] = BETA ? c.z[q][i] : 0.0;
-    }
+    for (int q = 0; q < SM; ++q)
+      if (q < s) {
+        lo[q] = dst[q][i];
+        hi[q] = BETA ? src[q][i] : 0.0;
+      }
+  }
+  // The AQ role overwrites Z column 0 with z_0 = M^-1 r below, which the Q role
+  // of the same rows reads above: every load of the block precedes every store.
+  if constexpr (Z0) __syncthreads();
+  if (!active) return;
   if constexpr (BETA) {
     // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39)
 #pragma unroll
@@ -340,46 +350,23 @@ __global__ void __launch_bounds__(kThreads, 2) update_kernel(UpdateArgs a, Cols<
       }
 #pragma unroll
     for (int j = 0; j < SM; ++j)
-      if (j < s) c.q[j][i] = hi[j];  // new Q_j
+      if (j < s) dst[j][i] = hi[j];
   }
   if constexpr (XR) {
+    // solver.cpp:159-162: x += alpha_j q_j ; r += (-alpha_j) aq_j, ascending j
+    const double sign = aq_role ? -1.0 : 1.0;
 #pragma unroll
     for (int j = 0; j < SM; ++j)
-      if (j < s) xv = __dadd_rn(xv, __dmul_rn(sh_alpha[j], BETA ? hi[j] : lo[j]));
-  }
-  // compiler memory barrier: reload beta from shared memory for the AQ half
-  // instead of keeping all s*s coefficients live in registers across halves
-  asm volatile("" ::: "memory");
-#pragma unroll
-  for (int q = 0; q < SM; ++q)
-    if (q < s) {
-      lo[q] = c.aq[q][i];
-      hi[q] = BETA ? c.p[q][i] : 0.0;
-    }
-  if constexpr (BETA) {
-#pragma unroll
-    for (int q = 0; q < SM; ++q)
-      if (q < s) {
-        const double xq = lo[q];
-#pragma unroll
-        for (int j = 0; j < SM; ++j)
-          if (j < s) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * s], xq));
-      }
-#pragma unroll
-    for (int j = 0; j < SM; ++j)
-      if (j < s) c.aq[j][i] = hi[j];  // new AQ_j
-  }
-  if constexpr (XR) {
-#pragma unroll
-    for (int j = 0; j < SM; ++j)
-      if (j < s) rv = __dadd_rn(rv, __dmul_rn(-sh_alpha[j], BETA ? hi[j] : lo[j]));
-    a.x[i] = xv;
-    a.r[i] = rv;
+      if (j < s) acc = __dadd_rn(acc, __dmul_rn(sign * sh_alpha[j], BETA ? hi[j] : lo[j]));
+    if (aq_role) a.r[i] = acc;
+    else a.x[i] = acc;
   }
   if constexpr (Z0) {
-    const double z = a.inv_diag ? __dmul_rn(a.inv_diag[i], rv) : rv;
-    a.zw[i] = z;
-    if (!isfinite(z)) atomicCAS(&a.st->pending, 0ull, make_err(4, 0));
+    if (aq_role) {
+      const double z = a.inv_diag ? __dmul_rn(a.inv_diag[i], acc) : acc;
+      a.zw[i] = z;
+      if (!isfinite(z)) atomicCAS(&a.st->pending, 0ull, make_err(4, 0));
+    }
   }
 }
 
@@ -398,7 +385,7 @@ Cols<S> make_cols(const UpdateArgs& a) {
 
 template <bool BETA, bool XR, bool Z0>
 void update_dispatch(const UpdateArgs& a, cudaStream_t st) {
-  const unsigned grid = grid_for(a.n);
+  const unsigned grid = grid_for(a.n, kUpdRows);
   if (a.n == 0) return;
 #define CSG_UPD(SV) \
   update_kernel<SV, BETA, XR, Z0><<<grid, kThreads, 0, st>>>(a, make_cols<SV ? SV : kMaxS>(a))

@@ -1,0 +1,43 @@
+"""Multi-GPU parity (needs >= 2 GPUs; skipped otherwise): runs
+tools/mgpu_check.py under torchrun, one rank per GPU, z-slab partition with
+NCCL halo exchange and one NCCL allreduce per outer iteration."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.parametrize("stencil,n,nz", [("poisson27", 40, 48), ("poisson7", 32, 40)])
+def test_multi_gpu_parity(stencil, n, nz):
+    ng = _gpus()
+    if ng < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(ng, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--grid", str(n), "--nz", str(nz),
+           "--stencil", stencil]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    line = [l for l in out.stdout.splitlines() if l.startswith("MGPU ")]
+    assert line, out.stdout[-3000:] + out.stderr[-3000:]
+    res = json.loads(line[0][5:])
+    assert len(res) == world
+    for r in res:
+        assert r["assembly_bitwise"] and r["ghosts_ok"] and r["spmv_bitwise"], r
+        assert r["outer_ok"], r
+        assert r["x_rel"] <= 1e-8, r
+        assert abs(r["pcg_iters"][0] - r["pcg_iters"][1]) <= 1 and r["pcg_x_rel"] <= 1e-8, r
+        assert r["lambda_rel"] < 1e-9, r

@@ -1,0 +1,92 @@
+"""Multi-GPU parity driver (torchrun, one process per GPU), used by
+tests/test_gpu_multi.py:
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mgpu_check.py --grid 48
+
+Each rank owns a z-slab of a global 27-point (or 7-point) grid generated on
+its GPU. Checks, per rank, against the CPU oracle (test infrastructure):
+  * partitioned assembly: local rows with global columns == the oracle's rows, bitwise;
+  * ghost list == the neighbour planes;
+  * distributed SpMV (NCCL halo exchange + SELL kernel) == oracle rows, bitwise;
+  * distributed fast-mode PCG-S (one NCCL allreduce per outer iteration):
+    outer count within +-1 of the oracle, x within 1e-8 relative;
+  * classical PCG on the same slabs.
+Rank 0 prints one JSON line with every verdict.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--grid", type=int, default=48)
+    ap.add_argument("--nz", type=int, default=0)
+    ap.add_argument("--s", type=int, default=4)
+    ap.add_argument("--stencil", default="poisson27")
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    rank, world, local = (int(os.environ[k]) for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    import paper_2603_09790_b200 as cs
+    from oracle.oracle import Oracle
+    ctx = cs.Context(local)
+    cs.set_default_context(ctx)
+    obj = [cs.Context.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.comm_init(world, rank, obj[0])
+    n, nz = a.grid, a.nz or a.grid
+    port = Oracle("port")
+    o = port.poisson27(n, n, nz) if a.stencil == "poisson27" else port.stencil7(n, n, nz)
+    p = cs.DeviceProblem.generate(a.stencil, n, n, nz, ctx=ctx).set_precond("jacobi")
+    b0, e0 = p.row_begin, p.row_begin + p.n_local
+    res = {"rank": rank, "rows": [b0, e0]}
+    loc = p.to_csr()
+    rp = o.rowptr[b0:e0 + 1] - o.rowptr[b0]
+    res["assembly_bitwise"] = bool(
+        loc.row_offsets.tobytes() == rp.tobytes()
+        and loc.col_indices.tobytes() == o.col[o.rowptr[b0]:o.rowptr[e0]].tobytes()
+        and loc.values.tobytes() == o.val[o.rowptr[b0]:o.rowptr[e0]].tobytes())
+    plane = n * n
+    want = (list(range(b0 - plane, b0)) if b0 > 0 else []) + \
+        (list(range(e0, e0 + plane)) if e0 < o.n else [])
+    res["ghosts_ok"] = p.ghosts().tolist() == want
+    xg = np.random.default_rng(3).standard_normal(o.n)
+    y = p.spmv(xg[b0:e0])
+    res["spmv_bitwise"] = bool(y.tobytes() == port.spmv(o, xg)[b0:e0].tobytes())
+    # distributed fast-mode solve vs the oracle
+    x_o, r_o = port.pcg_s_solve(o, s=a.s, tol=1e-8, max_outer=5000)
+    sol = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000))
+    parts = [None] * world
+    dist.all_gather_object(parts, (b0, sol.x))
+    x = np.concatenate([v for _, v in sorted(parts, key=lambda t: t[0])])
+    res["outer"] = [sol.report.outer_iters, r_o.outer_iters]
+    res["outer_ok"] = abs(sol.report.outer_iters - r_o.outer_iters) <= 1
+    res["x_rel"] = float(np.linalg.norm(x - x_o) / np.linalg.norm(x_o))
+    res["allreduces"] = sol.report.device_allreduces
+    res["lambda_rel"] = abs(sol.report.spectrum_used.lambda_min / r_o.lambda_min - 1)
+    pc = p.pcg_solve(tol=1e-8, max_iter=5000)
+    xp, rpcg = port.pcg_solve(o, tol=1e-8, max_iter=5000)
+    parts = [None] * world
+    dist.all_gather_object(parts, (b0, pc.x))
+    x2 = np.concatenate([v for _, v in sorted(parts, key=lambda t: t[0])])
+    res["pcg_iters"] = [pc.report.outer_iters, rpcg.outer_iters]
+    res["pcg_x_rel"] = float(np.linalg.norm(x2 - xp) / np.linalg.norm(xp))
+    allres = [None] * world
+    dist.all_gather_object(allres, res)
+    if rank == 0:
+        print("MGPU " + json.dumps(allres), flush=True)
+    p.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -36,7 +36,8 @@ def _sources():
 
 
 def _headers():
-    return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    return (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+            + glob.glob(os.path.join(ROOT, "include", "chebstep", "*.hpp")))
 
 
 def _stale(target, deps):
@@ -46,12 +47,21 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+CXX = shutil.which("g++") or "g++"
+CUDA_INC = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
+CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+            "-I" + CUDA_INC]
+
+
 def _compile(src, force):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     if not force and not _stale(obj, [src] + _headers()):
         return obj, None
-    cmd = [NVCC, *ARCH, *COMMON, "-Xptxas", "-v" if os.environ.get("CS_PTXAS_V") else "-O3",
-           "-c", src, "-o", obj]
+    if src.endswith(".cpp"):  # host-only C++ (C++20 for the std::span drop-in API)
+        cmd = [CXX, *CXXFLAGS, "-c", src, "-o", obj]
+    else:
+        cmd = [NVCC, *ARCH, *COMMON, "-Xptxas", "-v" if os.environ.get("CS_PTXAS_V") else "-O3",
+               "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         return obj, f"{' '.join(cmd)}\n{r.stdout}\n{r.stderr}"

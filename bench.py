@@ -132,26 +132,39 @@ def nnz_of(stencil, nx, ny, nz):
     return n + 2 * ((nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1))
 
 
-def spmv_alg_bytes(nnz, n, s, outer, lanczos_steps, jacobi=True):
-    """Algorithmic bytes of every SpMV-phase kernel of one solve (DESIGN.md):
-    12 B per nonzero (FP64 value + int32 column), x read once, outputs once."""
-    b_spmv = 12 * nnz + 16 * n                       # y = A x
-    b_resid = 12 * nnz + 24 * n                      # r = b - A x
-    b_dot = 12 * nnz + 16 * n                        # Lanczos t = A v (+ v.t)
-    j = 8 * n if jacobi else 0
-    b_first = 12 * nnz + 16 * n + 8 * n + j + (8 * n if jacobi else 0) + 8 * n  # zp0 rd, zp wr, z wr
-    b_mid = 12 * nnz + 16 * n + 16 * n + j + (8 * n if jacobi else 0) + 8 * n
+def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=True):
+    """Algorithmic bytes of every SpMV-phase kernel of one solve (DESIGN.md 3):
+    the matrix in the format actually stored (SELL-32P: FP64 value slots +
+    per-slice column/pattern/meta bytes) read once, x read once, each output
+    written once, plus the epilogue vectors of each MPK step."""
+    v = 8 * n
+    b_spmv = mat_bytes + 2 * v                       # y = A x
+    b_resid = mat_bytes + 3 * v                      # r = b - A x
+    b_dot = mat_bytes + 2 * v                        # Lanczos t = A v (+ v.t)
+    if mode == "fast":                               # z_q = 2a D^-1 p_q - 2s z_{q-1} - z_{q-2}
+        b_first = mat_bytes + 3 * v                  # x, p, z
+        b_mid = mat_bytes + 4 * v                    # x, p, z_{q-2}, z
+    else:                                            # reference zp recurrence (+ D^-1 vector)
+        j = v if jacobi else 0
+        b_first = mat_bytes + 2 * v + v + j + (v if jacobi else 0) + v
+        b_mid = mat_bytes + 2 * v + 2 * v + j + (v if jacobi else 0) + v
     b_last = b_spmv
-    if s == 1:
-        per_mpk = b_last
-    else:
-        per_mpk = b_first + (s - 2) * b_mid + b_last
+    per_mpk = b_last if s == 1 else b_first + (s - 2) * b_mid + b_last
     mpks = 1 + outer  # setup MPK + one (speculative) MPK per outer iteration (fast algebra)
     return b_resid + lanczos_steps * b_dot + mpks * per_mpk, b_spmv
 
 
+def outer_bytes_format(mat_bytes, n, s):
+    """Per-outer algorithmic bytes of the fast schedule in the stored format:
+    s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+5)."""
+    v = 8 * n
+    mpk = (mat_bytes + 3 * v) + (s - 2) * (mat_bytes + 4 * v) + (mat_bytes + 2 * v) if s > 1 \
+        else mat_bytes + 2 * v
+    return mpk + v * (3 * s + 1) + v * (6 * s + 5)
+
+
 def outer_bytes(nnz, n, s):
-    """B_outer(s) = s*B_spmv + 8n(14s+3) (Jacobi)."""
+    """B_outer(s) = s*B_spmv + 8n(14s+3) (Jacobi, 12 B/nnz CSR/SELL)."""
     return s * (12 * nnz + 16 * n) + 8 * n * (14 * s + 3)
 
 
@@ -300,7 +313,8 @@ def run_ours(args):
 
     # roofline of the dominant kernel (SpMV fused with the MPK epilogue)
     nnz_l = prob.nnz_local
-    alg, b_spmv = spmv_alg_bytes(nnz_l, nl, args.s, rep.outer_iters, cfg.lanczos_steps)
+    mat = prob.device_bytes
+    alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode)
     spmv_ms = phases["spmv"][0]
     achieved = alg * args.steps / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
     peak, peak_src = measured_peak()
@@ -312,13 +326,18 @@ def run_ours(args):
             "traffic_alg_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
             "peak_source": peak_src,
             "spmv_share_of_step": spmv_ms / (t_ms) if t_ms > 0 else None,
-            "alg_bytes_per_spmv": b_spmv}
+            "alg_bytes_per_spmv": b_spmv,
+            "matrix_bytes": mat, "matrix_bytes_per_nnz": mat / nnz_l,
+            "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}
     # whole-solve bandwidth against B_outer
     solve_outer_ms = rep.t_solve_ms / max(rep.outer_iters, 1)
-    b_out = outer_bytes(nnz_l, nl, args.s)
+    b_out = outer_bytes_format(mat, nl, args.s)
+    b_survey = outer_bytes(nnz_l, nl, args.s)
     solve_level = {"t_outer_ms": solve_outer_ms, "B_outer_GB": b_out / 1e9,
                    "achieved_GBps": b_out / (solve_outer_ms / 1e3) / 1e9,
                    "frac_of_peak": b_out / (solve_outer_ms / 1e3) / 1e9 / peak,
+                   "survey_B_outer_GB_12B_per_nnz": b_survey / 1e9,
+                   "survey_roofline_ms_at_peak": b_survey / peak / 1e6,
                    "t_lanczos_ms": rep.t_lanczos_ms, "t_solve_ms": rep.t_solve_ms}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

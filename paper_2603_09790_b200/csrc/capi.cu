@@ -193,7 +193,8 @@ int cs_problem_info(cs_problem* p, int64_t* info) {
     info[2] = p->nnz_local;
     info[3] = p->row_begin;
     info[4] = p->n_ghost;
-    info[5] = static_cast<int64_t>(p->vals.bytes + p->cols.bytes + p->slice_ptr.bytes);
+    info[5] = static_cast<int64_t>(p->vals.bytes + p->cols.bytes + p->pat.bytes + p->meta.bytes +
+                                   p->slice_ptr.bytes);
   });
 }
 

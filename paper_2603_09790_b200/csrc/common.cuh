@@ -37,12 +37,21 @@ struct DevState {
   double scal[8];    // small scalars (classical PCG step, beta ...)
 };
 
+// Pattern-compressed SELL-32 ("SELL-32P"): slice s owns value slots
+// [slice_ptr[s], slice_ptr[s+1]) (32 lanes per slot). meta[s] >= 0: explicit
+// int32 columns at cols[meta[s] + 32k + lane]. meta[s] < 0: the slice's rows share
+// one sorted relative-offset pattern -- slot k of lane l is column row_l + off_k
+// if bit l of mask_k is set (else an empty slot), with {off_k, mask_k} at
+// pat[-meta[s]-1 + k]. Either way a row's entries are visited in its stored
+// (ascending) column order, so sums are bitwise the CSR row-serial sums.
 struct SellView {
   int64_t n_local;
   int64_t nslices;
   const int64_t* __restrict__ slice_ptr;
   const double* __restrict__ vals;
   const int32_t* __restrict__ cols;
+  const int64_t* __restrict__ meta;
+  const int2* __restrict__ pat;
   const double* __restrict__ inv_diag;  // nullptr for identity
 };
 

@@ -32,11 +32,22 @@ void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* gho
                         const int64_t* rowptr, int64_t* col, double* val, cudaStream_t st);
 void scan_rowptr(const int64_t* len, int64_t n, int64_t* rowptr, void* tmp, size_t* tmp_bytes,
                  cudaStream_t st);
+// SELL-32 -> SELL-32P conversion (see SellView): plan per-slice sizes, then fill.
+void launch_compress_plan(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
+                          int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt, cudaStream_t st);
+void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
+                          const double* vals, const int64_t* new_ptr, const int64_t* pat_ptr,
+                          const int64_t* col_ptr, double* nvals, int32_t* ncols, int2* pat,
+                          int64_t* meta, cudaStream_t st);
 // inv_diag[i] = 1/diag[i]; *bad = 1 if any diag <= 0 (precond.cpp:17-22)
 void launch_inv_diag(int64_t n, const double* diag, double* inv_diag, int* bad, cudaStream_t st);
 
 // ------------------------------------------------------------------ SpMV family (spmv.cu)
-enum SpmvKind { kPlain = 0, kResid = 1, kMpkFirst = 2, kMpkMid = 3, kMpkLast = 4, kDot = 5 };
+enum SpmvKind {
+  kPlain = 0, kResid = 1, kMpkFirst = 2, kMpkMid = 3, kMpkLast = 4, kDot = 5,
+  // fast algebra: z_q = ca*D^-1 p_q + cb*z_{q-1} + cc*z_{q-2}, no zp vectors, D from the row
+  kMpkFirstF = 6, kMpkMidF = 7
+};
 struct SpmvArgs {
   const double* x = nullptr;   // operand (owned + ghost slots)
   double* y = nullptr;         // A x (p column, r, ...)

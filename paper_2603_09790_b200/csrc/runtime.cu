@@ -250,6 +250,55 @@ int64_t read_i64(cs_ctx* c, const int64_t* dev) {
   return v;
 }
 
+// Convert the freshly assembled explicit SELL-32 into SELL-32P (common.cuh):
+// pattern-compressed slices drop their 4 B/slot column stream.
+void compress_sell(cs_problem* p) {
+  cs_ctx* c = p->ctx;
+  const int64_t ns = p->nslices;
+  DBuf cnt(sizeof(int64_t) * 3 * std::max<int64_t>(ns, 1));
+  DBuf ptrs(sizeof(int64_t) * 3 * (ns + 1));
+  int64_t* val_cnt = cnt.as<int64_t>();
+  int64_t* pat_cnt = val_cnt + ns;
+  int64_t* col_cnt = pat_cnt + ns;
+  int64_t* new_ptr = ptrs.as<int64_t>();
+  int64_t* pat_ptr = new_ptr + (ns + 1);
+  int64_t* col_ptr = pat_ptr + (ns + 1);
+  launch_compress_plan(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), val_cnt, pat_cnt,
+                       col_cnt, c->stream);
+  size_t tb = 0;
+  scan_slice_ptr(val_cnt, ns, new_ptr, nullptr, &tb, c->stream);
+  DBuf tmp(tb);
+  for (int64_t* pair : {val_cnt, pat_cnt, col_cnt}) {
+    int64_t* out = pair == val_cnt ? new_ptr : pair == pat_cnt ? pat_ptr : col_ptr;
+    if (ns > 0) scan_slice_ptr(pair, ns, out, tmp.p, &tb, c->stream);
+    else CS_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), c->stream));
+  }
+  const int64_t nval = read_i64(c, new_ptr + ns);
+  const int64_t npat = read_i64(c, pat_ptr + ns);
+  const int64_t ncol = read_i64(c, col_ptr + ns);
+  DBuf nvals(sizeof(double) * std::max<int64_t>(nval, 1));
+  DBuf ncols(sizeof(int32_t) * std::max<int64_t>(ncol, 1));
+  p->pat.alloc(sizeof(int2) * std::max<int64_t>(npat, 1));
+  p->meta.alloc(sizeof(int64_t) * std::max<int64_t>(ns, 1));
+  launch_compress_fill(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), p->vals.as<double>(),
+                       new_ptr, pat_ptr, col_ptr, nvals.as<double>(), ncols.as<int32_t>(),
+                       p->pat.as<int2>(), p->meta.as<int64_t>(), c->stream);
+  DBuf nptr(sizeof(int64_t) * (ns + 1));
+  CS_CUDA(cudaMemcpyAsync(nptr.p, new_ptr, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToDevice,
+                          c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  p->vals = std::move(nvals);
+  p->cols = std::move(ncols);
+  p->slice_ptr = std::move(nptr);
+  int64_t nc = 0;
+  {
+    std::vector<int64_t> h(ns);
+    if (ns) CS_CUDA(cudaMemcpy(h.data(), pat_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost));
+    for (int64_t v : h) nc += v > 0;
+  }
+  p->compressed_slices = nc;
+}
+
 }  // namespace
 
 cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
@@ -304,6 +353,7 @@ cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_
   p->diag.alloc(sizeof(double) * std::max<int64_t>(p->n_local, 1));
   launch_stencil_fill(d, p->n_local, p->nslices, p->slice_ptr.as<int64_t>(), p->vals.as<double>(),
                       p->cols.as<int32_t>(), p->diag.as<double>(), c->stream);
+  compress_sell(p.get());
   // ghost global ids: plane z0-1 then plane z1
   for (int64_t i = 0; i < p->ghost_lo; ++i) p->ghosts_host.push_back(r0 - plane + i);
   for (int64_t i = 0; i < p->ghost_hi; ++i) p->ghosts_host.push_back(r1 + i);
@@ -365,6 +415,7 @@ cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, cons
   CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CS_CUDA(cudaStreamSynchronize(c->stream));
   if (hbad) fail(CS_ERR_INVALID_MATRIX, 0, "column index out of range");
+  compress_sell(p.get());
   p->ghost_global.alloc(8);
   return p.release();
 }

@@ -91,7 +91,8 @@ struct cs_problem {
   int64_t ghost_lo = 0, ghost_hi = 0, send_lo = 0, send_hi = 0;
   int gen_kind = -1;
   int64_t nx = 0, ny = 0, nz = 0;
-  csg::DBuf slice_ptr, vals, cols, diag, inv_diag, ghost_global;
+  csg::DBuf slice_ptr, vals, cols, meta, pat, diag, inv_diag, ghost_global;
+  int64_t compressed_slices = 0;
   std::vector<int64_t> ghosts_host;
   int precond = CS_PRECOND_IDENTITY;
   // cached solve workspace
@@ -104,6 +105,8 @@ struct cs_problem {
     v.slice_ptr = slice_ptr.as<int64_t>();
     v.vals = vals.as<double>();
     v.cols = cols.as<int32_t>();
+    v.meta = meta.as<int64_t>();
+    v.pat = pat.as<int2>();
     v.inv_diag = precond == CS_PRECOND_JACOBI ? inv_diag.as<double>() : nullptr;
     return v;
   }

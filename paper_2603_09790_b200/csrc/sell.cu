@@ -194,6 +194,15 @@ __global__ void csr_fill_kernel(int64_t n, const int64_t* __restrict__ rowptr,
   }
 }
 
+// column of slot k of `lane` in slice `slice`, or -1 for an empty slot
+__device__ __forceinline__ int32_t slot_col(const SellView& a, int64_t slice, int64_t base, int k,
+                                            int lane, int64_t row) {
+  const int64_t m = a.meta[slice];
+  if (m >= 0) return a.cols[m + k * kSliceRows + lane];
+  const int2 e = a.pat[-m - 1 + k];
+  return ((e.y >> lane) & 1) ? static_cast<int32_t>(row + e.x) : -1;
+}
+
 __global__ void sell_row_len_kernel(SellView a, int64_t* len) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (row >= a.n_local) return;
@@ -203,7 +212,7 @@ __global__ void sell_row_len_kernel(SellView a, int64_t* len) {
   const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
   int cnt = 0;
   for (int k = 0; k < width; ++k)
-    if (a.cols[base + k * kSliceRows + lane] >= 0) ++cnt;
+    if (slot_col(a, slice, base, k, lane, row) >= 0) ++cnt;
   len[row] = cnt;
 }
 
@@ -219,11 +228,107 @@ __global__ void sell_to_csr_kernel(SellView a, int64_t row_begin,
   const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
   int64_t o = rowptr[row];
   for (int k = 0; k < width; ++k) {
-    const int32_t c = a.cols[base + k * kSliceRows + lane];
+    const int32_t c = slot_col(a, slice, base, k, lane, row);
     if (c < 0) continue;
     col[o] = c < a.n_local ? row_begin + c : ghost_global[c - a.n_local];
     val[o] = a.vals[base + k * kSliceRows + lane];
     ++o;
+  }
+}
+
+// ---------------------------------------------------------------- SELL-32 -> SELL-32P
+// A slice is pattern-compressed when every row's columns are strictly ascending
+// and the union U of the rows' relative offsets (col - row) is small enough that
+// 32U value slots + U pattern entries cost less than 32W values + 32W columns.
+// The union is built by a warp-wide merge of the 32 sorted offset lists.
+constexpr int kSentinel = 0x7fffffff;
+
+__device__ __forceinline__ int lane_offset(const int32_t* cols, int64_t base, int idx, int len,
+                                           int64_t row) {
+  return idx < len ? static_cast<int>(cols[base + idx * kSliceRows] - row) : kSentinel;
+}
+
+__global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
+                                     const int32_t* __restrict__ cols, int64_t* val_cnt,
+                                     int64_t* pat_cnt, int64_t* col_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (slice >= nslices) return;
+  const int64_t row = slice * kSliceRows + lane;
+  const int64_t base = slice_ptr[slice] + lane;
+  const int W = static_cast<int>((slice_ptr[slice + 1] - slice_ptr[slice]) >> 5);
+  int len = 0;
+  bool sorted = true;
+  int32_t prev = -1;
+  for (int k = 0; k < W; ++k) {
+    const int32_t c = cols[base + k * kSliceRows];
+    if (c < 0) break;  // trailing padding
+    if (c <= prev) sorted = false;
+    prev = c;
+    ++len;
+  }
+  bool ok = __all_sync(0xffffffffu, sorted) && W > 0;
+  int U = 0;
+  if (ok) {
+    int idx = 0;
+    for (;;) {
+      const int cur = lane_offset(cols, base, idx, len, row);
+      const int m = __reduce_min_sync(0xffffffffu, cur);
+      if (m == kSentinel) break;
+      ++U;
+      if (264 * U > 384 * W) {
+        ok = false;
+        break;
+      }
+      if (cur == m) ++idx;
+    }
+  }
+  if (lane == 0) {
+    val_cnt[slice] = static_cast<int64_t>(kSliceRows) * (ok ? U : W);
+    pat_cnt[slice] = ok ? U : 0;
+    col_cnt[slice] = ok ? 0 : static_cast<int64_t>(kSliceRows) * W;
+  }
+}
+
+__global__ void compress_fill_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
+                                     const int32_t* __restrict__ cols,
+                                     const double* __restrict__ vals,
+                                     const int64_t* __restrict__ new_ptr,
+                                     const int64_t* __restrict__ pat_ptr,
+                                     const int64_t* __restrict__ col_ptr, double* nvals,
+                                     int32_t* ncols, int2* pat, int64_t* meta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (slice >= nslices) return;
+  const int64_t row = slice * kSliceRows + lane;
+  const int64_t base = slice_ptr[slice] + lane;
+  const int W = static_cast<int>((slice_ptr[slice + 1] - slice_ptr[slice]) >> 5);
+  const int64_t nb = new_ptr[slice] + lane;
+  const int64_t U = pat_ptr[slice + 1] - pat_ptr[slice];
+  if (U > 0) {
+    int len = 0;
+    for (int k = 0; k < W; ++k) {
+      if (cols[base + k * kSliceRows] < 0) break;
+      ++len;
+    }
+    int idx = 0;
+    for (int u = 0; u < U; ++u) {
+      const int cur = lane_offset(cols, base, idx, len, row);
+      const int m = __reduce_min_sync(0xffffffffu, cur);
+      const bool hit = cur == m;
+      const unsigned mask = __ballot_sync(0xffffffffu, hit);
+      nvals[nb + u * kSliceRows] = hit ? vals[base + idx * kSliceRows] : 0.0;
+      if (lane == 0) pat[pat_ptr[slice] + u] = make_int2(m, static_cast<int>(mask));
+      if (hit) ++idx;
+    }
+    if (lane == 0) meta[slice] = -pat_ptr[slice] - 1;
+  } else {
+    const int64_t cb = col_ptr[slice] + lane;
+    for (int k = 0; k < W; ++k) {
+      nvals[nb + k * kSliceRows] = vals[base + k * kSliceRows];
+      ncols[cb + k * kSliceRows] = cols[base + k * kSliceRows];
+    }
+    if (lane == 0) meta[slice] = col_ptr[slice];
   }
 }
 
@@ -294,6 +399,24 @@ void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* gho
                         const int64_t* rowptr, int64_t* col, double* val, cudaStream_t st) {
   sell_to_csr_kernel<<<grid_for(a.n_local), kThreads, 0, st>>>(a, row_begin, ghost_global, rowptr,
                                                               col, val);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_compress_plan(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
+                          int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt, cudaStream_t st) {
+  if (nslices == 0) return;
+  compress_plan_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(nslices, slice_ptr, cols,
+                                                                    val_cnt, pat_cnt, col_cnt);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
+                          const double* vals, const int64_t* new_ptr, const int64_t* pat_ptr,
+                          const int64_t* col_ptr, double* nvals, int32_t* ncols, int2* pat,
+                          int64_t* meta, cudaStream_t st) {
+  if (nslices == 0) return;
+  compress_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
+      nslices, slice_ptr, cols, vals, new_ptr, pat_ptr, col_ptr, nvals, ncols, pat, meta);
   CS_CUDA(cudaGetLastError());
 }
 

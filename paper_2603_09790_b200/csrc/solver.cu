@@ -265,7 +265,7 @@ Blocks workspace(cs_problem* p, int s) {
 
 // MPK steps 1..s on a basis whose z_0 is already in Z column 0 (mpk.cpp:53-69).
 void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int pending,
-               DevState* st) {
+               DevState* st, bool fast = false) {
   const int64_t ld = p->ld;
   const double alpha = 2.0 / (hi - lo);           // mpk.hpp:22
   const double sigma = (hi + lo) / (hi - lo);     // mpk.hpp:23-25
@@ -282,8 +282,8 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     g.x = zcol(q - 1);
     g.y = bk.P + (q - 1) * ld;
     g.zp1 = zp(q - 1);
-    g.zp2 = q >= 2 ? zp(q - 2) : nullptr;
-    g.zpout = jac ? zp(q) : nullptr;
+    g.zp2 = q >= 2 ? (fast ? zcol(q - 2) : zp(q - 2)) : nullptr;
+    g.zpout = jac && !fast ? zp(q) : nullptr;
     g.zout = zcol(q);
     if (q == 1) {
       g.ca = alpha;
@@ -297,7 +297,8 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     g.col = q;
     g.pending = pending;
     g.st = st;
-    spmv_halo(p, q == 1 ? kMpkFirst : kMpkMid, g, zcol(q - 1));
+    const int kind = fast ? (q == 1 ? kMpkFirstF : kMpkMidF) : (q == 1 ? kMpkFirst : kMpkMid);
+    spmv_halo(p, kind, g, zcol(q - 1));
   }
   SpmvArgs g;
   g.x = zcol(s - 1);
@@ -456,7 +457,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     Launch L(c, CS_PHASE_UPDATE);
     launch_precond_apply(n, A.inv_diag, bk.r, bk.Z, st, 0, 0, c->stream);
   }
-  mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st);
+  mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st, mode == CS_MODE_FAST);
   std::swap(bk.Q, bk.Z);  // q = basis.z ; aq = basis.p.columns(1, s)
   std::swap(bk.AQ, bk.P);
   ua.q = bk.Q;
@@ -478,7 +479,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
       Launch L(c, CS_PHASE_UPDATE);
       launch_fast_update(ua, c->stream);
     }
-    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st);
+    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true);
     packed_reduce(bk.Q, bk.Z);
     small(launch_fast_step);
   };

@@ -18,6 +18,10 @@
 //              z_q = M^-1 zp_q; finite check                (mpk.cpp:60-66)
 //   kMpkLast   p_s = A z_{s-1}; finite check on p_s (label s-1, mpk.cpp:68-69)
 //   kDot       y = A x and the deterministic block sum of x.y (classical PCG p.q)
+//   kMpkFirstF/kMpkMidF (fast algebra only): with Jacobi zp_j = D z_j, so
+//              z_q = 2a D^-1 p_q - 2s z_{q-1} - z_{q-2}  (first step: a, -s, no z_{q-2});
+//              D = a_ii and z_{q-1}[row] are picked up by the row loop itself, so
+//              the step reads/writes 24n fewer bytes than the reference recurrence.
 #include "kernels.cuh"
 
 namespace csg {
@@ -40,20 +44,41 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int warp = threadIdx.x >> 5;
   const int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   const bool active = slice < slice_end;
-  double acc = 0.0;
+  double acc = 0.0, dval = 1.0, xd = 0.0;
   int64_t row = 0;
   if (active) {
     row = slice * kSliceRows + lane;
     const int64_t base = a.slice_ptr[slice];
     const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
     const double* vp = a.vals + base + lane;
-    const int32_t* cp = a.cols + base + lane;
     const double* __restrict__ x = g.x;
+    auto term = [&](int32_t c, double v) {
+      const double xv = __ldg(x + c);
+      acc = __dadd_rn(acc, __dmul_rn(v, xv));
+      if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
+        if (c == row) {
+          dval = v;
+          xd = xv;
+        }
+      }
+    };
+    const int64_t m = a.meta[slice];
+    if (m >= 0) {  // explicit int32 columns
+      const int32_t* cp = a.cols + m + lane;
 #pragma unroll 9
-    for (int k = 0; k < width; ++k) {
-      const int32_t c = __ldcs(cp + k * kSliceRows);
-      const double v = __ldcs(vp + k * kSliceRows);
-      if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
+      for (int k = 0; k < width; ++k) {
+        const int32_t c = __ldcs(cp + k * kSliceRows);
+        const double v = __ldcs(vp + k * kSliceRows);
+        if (c >= 0) term(c, v);
+      }
+    } else {  // shared relative-offset pattern: column = row + off_k where lane bit set
+      const int2* pp = a.pat + (-m - 1);
+#pragma unroll 9
+      for (int k = 0; k < width; ++k) {
+        const int2 e = __ldg(pp + k);
+        const double v = __ldcs(vp + k * kSliceRows);
+        if ((e.y >> lane) & 1) term(static_cast<int32_t>(row + e.x), v);
+      }
     }
   }
   const bool own = active && row < a.n_local;
@@ -74,6 +99,14 @@ __global__ void __launch_bounds__(kWarps * 32)
         g.zpout[row] = zp;
         z = __dmul_rn(a.inv_diag[row], zp);
       }
+      g.zout[row] = z;
+      if (!isfinite(z)) report(g, g.col);
+    } else if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
+      g.y[row] = acc;
+      if constexpr (!JAC) xd = g.x[row];  // identity: z_{q-1}[row] even without a stored diagonal
+      const double dp = JAC ? acc / dval : acc;
+      double z = fma(g.cb, xd, g.ca * dp);
+      if constexpr (KIND == kMpkMidF) z = fma(g.cc, g.zp2[row], z);
       g.zout[row] = z;
       if (!isfinite(z)) report(g, g.col);
     } else if constexpr (KIND == kMpkLast) {
@@ -134,6 +167,8 @@ void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t sb, int
     case kMpkMid: launch_kind<kMpkMid>(jac, a, g, sb, se, st); break;
     case kMpkLast: launch_kind<kMpkLast>(false, a, g, sb, se, st); break;
     case kDot: launch_kind<kDot>(false, a, g, sb, se, st); break;
+    case kMpkFirstF: launch_kind<kMpkFirstF>(jac, a, g, sb, se, st); break;
+    case kMpkMidF: launch_kind<kMpkMidF>(jac, a, g, sb, se, st); break;
     default: throw LibError{9, 0, "bad spmv kind"};
   }
   CS_CUDA(cudaGetLastError());

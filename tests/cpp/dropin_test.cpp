@@ -106,11 +106,14 @@ int main() {
   const cs::SolveResult pcg = cs::pcg_solve(sys.a, b, x0, jac, 1e-9, 1000);
   EXPECT(pcg.report.converged);
 
-  // --- error convention: A = I, M = I, auto spectrum, s = 4
+  // --- error convention: A = I, M = I, s = 4, interval [0.9, 1.1] (the auto
+  // estimate's widening of lambda = 1): z_1 = (alpha - sigma) r = 0 exactly, so the
+  // Gram diagonal vanishes -> SolverBreakdownError at outer 1
   const cs::CsrMatrix eye = cs::CsrMatrix::identity(40);
   const std::vector<double> b40(40, 1.0), z40(40, 0.0);
   cs::SolverConfig c4;
   c4.s = 4;
+  c4.spectrum = cs::SpectrumEstimate{0.9, 1.1};
   cs::gpu::set_mode(cs::gpu::Mode::reference);
   bool thrown = false;
   try {

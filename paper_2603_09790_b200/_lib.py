@@ -11,7 +11,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libchebstep_gpu.so")
+LIB_PATH = os.environ.get("CS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "lib", "libchebstep_gpu.so")
 
 CS_OK = 0
 CS_ERR_DIMENSION = 1
@@ -96,6 +97,7 @@ SIGNATURES = {
     "cs_random_vector": (C.c_int, [_vp, C.c_int64, C.c_uint64, _f64p]),
     "cs_tridiag_eigvals": (C.c_int, [C.c_int, _f64p, _f64p, _f64p]),
     "cs_estimate_interval": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_int, _dp, _dp]),
+    "cs_bench_spmv": (C.c_int, [_vp, C.c_int, C.c_int, _dp]),
     "cs_config_default": (None, [C.POINTER(CsConfig)]),
     "cs_pcg_s_solve": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(CsConfig), _f64p,
                                  C.POINTER(CsReport)]),

@@ -53,6 +53,12 @@ CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.joi
             "-I" + CUDA_INC]
 
 
+EXTRA = [f"-D{d}" for d in os.environ.get("CS_DEFINES", "").split() if d]
+if EXTRA:  # experiment builds go to their own object dir / library
+    OBJ = OBJ + "_" + "_".join(d[2:] for d in EXTRA)
+    LIB = os.environ.get("CS_LIB_OUT", LIB)
+
+
 def _compile(src, force):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     if not force and not _stale(obj, [src] + _headers()):
@@ -60,8 +66,8 @@ def _compile(src, force):
     if src.endswith(".cpp"):  # host-only C++ (C++20 for the std::span drop-in API)
         cmd = [CXX, *CXXFLAGS, "-c", src, "-o", obj]
     else:
-        cmd = [NVCC, *ARCH, *COMMON, "-Xptxas", "-v" if os.environ.get("CS_PTXAS_V") else "-O3",
-               "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *EXTRA,
+               "-Xptxas", "-v" if os.environ.get("CS_PTXAS_V") else "-O3", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         return obj, f"{' '.join(cmd)}\n{r.stdout}\n{r.stderr}"

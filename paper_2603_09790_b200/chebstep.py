@@ -326,6 +326,13 @@ class DeviceProblem:
         _check(lib.cs_mpk(self.handle, r, s, params.lambda_min, params.lambda_max, z, p))
         return MpkResult(z.reshape(s, self.n_local).T, p.reshape(s + 1, self.n_local).T)
 
+    def bench_spmv(self, kind: str = "plain", reps: int = 20) -> float:
+        """Average ms of one SpMV-family launch timed alone (CUDA events)."""
+        k = {"plain": 0, "mpk_ref": 1, "mpk_fast": 2}[kind]
+        ms = C.c_double()
+        _check(lib.cs_bench_spmv(self.handle, k, reps, C.byref(ms)))
+        return ms.value
+
     def estimate_interval(self, steps: int = 40, seed: int = 1234, mode: str = "fast"):
         lo, hi = C.c_double(), C.c_double()
         _check(lib.cs_estimate_interval(self.handle, steps, seed, _mode(mode), C.byref(lo),

@@ -237,6 +237,48 @@ int cs_spmv(cs_problem* p, const double* x, double* y) {
   });
 }
 
+int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
+  return guard([&] {
+    cs_ctx* c = p->ctx;
+    CS_CUDA(cudaSetDevice(c->device));
+    if (reps < 1 || kind < 0 || kind > 2) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad bench args");
+    const int64_t ld = p->ld;
+    DBuf buf(sizeof(double) * ld * 6);
+    double* v = buf.as<double>();
+    {
+      Launch L(c, CS_PHASE_OTHER);
+      launch_random_vector(ld * 6, 0, 99, v, c->stream);
+    }
+    SpmvArgs g;
+    g.x = v;
+    g.y = v + ld;
+    g.zp1 = v + 2 * ld;
+    g.zp2 = v + 3 * ld;
+    g.zpout = p->precond == CS_PRECOND_JACOBI ? v + 4 * ld : nullptr;
+    g.zout = v + 5 * ld;
+    g.ca = 1.0;
+    g.cb = -0.5;
+    g.cc = -1.0;
+    const int k = kind == 0 ? kPlain : kind == 1 ? kMpkMid : kMpkMidF;
+    cudaEvent_t a, b;
+    CS_CUDA(cudaEventCreate(&a));
+    CS_CUDA(cudaEventCreate(&b));
+    launch_spmv(k, p->view(), g, 0, p->nslices, c->stream);  // warm-up
+    CS_CUDA(cudaEventRecord(a, c->stream));
+    for (int i = 0; i < reps; ++i) {
+      Launch L(c, CS_PHASE_SPMV);
+      launch_spmv(k, p->view(), g, 0, p->nslices, c->stream);
+    }
+    CS_CUDA(cudaEventRecord(b, c->stream));
+    CS_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_launch = ms / reps;
+  });
+}
+
 int cs_mpk(cs_problem* p, const double* r, int s, double lo, double hi, double* z, double* pblk) {
   return guard([&] {
     cs_ctx* c = p->ctx;

@@ -13,6 +13,8 @@
 //    entries keep ascending GLOBAL column order, so per-row summation order
 //    is partition-invariant.
 //  * CSR -> SELL conversion for uploaded reference CsrMatrix data.
+#include <cstdlib>
+
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.cuh"
@@ -250,7 +252,7 @@ __device__ __forceinline__ int lane_offset(const int32_t* cols, int64_t base, in
 
 __global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
                                      const int32_t* __restrict__ cols, int64_t* val_cnt,
-                                     int64_t* pat_cnt, int64_t* col_cnt) {
+                                     int64_t* pat_cnt, int64_t* col_cnt, int allow) {
   const int lane = threadIdx.x & 31;
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices) return;
@@ -267,7 +269,7 @@ __global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict_
     prev = c;
     ++len;
   }
-  bool ok = __all_sync(0xffffffffu, sorted) && W > 0;
+  bool ok = __all_sync(0xffffffffu, sorted) && W > 0 && allow;
   int U = 0;
   if (ok) {
     int idx = 0;
@@ -405,8 +407,10 @@ void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* gho
 void launch_compress_plan(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
                           int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt, cudaStream_t st) {
   if (nslices == 0) return;
+  // CS_SELL_EXPLICIT=1 keeps every slice explicit (format A/B experiments)
+  static const int allow = std::getenv("CS_SELL_EXPLICIT") ? 0 : 1;
   compress_plan_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(nslices, slice_ptr, cols,
-                                                                    val_cnt, pat_cnt, col_cnt);
+                                                                    val_cnt, pat_cnt, col_cnt, allow);
   CS_CUDA(cudaGetLastError());
 }
 

@@ -27,7 +27,13 @@
 namespace csg {
 namespace {
 
-constexpr int kWarps = 8;  // slices per 256-thread block
+constexpr int kWarps = 8;  // warps per 256-thread block
+#ifndef CS_SPMV_MINB
+#define CS_SPMV_MINB 8  // 32 registers: full occupancy (64 warps / SM)
+#endif
+#ifndef CS_SPMV_PERSIST
+#define CS_SPMV_PERSIST 1
+#endif
 
 __device__ __forceinline__ void report(const SpmvArgs& g, int col) {
   if (g.st == nullptr) return;
@@ -36,86 +42,124 @@ __device__ __forceinline__ void report(const SpmvArgs& g, int col) {
   if (!g.pending) g.st->done = 1;
 }
 
+struct SliceMeta {
+  int64_t base, end, meta;
+};
+
+__device__ __forceinline__ SliceMeta load_meta(const SellView& a, int64_t slice, int64_t se) {
+  SliceMeta m{0, 0, 0};
+  if (slice < se) {
+    m.base = a.slice_ptr[slice];
+    m.end = a.slice_ptr[slice + 1];
+    m.meta = a.meta[slice];
+  }
+  return m;
+}
+
+// One row of one slice: sum_k v_k * x[c_k] in stored order, acc = acc + v*x.
+__device__ __forceinline__ double row_sum(const SellView& a, const double* __restrict__ x,
+                                          const SliceMeta& sm, int64_t row, int lane) {
+  double acc = 0.0;
+  const int width = static_cast<int>((sm.end - sm.base) >> 5);
+  const double* vp = a.vals + sm.base + lane;
+  if (sm.meta >= 0) {  // explicit int32 columns
+    const int32_t* cp = a.cols + sm.meta + lane;
+#pragma unroll 9
+    for (int k = 0; k < width; ++k) {
+      const int32_t c = __ldcs(cp + k * kSliceRows);
+      const double v = __ldcs(vp + k * kSliceRows);
+      if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
+    }
+  } else if (width <= 32) {  // shared relative-offset pattern: column = row + off_k
+    // lane k holds pattern entry k; every slot's {off, mask} arrives by shuffle
+    const int2* pp = a.pat + (-sm.meta - 1);
+    const int2 pl = lane < width ? __ldg(pp + lane) : make_int2(0, 0);
+#pragma unroll 9
+    for (int k = 0; k < width; ++k) {
+      const int off = __shfl_sync(0xffffffffu, pl.x, k);
+      const unsigned msk = static_cast<unsigned>(__shfl_sync(0xffffffffu, pl.y, k));
+      const double v = __ldcs(vp + k * kSliceRows);
+      if ((msk >> lane) & 1u) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + row + off)));
+    }
+  } else {  // wide pattern: broadcast entry loads
+    const int2* pp = a.pat + (-sm.meta - 1);
+    for (int k = 0; k < width; ++k) {
+      const int2 e = __ldg(pp + k);
+      const double v = __ldcs(vp + k * kSliceRows);
+      if ((e.y >> lane) & 1) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + row + e.x)));
+    }
+  }
+  return acc;
+}
+
+// Persistent warps walk slices with a grid stride; the next slice's metadata
+// and the epilogue operands of the current rows are loaded ahead of the row
+// sums so that their latency overlaps the value/x stream.
 template <int KIND, bool JAC>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, CS_SPMV_MINB)
     sell_kernel(SellView a, SpmvArgs g, int64_t slice_begin, int64_t slice_end) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
-  const bool active = slice < slice_end;
-  double acc = 0.0, dval = 1.0, xd = 0.0;
-  int64_t row = 0;
-  if (active) {
-    row = slice * kSliceRows + lane;
-    const int64_t base = a.slice_ptr[slice];
-    const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
-    const double* vp = a.vals + base + lane;
-    const double* __restrict__ x = g.x;
-    auto term = [&](int32_t c, double v) {
-      const double xv = __ldg(x + c);
-      acc = __dadd_rn(acc, __dmul_rn(v, xv));
-      if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
-        if (c == row) {
-          dval = v;
-          xd = xv;
-        }
-      }
-    };
-    const int64_t m = a.meta[slice];
-    if (m >= 0) {  // explicit int32 columns
-      const int32_t* cp = a.cols + m + lane;
-#pragma unroll 9
-      for (int k = 0; k < width; ++k) {
-        const int32_t c = __ldcs(cp + k * kSliceRows);
-        const double v = __ldcs(vp + k * kSliceRows);
-        if (c >= 0) term(c, v);
-      }
-    } else {  // shared relative-offset pattern: column = row + off_k where lane bit set
-      const int2* pp = a.pat + (-m - 1);
-#pragma unroll 9
-      for (int k = 0; k < width; ++k) {
-        const int2 e = __ldg(pp + k);
-        const double v = __ldcs(vp + k * kSliceRows);
-        if ((e.y >> lane) & 1) term(static_cast<int32_t>(row + e.x), v);
-      }
-    }
-  }
-  const bool own = active && row < a.n_local;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  const double* __restrict__ x = g.x;
   double dotv = 0.0;
-  if (own) {
-    if constexpr (KIND == kPlain) {
-      g.y[row] = acc;
-    } else if constexpr (KIND == kResid) {
-      g.y[row] = __dsub_rn(g.b[row], acc);
-    } else if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
-      g.y[row] = acc;
-      const double y1 = g.zp1[row];
-      const double y2 = (KIND == kMpkFirst) ? y1 : g.zp2[row];
-      const double t = __dadd_rn(__dmul_rn(g.ca, acc), __dmul_rn(g.cb, y1));
-      const double zp = __dadd_rn(t, __dmul_rn(g.cc, y2));
-      double z = zp;
-      if constexpr (JAC) {
-        g.zpout[row] = zp;
-        z = __dmul_rn(a.inv_diag[row], zp);
+  SliceMeta sm = load_meta(a, slice, slice_end);
+  for (; slice < slice_end; slice += wstride) {
+    const SliceMeta next = load_meta(a, slice + wstride, slice_end);
+    const int64_t row = slice * kSliceRows + lane;
+    const bool own = row < a.n_local;
+    // epilogue operands first (independent of the row sum)
+    double e1 = 0.0, e2 = 0.0, einv = 1.0, exd = 0.0;
+    if (own) {
+      if constexpr (KIND == kResid) e1 = g.b[row];
+      if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
+        e1 = g.zp1[row];
+        if constexpr (KIND == kMpkMid) e2 = g.zp2[row];
+        if constexpr (JAC) einv = a.inv_diag[row];
       }
-      g.zout[row] = z;
-      if (!isfinite(z)) report(g, g.col);
-    } else if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
-      g.y[row] = acc;
-      if constexpr (!JAC) xd = g.x[row];  // identity: z_{q-1}[row] even without a stored diagonal
-      const double dp = JAC ? acc / dval : acc;
-      double z = fma(g.cb, xd, g.ca * dp);
-      if constexpr (KIND == kMpkMidF) z = fma(g.cc, g.zp2[row], z);
-      g.zout[row] = z;
-      if (!isfinite(z)) report(g, g.col);
-    } else if constexpr (KIND == kMpkLast) {
-      g.y[row] = acc;
-      if (!isfinite(acc)) report(g, g.col);
-    } else if constexpr (KIND == kDot) {
-      g.y[row] = acc;
-      dotv = g.x[row] * acc;
+      if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
+        exd = x[row];
+        if constexpr (KIND == kMpkMidF) e2 = g.zp2[row];
+        if constexpr (JAC) einv = a.inv_diag[row];
+      }
+      if constexpr (KIND == kDot) exd = x[row];
     }
+    const double acc = row_sum(a, x, sm, row, lane);
+    if (own) {
+      if constexpr (KIND == kPlain) {
+        g.y[row] = acc;
+      } else if constexpr (KIND == kResid) {
+        g.y[row] = __dsub_rn(e1, acc);
+      } else if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
+        g.y[row] = acc;
+        const double y2 = (KIND == kMpkFirst) ? e1 : e2;
+        const double t = __dadd_rn(__dmul_rn(g.ca, acc), __dmul_rn(g.cb, e1));
+        const double zp = __dadd_rn(t, __dmul_rn(g.cc, y2));
+        double z = zp;
+        if constexpr (JAC) {
+          g.zpout[row] = zp;
+          z = __dmul_rn(einv, zp);
+        }
+        g.zout[row] = z;
+        if (!isfinite(z)) report(g, g.col);
+      } else if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
+        g.y[row] = acc;
+        const double dp = JAC ? acc * einv : acc;
+        double z = fma(g.cb, exd, g.ca * dp);
+        if constexpr (KIND == kMpkMidF) z = fma(g.cc, e2, z);
+        g.zout[row] = z;
+        if (!isfinite(z)) report(g, g.col);
+      } else if constexpr (KIND == kMpkLast) {
+        g.y[row] = acc;
+        if (!isfinite(acc)) report(g, g.col);
+      } else if constexpr (KIND == kDot) {
+        g.y[row] = acc;
+        dotv += exd * acc;
+      }
+    }
+    sm = next;
   }
   if constexpr (KIND == kDot) {
     // fixed-shape tree: warp shuffle, then warp 0 over the 8 warp sums
@@ -142,10 +186,17 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+int spmv_grid(int64_t nslices) {
+  const int64_t want = (nslices + kWarps - 1) / kWarps;
+  if (!CS_SPMV_PERSIST) return static_cast<int>(want > 0 ? want : 1);
+  const int64_t cap = 148 * (64 / kWarps);  // one wave of resident blocks at full occupancy
+  return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
 template <int KIND>
 void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,
                  cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>((se - sb + kWarps - 1) / kWarps);
+  const unsigned grid = static_cast<unsigned>(spmv_grid(se - sb));
   if (jac)
     sell_kernel<KIND, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
   else
@@ -154,7 +205,7 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
 
 }  // namespace
 
-int spmv_dot_blocks(int64_t nslices) { return static_cast<int>((nslices + kWarps - 1) / kWarps); }
+int spmv_dot_blocks(int64_t nslices) { return spmv_grid(nslices); }
 
 void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,
                  cudaStream_t st) {

@@ -23,3 +23,17 @@ for _ in range(a.solves):
     r = p.pcg_s_solve(cfg=cfg)
     print(f"outer={r.report.outer_iters} launches={r.report.kernel_launches} "
           f"t_solve_ms={r.report.t_solve_ms:.1f} t_lanczos_ms={r.report.t_lanczos_ms:.1f}")
+if a.solves >= 1:
+    ctx = cs.default_context()
+    ctx.reset_timing()
+    ctx.set_timing(True)
+    r = p.pcg_s_solve(cfg=cfg)
+    ctx.set_timing(False)
+    t = ctx.timing()
+    mat = p.device_bytes
+    n = p.n_local
+    per = {k: (round(v[0], 3), v[1], round(v[0] / max(v[1], 1), 4)) for k, v in t.items() if v[1]}
+    print("timed solve: outer", r.report.outer_iters, "phases (ms, launches, ms/launch):", per)
+    sp = t["spmv"]
+    print(f"matrix {mat/1e9:.3f} GB ({mat/p.nnz_local:.2f} B/nnz); spmv avg {sp[0]/sp[1]:.4f} ms "
+          f"-> {(mat + 24*n)/(sp[0]/sp[1]/1e3)/1e9:.0f} GB/s (mat+3 vectors)")

@@ -1,0 +1,21 @@
+"""Time the SpMV-family kernels alone on a device-generated problem.
+
+    python tools/spmv_micro.py [--n 256] [--stencil poisson27]
+"""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_09790_b200 as cs  # noqa: E402
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=256)
+ap.add_argument("--stencil", default="poisson27")
+a = ap.parse_args()
+p = cs.DeviceProblem.generate(a.stencil, a.n, a.n, a.n).set_precond("jacobi")
+n, mat = p.n_local, p.device_bytes
+v = 8 * n
+res = {}
+for kind, extra in (("plain", 2 * v), ("mpk_ref", 7 * v), ("mpk_fast", 4 * v)):
+    ms = p.bench_spmv(kind, 20)
+    res[kind] = (round(ms, 4), round((mat + extra) / (ms / 1e3) / 1e9))
+print(f"{os.environ.get('CS_LIB', 'default')} {a.stencil} {a.n}^3 mat {mat/p.nnz_local:.2f} B/nnz "
+      f"explicit={bool(os.environ.get('CS_SELL_EXPLICIT'))}: " +
+      " ".join(f"{k}={v[0]}ms/{v[1]}GB/s" for k, v in res.items()))

@@ -192,9 +192,11 @@ int cs_tridiag_eigvals(int m, const double* diag, const double* off, double* out
 int cs_estimate_interval(cs_problem* p, int steps, uint64_t seed, int mode, double* lambda_min,
                          double* lambda_max);
 
-/* Time one SpMV-family kernel alone on device-resident data (CUDA events):
- * kind 0 = y = A x, 1 = fused MPK middle step (reference recurrence),
- * 2 = fused MPK middle step (fast recurrence). Average ms per launch. */
+/* Time one solve kernel alone on device-resident data (CUDA events), for
+ * roofline measurements: kind 0 = y = A x, 1 = fused MPK middle step
+ * (reference recurrence), 2 = fused MPK middle step (fast recurrence),
+ * 3 = packed one-allreduce reduction (s = 8), 4 = fused update pass (s = 8).
+ * Average ms per launch. */
 int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch);
 
 /* ------------------------------------------------------------ solves */

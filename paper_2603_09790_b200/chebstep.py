@@ -328,7 +328,7 @@ class DeviceProblem:
 
     def bench_spmv(self, kind: str = "plain", reps: int = 20) -> float:
         """Average ms of one SpMV-family launch timed alone (CUDA events)."""
-        k = {"plain": 0, "mpk_ref": 1, "mpk_fast": 2}[kind]
+        k = {"plain": 0, "mpk_ref": 1, "mpk_fast": 2, "pack8": 3, "update8": 4}[kind]
         ms = C.c_double()
         _check(lib.cs_bench_spmv(self.handle, k, reps, C.byref(ms)))
         return ms.value

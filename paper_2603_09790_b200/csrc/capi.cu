@@ -3,6 +3,7 @@
 // message and payload, mirroring the reference's exception types
 // (errors.hpp:9-56) so the C++ and Python layers can re-raise them.
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "runtime.cuh"
@@ -241,33 +242,66 @@ int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
-    if (reps < 1 || kind < 0 || kind > 2) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad bench args");
-    const int64_t ld = p->ld;
-    DBuf buf(sizeof(double) * ld * 6);
+    if (reps < 1 || kind < 0 || kind > 4) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad bench args");
+    const int64_t ld = p->ld, n = p->n_local;
+    constexpr int S = 8;
+    const int nvec = kind <= 2 ? 6 : 4 * S + 4;
+    DBuf buf(sizeof(double) * ld * nvec), small(sizeof(double) * (4 * S * S + 4096) + 4096);
     double* v = buf.as<double>();
     {
       Launch L(c, CS_PHASE_OTHER);
-      launch_random_vector(ld * 6, 0, 99, v, c->stream);
+      launch_random_vector(ld * nvec, 0, 99, v, c->stream);
     }
+    double* sm = small.as<double>();
+    CS_CUDA(cudaMemsetAsync(sm, 0, small.bytes, c->stream));
+    DBuf part(sizeof(double) * (pack_partial_doubles(S, n) + 64));
+    std::function<void()> run;
     SpmvArgs g;
-    g.x = v;
-    g.y = v + ld;
-    g.zp1 = v + 2 * ld;
-    g.zp2 = v + 3 * ld;
-    g.zpout = p->precond == CS_PRECOND_JACOBI ? v + 4 * ld : nullptr;
-    g.zout = v + 5 * ld;
-    g.ca = 1.0;
-    g.cb = -0.5;
-    g.cc = -1.0;
-    const int k = kind == 0 ? kPlain : kind == 1 ? kMpkMid : kMpkMidF;
+    UpdateArgs ua{};
+    if (kind <= 2) {
+      g.x = v;
+      g.y = v + ld;
+      g.zp1 = v + 2 * ld;
+      g.zp2 = v + 3 * ld;
+      g.zpout = p->precond == CS_PRECOND_JACOBI ? v + 4 * ld : nullptr;
+      g.zout = v + 5 * ld;
+      g.ca = 1.0;
+      g.cb = -0.5;
+      g.cc = -1.0;
+      const int k = kind == 0 ? kPlain : kind == 1 ? kMpkMid : kMpkMidF;
+      run = [&, k] { launch_spmv(k, p->view(), g, 0, p->nslices, c->stream); };
+    } else if (kind == 3) {
+      unsigned* ticket = reinterpret_cast<unsigned*>(sm + 4 * S * S + 2048);
+      run = [&, ticket] {
+        launch_pack(S, n, ld, v, v + S * ld, v + 2 * S * ld, v + 3 * S * ld, sm, part.as<double>(),
+                    ticket, nullptr, c->stream);
+      };
+    } else {
+      ua.s = S;
+      ua.n = n;
+      ua.ld = ld;
+      ua.q = v;
+      ua.aq = v + S * ld;
+      ua.z = v + 2 * S * ld;
+      ua.zw = v + 2 * S * ld;
+      ua.p = v + 3 * S * ld;
+      ua.x = v + 4 * S * ld;
+      ua.r = v + (4 * S + 1) * ld;
+      ua.inv_diag = p->view().inv_diag;
+      ua.alpha = sm;
+      ua.beta = sm + S;
+      ua.st = c->state.as<DevState>();
+      CS_CUDA(cudaMemsetAsync(c->state.p, 0, sizeof(DevState), c->stream));
+      run = [&] { launch_fast_update(ua, c->stream); };
+    }
     cudaEvent_t a, b;
     CS_CUDA(cudaEventCreate(&a));
     CS_CUDA(cudaEventCreate(&b));
-    launch_spmv(k, p->view(), g, 0, p->nslices, c->stream);  // warm-up
+    run();  // warm-up
     CS_CUDA(cudaEventRecord(a, c->stream));
     for (int i = 0; i < reps; ++i) {
-      Launch L(c, CS_PHASE_SPMV);
-      launch_spmv(k, p->view(), g, 0, p->nslices, c->stream);
+      Launch L(c, kind <= 2 ? CS_PHASE_SPMV : kind == 3 ? CS_PHASE_REDUCE : CS_PHASE_UPDATE);
+      run();
     }
     CS_CUDA(cudaEventRecord(b, c->stream));
     CS_CUDA(cudaEventSynchronize(b));

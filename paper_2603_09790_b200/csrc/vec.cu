@@ -150,8 +150,11 @@ struct PackShape {
   static constexpr size_t smem_bytes = smem_warp * kPackWarps * sizeof(double);
 };
 
+#ifndef CS_PACK_MINB
+#define CS_PACK_MINB 2
+#endif
 template <int S>
-__global__ void __launch_bounds__(kPackWarps * 32)
+__global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     pack_kernel(int64_t n, int64_t ld, const double* __restrict__ Q, const double* __restrict__ Z,
                 const double* __restrict__ P, const double* __restrict__ r, double* packed,
                 double* partial, unsigned* ticket, DevState* st) {
@@ -264,7 +267,8 @@ __global__ void __launch_bounds__(kPackWarps * 32)
 int pack_grid(int64_t n) {
   const int64_t chunks = (n + 31) / 32;
   const int64_t want = (chunks + kPackWarps - 1) / kPackWarps;
-  return static_cast<int>(want < 148 * 3 ? (want > 0 ? want : 1) : 148 * 3);
+  const int64_t cap = 148 * (CS_PACK_MINB > 2 ? CS_PACK_MINB : 3);
+  return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
 template <int S>

@@ -292,8 +292,7 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = Clocks(local)
     barrier()
-    ctx.reset_timing()
-    ctx.set_timing(True)
+    # (1) the headline: K solves, no per-launch instrumentation
     l0 = ctx.launches()
     clocks.start()
     e0.record(ext)
@@ -301,10 +300,20 @@ def run_ours(args):
     e1.record(ext)
     e1.synchronize()
     clk = clocks.stop()
-    ctx.set_timing(False)
     launches = ctx.launches() - l0
     t_ms = e0.elapsed_time(e1)
     t_max = ctx.allreduce_max(t_ms)
+    barrier()
+    # (2) the same K solves again with CUDA events around every launch: per-phase
+    # kernel times for the roofline (instrumentation overhead reported)
+    ctx.reset_timing()
+    ctx.set_timing(True)
+    e0.record(ext)
+    reps_t = [step() for _ in range(args.steps)]
+    e1.record(ext)
+    e1.synchronize()
+    ctx.set_timing(False)
+    t_inst = e0.elapsed_time(e1)
     barrier()
     phases = ctx.timing()
     rep = reps[-1]
@@ -316,7 +325,9 @@ def run_ours(args):
     mat = prob.device_bytes
     alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode)
     spmv_ms = phases["spmv"][0]
-    achieved = alg * args.steps / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
+    alg_t = sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps, args.mode)[0]
+                for r in reps_t)
+    achieved = alg_t / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
     peak, peak_src = measured_peak()
     tr = ncu_traffic()
     roof = {"kernel": "sell_kernel<kMpk*> (SELL-32 FP64 SpMV + fused MPK epilogue)",
@@ -325,7 +336,10 @@ def run_ours(args):
             "traffic": tr.get("bytes_per_launch") if tr else None,
             "traffic_alg_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
             "peak_source": peak_src,
-            "spmv_share_of_step": spmv_ms / (t_ms) if t_ms > 0 else None,
+            "spmv_share_of_step": spmv_ms / t_inst if t_inst > 0 else None,
+            "measured": "CUDA events around every launch of K instrumented solves run right "
+                        "after the timed region (instrumentation overhead %.1f%%)" %
+                        (100 * (t_inst / t_ms - 1) if t_ms > 0 else 0),
             "alg_bytes_per_spmv": b_spmv,
             "matrix_bytes": mat, "matrix_bytes_per_nnz": mat / nnz_l,
             "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}

@@ -227,6 +227,7 @@ int cs_spmv(cs_problem* p, const double* x, double* y) {
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
     DBuf dx(sizeof(double) * p->ld), dy(sizeof(double) * p->ld);
     CS_CUDA(cudaMemcpyAsync(dx.p, x, sizeof(double) * p->n_local, cudaMemcpyHostToDevice, c->stream));
     SpmvArgs g;
@@ -242,6 +243,7 @@ int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
     if (reps < 1 || kind < 0 || kind > 4) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad bench args");
     const int64_t ld = p->ld, n = p->n_local;
     constexpr int S = 8;
@@ -317,6 +319,7 @@ int cs_mpk(cs_problem* p, const double* r, int s, double lo, double hi, double* 
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
     if (s < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "mpk: s must be >= 1");
     if (!(hi > lo) || !(lo > 0.0) || !std::isfinite(hi))
       fail(CS_ERR_INVALID_ARGUMENT, 0, "ChebyshevParams: need lambda_max > lambda_min > 0");
@@ -352,6 +355,7 @@ int cs_block_gram(cs_ctx* ctx, int64_t n, int ku, int kv, const double* u, const
                   double* g, int mode) {
   return guard([&] {
     CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
     if (ku < 0 || kv < 0 || ku > kMaxS || kv > kMaxS)
       fail(CS_ERR_DIMENSION, 0, "SmallDense: dimensions must be in [0, 64]");
     if (ku == 0 || kv == 0) return;
@@ -377,6 +381,7 @@ int cs_block_update(cs_ctx* ctx, int64_t n, int m, int k, const double* y, const
                     const double* c, double* out) {
   return guard([&] {
     CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
     if (m > kMaxS || k > kMaxS) fail(CS_ERR_DIMENSION, 0, "SmallDense: dimensions must be in [0, 64]");
     HostIn dy(ctx, y, sizeof(double) * n * k), dx(ctx, x, sizeof(double) * n * m),
         dc(ctx, c, sizeof(double) * m * k);
@@ -395,6 +400,7 @@ int cs_assemble_gram(cs_ctx* ctx, int64_t n, int k, const double* q, const doubl
                      int mode) {
   return guard([&] {
     CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
     if (k < 1 || k > kMaxS) fail(CS_ERR_DIMENSION, 0, "SmallDense: dimensions must be in [0, 64]");
     HostIn dq(ctx, q, sizeof(double) * n * k), da(ctx, aq, sizeof(double) * n * k);
     DBuf dw(sizeof(double) * k * k), part(sizeof(double) * tree_gram_partial_doubles(n, k, k)),
@@ -425,6 +431,7 @@ int cs_fgs_solve(cs_ctx* ctx, int s, const double* w, int k, const double* rhs, 
                  double* x, double* delta) {
   return guard([&] {
     CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
     if (s < 1 || k < 1 || s > kMaxS || k > kMaxS)
       fail(CS_ERR_DIMENSION, 0, "SmallDense: dimensions must be in [0, 64]");
     if (nu < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "fgs: nu must be >= 1");
@@ -448,6 +455,7 @@ int cs_fgs_solve(cs_ctx* ctx, int s, const double* w, int k, const double* rhs, 
 int cs_cholesky_solve(cs_ctx* ctx, int s, const double* w, int k, const double* rhs, double* x) {
   return guard([&] {
     CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
     if (s < 1 || k < 1 || s > kMaxS || k > kMaxS)
       fail(CS_ERR_DIMENSION, 0, "SmallDense: dimensions must be in [0, 64]");
     HostIn dw(ctx, w, sizeof(double) * s * s), dr(ctx, rhs, sizeof(double) * s * k);
@@ -469,6 +477,7 @@ int cs_cholesky_solve(cs_ctx* ctx, int s, const double* w, int k, const double* 
 int cs_random_vector(cs_ctx* ctx, int64_t n, uint64_t seed, double* out) {
   return guard([&] {
     CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
     DBuf d(sizeof(double) * n);
     {
       Launch L(ctx, CS_PHASE_OTHER);
@@ -517,6 +526,7 @@ int cs_pcg_s_solve(cs_problem* p, const double* b, const double* x0, const cs_co
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
     const size_t bytes = sizeof(double) * p->n_local;
     HostIn db(c, b, bytes), dx0(c, x0, bytes);
     DBuf dx(bytes);
@@ -531,6 +541,7 @@ int cs_pcg_solve(cs_problem* p, const double* b, const double* x0, double tol, i
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
     const size_t bytes = sizeof(double) * p->n_local;
     HostIn db(c, b, bytes), dx0(c, x0, bytes);
     DBuf dx(bytes);

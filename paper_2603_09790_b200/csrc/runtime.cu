@@ -7,6 +7,8 @@
 
 namespace csg {
 
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 [[noreturn]] void fail(int code, int payload, const std::string& msg) {
   throw LibError{code, payload, msg};
 }
@@ -177,6 +179,11 @@ cs_ctx* ctx_create(int device) {
   CS_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
   CS_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
   CS_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  // keep freed pool memory cached for reuse (repeated solves / uploads)
+  cudaMemPool_t pool;
+  CS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = ~uint64_t{0};
+  CS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   c->state.alloc(sizeof(DevState));
   CS_CUDA(cudaMallocHost(&c->pinned, 4096));
   return c.release();
@@ -191,6 +198,11 @@ void ctx_destroy(cs_ctx* c) {
     cudaEventDestroy(s.b);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  // pooled buffers are freed on the context stream: release them before it goes
+  c->scratch.release();
+  c->normbuf.release();
+  c->state.release();
+  cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
   cudaEventDestroy(c->ev_ready);
   cudaEventDestroy(c->ev_halo);
@@ -203,6 +215,7 @@ void ctx_destroy(cs_ctx* c) {
 void comm_init(cs_ctx* c, int nranks, int rank, const unsigned char id[128]) {
   if (nranks < 1 || rank < 0 || rank >= nranks) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad rank");
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   if (c->comm) {
     ncclCommDestroy(c->comm);
     c->comm = nullptr;
@@ -311,6 +324,7 @@ cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_
   if (nx > kMaxN / ny || nx * ny > kMaxN / nz)
     fail(CS_ERR_INVALID_ARGUMENT, 0, "poisson27: grid size overflow");
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   auto p = std::make_unique<cs_problem>();
   p->ctx = c;
   p->gen_kind = kind;
@@ -375,6 +389,7 @@ cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, cons
   const int64_t nnz = rowptr[n];
   if (nnz < 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[n] must equal nnz");
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   auto p = std::make_unique<cs_problem>();
   p->ctx = c;
   p->n_global = p->n_local = n;
@@ -423,6 +438,7 @@ cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, cons
 void problem_set_precond(cs_problem* p, int kind) {
   cs_ctx* c = p->ctx;
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   if (kind == CS_PRECOND_IDENTITY) {
     p->precond = kind;
     return;
@@ -446,6 +462,7 @@ void problem_set_precond(cs_problem* p, int kind) {
 void problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val) {
   cs_ctx* c = p->ctx;
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   const int64_t n = p->n_local;
   DBuf len(sizeof(int64_t) * std::max<int64_t>(n, 1)), rp(sizeof(int64_t) * (n + 1));
   const SellView A = p->view();

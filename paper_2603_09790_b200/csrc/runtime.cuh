@@ -17,19 +17,35 @@
 
 namespace csg {
 
+// Stream the current library call allocates on (set by bind_stream for the
+// duration of a context/problem operation). With a stream bound, buffers come
+// from the device's stream-ordered memory pool (cudaMallocAsync), which the
+// context configures to retain freed memory -- so repeated solves/uploads reuse
+// HBM instead of cudaMalloc/cudaFree-ing tens of GB per call.
+extern thread_local cudaStream_t g_alloc_stream;
+struct StreamBind {
+  cudaStream_t prev;
+  explicit StreamBind(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~StreamBind() { g_alloc_stream = prev; }
+};
+
 // RAII device buffer
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t stream = nullptr;  // allocation stream (pool) or nullptr (cudaMalloc)
+  bool pooled = false;
   DBuf() = default;
   explicit DBuf(size_t b) { alloc(b); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), stream(o.stream), pooled(o.pooled) {
+    o.p = nullptr, o.bytes = 0;
+  }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p, bytes = o.bytes;
+      p = o.p, bytes = o.bytes, stream = o.stream, pooled = o.pooled;
       o.p = nullptr, o.bytes = 0;
     }
     return *this;
@@ -38,11 +54,21 @@ struct DBuf {
   void alloc(size_t b) {
     release();
     if (b == 0) b = 8;
-    CS_CUDA(cudaMalloc(&p, b));
+    if (g_alloc_stream != nullptr) {
+      CS_CUDA(cudaMallocAsync(&p, b, g_alloc_stream));
+      stream = g_alloc_stream;
+      pooled = true;
+    } else {
+      CS_CUDA(cudaMalloc(&p, b));
+      pooled = false;
+    }
     bytes = b;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, stream);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -78,6 +104,7 @@ struct cs_ctx {
   // scratch
   csg::DBuf state;      // DevState
   csg::DBuf scratch;    // partials / tickets / scalars
+  csg::DBuf normbuf;    // ||b|| reduction scratch
   size_t scratch_bytes = 0;
   void* pinned = nullptr;  // pinned host staging for flags
 };
@@ -95,9 +122,10 @@ struct cs_problem {
   int64_t compressed_slices = 0;
   std::vector<int64_t> ghosts_host;
   int precond = CS_PRECOND_IDENTITY;
-  // cached solve workspace
+  // cached solve workspace and Lanczos basis (reused across solves)
   int ws_s = -1;
   csg::DBuf ws;
+  csg::DBuf lz;
   csg::SellView view() const {
     csg::SellView v;
     v.n_local = n_local;

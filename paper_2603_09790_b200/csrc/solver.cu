@@ -86,8 +86,9 @@ void dot_into(cs_problem* p, const double* u, const double* v, double* dev, int 
 
 double host_norm(cs_problem* p, const double* v, int mode) {
   cs_ctx* c = p->ctx;
-  DBuf tmp(sizeof(double) * (tree_gram_partial_doubles(p->n_local, 1, 1) + 64));
-  Arena ar{tmp.as<char>()};
+  const size_t need = sizeof(double) * (tree_gram_partial_doubles(p->n_local, 1, 1) + 64) + 1024;
+  if (c->normbuf.bytes < need) c->normbuf.alloc(need);
+  Arena ar{c->normbuf.as<char>()};
   double* d = ar.take<double>(1);
   unsigned* ticket = ar.take<unsigned>(1);
   double* partial = ar.take<double>(tree_gram_partial_doubles(p->n_local, 1, 1));
@@ -111,9 +112,24 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
   if (mode == CS_MODE_REFERENCE && c->nranks > 1)
     fail(CS_ERR_INVALID_ARGUMENT, 0, "reference mode is single-GPU");
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   const int64_t n = p->n_local, ld = p->ld;
-  DBuf work(sizeof(double) * (static_cast<size_t>(2 * steps + 3) * ld));
-  double* V = work.as<double>();
+  // The 2*steps basis vectors are cached on the problem; when HBM is short
+  // (512^3: 86 GB of basis next to a 43 GB matrix) the solve workspace is
+  // released first and reallocated after the estimate.
+  const size_t lz_bytes = sizeof(double) * (static_cast<size_t>(2 * steps + 3) * ld);
+  if (p->lz.bytes < lz_bytes) {
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    p->lz.release();
+    size_t free_b = 0, total_b = 0;
+    CS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (free_b < lz_bytes + (size_t{1} << 30)) {
+      p->ws.release();
+      p->ws_s = -1;
+    }
+    p->lz.alloc(lz_bytes);
+  }
+  double* V = p->lz.as<double>();
   double* G = V + steps * ld;
   double* t = G + steps * ld;
   double* r = t + ld;
@@ -326,6 +342,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
                     const cs_config& cfg, double* x_dev, cs_report* rep) {
   cs_ctx* c = p->ctx;
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   // SolverConfig::validate, solver.cpp:15-22
   if (cfg.s < 1 || cfg.s > kMaxS) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: s must be in [1, 64]");
   if (!(cfg.tol > 0.0)) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: tol must be > 0");
@@ -358,7 +375,14 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     return;
   }
   double lo = cfg.lambda_min, hi = cfg.lambda_max, t_lz = 0.0;
-  if (!cfg.has_spectrum) estimate_interval_dev(p, cfg.lanczos_steps, cfg.seed, mode, &lo, &hi, &t_lz);
+  if (!cfg.has_spectrum) {
+    estimate_interval_dev(p, cfg.lanczos_steps, cfg.seed, mode, &lo, &hi, &t_lz);
+    if (p->ws_s != s) {  // the estimate released the workspace for memory: rebuild, re-stage b/x0
+      bk = workspace(p, s);
+      CS_CUDA(cudaMemcpyAsync(bk.x, x0_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+      CS_CUDA(cudaMemcpyAsync(bk.b, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
   rep->lambda_min = lo;
   rep->lambda_max = hi;
   if (!(hi > lo) || !(lo > 0.0) || !std::isfinite(hi))  // mpk.cpp:11-16
@@ -582,6 +606,7 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
                    int max_iter, int mode, double* x_dev, cs_report* rep) {
   cs_ctx* c = p->ctx;
   CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
   if (!(tol >= 0.0) || max_iter < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "pcg_solve: bad tol/max_iter");
   if (mode == CS_MODE_REFERENCE && c->nranks > 1)
     fail(CS_ERR_INVALID_ARGUMENT, 0, "reference mode is single-GPU");

@@ -2,6 +2,9 @@
 // catches library / CUDA errors and returns a CS_* status with a thread-local
 // message and payload, mirroring the reference's exception types
 // (errors.hpp:9-56) so the C++ and Python layers can re-raise them.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -66,6 +69,25 @@ void to_host(cs_ctx* c, void* h, const void* d, size_t bytes) {
 }
 
 void sync(cs_ctx* c) { CS_CUDA(cudaStreamSynchronize(c->stream)); }
+
+// CS_TRACE=1: host-side phase timestamps of the drop-in entries on stderr
+struct Trace {
+  const char* what;
+  cudaStream_t st;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  Trace(const char* w, cudaStream_t s) : what(w), st(s), on(std::getenv("CS_TRACE") != nullptr) {
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cs-trace] %s %s %.1f ms\n", what, phase,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 void small_status(int st) {
   if (st == 0) return;
@@ -562,14 +584,23 @@ int cs_pcg_s_solve_csr(cs_ctx* ctx, int64_t n, const int64_t* rowptr, const int6
     if (!(cfg->tol > 0.0)) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: tol must be > 0");
     if (cfg->max_outer < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: max_outer must be >= 1");
     if (cfg->nu < 1) fail(CS_ERR_INVALID_ARGUMENT, 0, "SolverConfig: nu must be >= 1");
+    CS_CUDA(cudaSetDevice(ctx->device));
+    StreamBind bind_stream_(ctx->stream);
+    Trace tr("cs_pcg_s_solve_csr", ctx->stream);
     std::unique_ptr<cs_problem> p(problem_upload_csr(ctx, n, rowptr, col, val));
+    tr.mark("upload+SELL-32P");
     problem_set_precond(p.get(), precond);
     const size_t bytes = sizeof(double) * n;
     HostIn db(ctx, b, bytes), dx0(ctx, x0, bytes);
     DBuf dx(bytes);
+    tr.mark("precond+vectors");
     pcgs_solve_dev(p.get(), db.d.as<double>(), dx0.d.as<double>(), *cfg, dx.as<double>(), rep);
+    tr.mark("solve");
     to_host(ctx, x, dx.p, bytes);
     sync(ctx);
+    tr.mark("download");
+    p.reset();
+    tr.mark("release");
   });
 }
 

@@ -53,6 +53,7 @@ struct SellView {
   const int64_t* __restrict__ meta;
   const int2* __restrict__ pat;
   const double* __restrict__ inv_diag;  // nullptr for identity
+  int max_width;                        // widest slice (slots)
 };
 
 __host__ __device__ inline unsigned long long make_err(int code, int payload) {

@@ -303,13 +303,18 @@ void compress_sell(cs_problem* p) {
   p->vals = std::move(nvals);
   p->cols = std::move(ncols);
   p->slice_ptr = std::move(nptr);
-  int64_t nc = 0;
+  int64_t nc = 0, wmax = 0;
   {
-    std::vector<int64_t> h(ns);
-    if (ns) CS_CUDA(cudaMemcpy(h.data(), pat_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> h(ns), w(ns);
+    if (ns) {
+      CS_CUDA(cudaMemcpy(h.data(), pat_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost));
+      CS_CUDA(cudaMemcpy(w.data(), val_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost));
+    }
     for (int64_t v : h) nc += v > 0;
+    for (int64_t v : w) wmax = std::max(wmax, v / kSliceRows);
   }
   p->compressed_slices = nc;
+  p->max_width = static_cast<int>(wmax);
 }
 
 }  // namespace

@@ -120,6 +120,7 @@ struct cs_problem {
   int64_t nx = 0, ny = 0, nz = 0;
   csg::DBuf slice_ptr, vals, cols, meta, pat, diag, inv_diag, ghost_global;
   int64_t compressed_slices = 0;
+  int max_width = 0;
   std::vector<int64_t> ghosts_host;
   int precond = CS_PRECOND_IDENTITY;
   // cached solve workspace and Lanczos basis (reused across solves)
@@ -135,6 +136,7 @@ struct cs_problem {
     v.cols = cols.as<int32_t>();
     v.meta = meta.as<int64_t>();
     v.pat = pat.as<int2>();
+    v.max_width = max_width;
     v.inv_diag = precond == CS_PRECOND_JACOBI ? inv_diag.as<double>() : nullptr;
     return v;
   }

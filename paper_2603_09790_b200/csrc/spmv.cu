@@ -92,6 +92,92 @@ __device__ __forceinline__ double row_sum(const SellView& a, const double* __res
   return acc;
 }
 
+// ------------------------------------------------------------------ shared pieces
+
+struct EpiOps {
+  double e1 = 0.0, e2 = 0.0, einv = 1.0, exd = 0.0;
+};
+
+// epilogue operands of one row, loaded ahead of (independent of) the row sum
+template <int KIND, bool JAC>
+__device__ __forceinline__ EpiOps epi_load(const SellView& a, const SpmvArgs& g, int64_t row) {
+  EpiOps e;
+  if constexpr (KIND == kResid) e.e1 = g.b[row];
+  if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
+    e.e1 = g.zp1[row];
+    if constexpr (KIND == kMpkMid) e.e2 = g.zp2[row];
+    if constexpr (JAC) e.einv = a.inv_diag[row];
+  }
+  if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
+    e.exd = g.x[row];
+    if constexpr (KIND == kMpkMidF) e.e2 = g.zp2[row];
+    if constexpr (JAC) e.einv = a.inv_diag[row];
+  }
+  if constexpr (KIND == kDot) e.exd = g.x[row];
+  return e;
+}
+
+template <int KIND, bool JAC>
+__device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double acc,
+                                          const EpiOps& e, double& dotv) {
+  if constexpr (KIND == kPlain) {
+    g.y[row] = acc;
+  } else if constexpr (KIND == kResid) {
+    g.y[row] = __dsub_rn(e.e1, acc);
+  } else if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
+    g.y[row] = acc;
+    const double y2 = (KIND == kMpkFirst) ? e.e1 : e.e2;
+    const double t = __dadd_rn(__dmul_rn(g.ca, acc), __dmul_rn(g.cb, e.e1));
+    const double zp = __dadd_rn(t, __dmul_rn(g.cc, y2));
+    double z = zp;
+    if constexpr (JAC) {
+      g.zpout[row] = zp;
+      z = __dmul_rn(e.einv, zp);
+    }
+    g.zout[row] = z;
+    if (!isfinite(z)) report(g, g.col);
+  } else if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
+    g.y[row] = acc;
+    const double dp = JAC ? acc * e.einv : acc;
+    double z = fma(g.cb, e.exd, g.ca * dp);
+    if constexpr (KIND == kMpkMidF) z = fma(g.cc, e.e2, z);
+    g.zout[row] = z;
+    if (!isfinite(z)) report(g, g.col);
+  } else if constexpr (KIND == kMpkLast) {
+    g.y[row] = acc;
+    if (!isfinite(acc)) report(g, g.col);
+  } else if constexpr (KIND == kDot) {
+    g.y[row] = acc;
+    dotv += e.exd * acc;
+  }
+}
+
+// kDot: fixed-shape block tree, then last-block finalisation in block order
+__device__ __forceinline__ void dot_finish(const SpmvArgs& g, double dotv) {
+  __shared__ double red[kWarps];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) dotv += __shfl_down_sync(0xffffffffu, dotv, off);
+  if (lane == 0) red[warp] = dotv;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kWarps; ++w) s += red[w];
+    g.partial[blockIdx.x] = s;
+    __threadfence();
+    const unsigned t = atomicAdd(g.ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    finalize_partials(g.partial, gridDim.x, 1, g.result);
+    if (threadIdx.x == 0) *g.ticket = 0u;
+  }
+}
+
+// ------------------------------------------------------------------ LDG kernel
 // Persistent warps walk slices with a grid stride; the next slice's metadata
 // and the epilogue operands of the current rows are loaded ahead of the row
 // sums so that their latency overlaps the value/x stream.
@@ -103,88 +189,153 @@ __global__ void __launch_bounds__(kWarps * 32, CS_SPMV_MINB)
   const int warp = threadIdx.x >> 5;
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
   int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
-  const double* __restrict__ x = g.x;
   double dotv = 0.0;
   SliceMeta sm = load_meta(a, slice, slice_end);
   for (; slice < slice_end; slice += wstride) {
     const SliceMeta next = load_meta(a, slice + wstride, slice_end);
     const int64_t row = slice * kSliceRows + lane;
     const bool own = row < a.n_local;
-    // epilogue operands first (independent of the row sum)
-    double e1 = 0.0, e2 = 0.0, einv = 1.0, exd = 0.0;
-    if (own) {
-      if constexpr (KIND == kResid) e1 = g.b[row];
-      if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
-        e1 = g.zp1[row];
-        if constexpr (KIND == kMpkMid) e2 = g.zp2[row];
-        if constexpr (JAC) einv = a.inv_diag[row];
-      }
-      if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
-        exd = x[row];
-        if constexpr (KIND == kMpkMidF) e2 = g.zp2[row];
-        if constexpr (JAC) einv = a.inv_diag[row];
-      }
-      if constexpr (KIND == kDot) exd = x[row];
-    }
-    const double acc = row_sum(a, x, sm, row, lane);
-    if (own) {
-      if constexpr (KIND == kPlain) {
-        g.y[row] = acc;
-      } else if constexpr (KIND == kResid) {
-        g.y[row] = __dsub_rn(e1, acc);
-      } else if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
-        g.y[row] = acc;
-        const double y2 = (KIND == kMpkFirst) ? e1 : e2;
-        const double t = __dadd_rn(__dmul_rn(g.ca, acc), __dmul_rn(g.cb, e1));
-        const double zp = __dadd_rn(t, __dmul_rn(g.cc, y2));
-        double z = zp;
-        if constexpr (JAC) {
-          g.zpout[row] = zp;
-          z = __dmul_rn(einv, zp);
-        }
-        g.zout[row] = z;
-        if (!isfinite(z)) report(g, g.col);
-      } else if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
-        g.y[row] = acc;
-        const double dp = JAC ? acc * einv : acc;
-        double z = fma(g.cb, exd, g.ca * dp);
-        if constexpr (KIND == kMpkMidF) z = fma(g.cc, e2, z);
-        g.zout[row] = z;
-        if (!isfinite(z)) report(g, g.col);
-      } else if constexpr (KIND == kMpkLast) {
-        g.y[row] = acc;
-        if (!isfinite(acc)) report(g, g.col);
-      } else if constexpr (KIND == kDot) {
-        g.y[row] = acc;
-        dotv += exd * acc;
-      }
-    }
+    EpiOps e;
+    if (own) e = epi_load<KIND, JAC>(a, g, row);
+    const double acc = row_sum(a, g.x, sm, row, lane);
+    if (own) epi_store<KIND, JAC>(g, row, acc, e, dotv);
     sm = next;
   }
-  if constexpr (KIND == kDot) {
-    // fixed-shape tree: warp shuffle, then warp 0 over the 8 warp sums
-    __shared__ double red[kWarps];
-    __shared__ bool last;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) dotv += __shfl_down_sync(0xffffffffu, dotv, off);
-    if (lane == 0) red[warp] = dotv;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < kWarps; ++w) s += red[w];
-      g.partial[blockIdx.x] = s;
-      __threadfence();
-      const unsigned t = atomicAdd(g.ticket, 1u);
-      last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      finalize_partials(g.partial, gridDim.x, 1, g.result);
-      if (threadIdx.x == 0) *g.ticket = 0u;
-    }
-  }
+  if constexpr (KIND == kDot) dot_finish(g, dotv);
 }
+
+// ------------------------------------------------------------------ TMA kernel
+// A block owns tiles of kWarps consecutive slices; their value slots are one
+// contiguous range of `vals`, streamed into shared memory by a single
+// cp.async.bulk per tile (double-buffered, completion on an mbarrier) two tiles
+// ahead. Meanwhile each thread resolves its row's columns (pattern shuffles or
+// explicit column loads) and issues ALL of its x gathers into registers; after
+// the tile lands the row sum runs in stored order from shared memory + registers.
+constexpr int kXMax = 32;  // slice width served by this kernel
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+template <int KIND, bool JAC>
+__global__ void __launch_bounds__(kWarps * 32, 2)
+    sell_tma_kernel(SellView a, SpmvArgs g, int64_t sb, int64_t se, uint32_t stage_bytes) {
+  if (g.st != nullptr && *(volatile int*)&g.st->done) return;
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  __shared__ __align__(8) uint64_t full[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ntiles = (se - sb + kWarps - 1) / kWarps;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t, int st) {
+    const int64_t s0 = sb + t * kWarps;
+    const int64_t s1 = s0 + kWarps < se ? s0 + kWarps : se;
+    const int64_t vb = a.slice_ptr[s0], ve = a.slice_ptr[s1];
+    const uint32_t bytes = static_cast<uint32_t>((ve - vb) * sizeof(double));
+    mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(tma_smem + st * stage_bytes, a.vals + vb, bytes, &full[st]);
+  };
+  int64_t tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+    if (tile < ntiles) issue(tile, 0);
+    if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+  }
+  uint32_t phase0 = 0, phase1 = 0;
+  int st = 0;
+  double dotv = 0.0;
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t s0 = sb + tile * kWarps;
+    const int64_t slice = s0 + warp;
+    const bool active = slice < se;
+    const int64_t row = slice * kSliceRows + lane;
+    const bool own = active && row < a.n_local;
+    int width = 0;
+    int64_t voff = 0;
+    double xv[kXMax];
+    unsigned valid = 0;  // bit k: slot k contributes to this row
+    EpiOps e;
+    if (active) {
+      const int64_t base = a.slice_ptr[slice];
+      width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
+      voff = base - a.slice_ptr[s0];
+      const int64_t m = a.meta[slice];
+      if (own) e = epi_load<KIND, JAC>(a, g, row);
+      if (m < 0) {
+        const int2* pp = a.pat + (-m - 1);
+        const int2 pl = lane < width ? __ldg(pp + lane) : make_int2(0, 0);
+#pragma unroll
+        for (int k = 0; k < kXMax; ++k) {
+          const int off = __shfl_sync(0xffffffffu, pl.x, k);
+          const unsigned msk = static_cast<unsigned>(__shfl_sync(0xffffffffu, pl.y, k));
+          const bool on = k < width && ((msk >> lane) & 1u);
+          xv[k] = on ? __ldg(g.x + row + off) : 0.0;
+          valid |= on ? (1u << k) : 0u;
+        }
+      } else {
+        const int32_t* cp = a.cols + m + lane;
+#pragma unroll
+        for (int k = 0; k < kXMax; ++k) {
+          const int32_t c = k < width ? __ldcs(cp + k * kSliceRows) : -1;
+          xv[k] = c >= 0 ? __ldg(g.x + c) : 0.0;
+          valid |= c >= 0 ? (1u << k) : 0u;
+        }
+      }
+    }
+    if (st == 0) {
+      mbar_wait(&full[0], phase0);
+      phase0 ^= 1u;
+    } else {
+      mbar_wait(&full[1], phase1);
+      phase1 ^= 1u;
+    }
+    if (active) {
+      const double* vs = reinterpret_cast<const double*>(tma_smem + st * stage_bytes) + voff + lane;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kXMax; ++k)
+        if ((valid >> k) & 1u) acc = __dadd_rn(acc, __dmul_rn(vs[k * kSliceRows], xv[k]));
+      if (own) epi_store<KIND, JAC>(g, row, acc, e, dotv);
+    }
+    __syncthreads();  // every warp is done reading stage st
+    if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile + 2 * gridDim.x, st);
+    }
+    st ^= 1;
+  }
+  if constexpr (KIND == kDot) dot_finish(g, dotv);
+}
+
+#ifndef CS_SPMV_TMA
+#define CS_SPMV_TMA 0  // measured slower on B200 (16 warps/SM at 128 regs); DESIGN.md 3
+#endif
 
 int spmv_grid(int64_t nslices) {
   const int64_t want = (nslices + kWarps - 1) / kWarps;
@@ -193,9 +344,35 @@ int spmv_grid(int64_t nslices) {
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+int tma_grid(int64_t nslices) {
+  const int64_t tiles = (nslices + kWarps - 1) / kWarps;
+  const int64_t cap = 148 * 2;  // 2 resident blocks per SM (2 x 2 stages of shared memory)
+  return static_cast<int>(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+}
+
+bool use_tma(const SellView& a) { return CS_SPMV_TMA && a.max_width > 0 && a.max_width <= kXMax; }
+
+template <int KIND, bool JAC>
+void tma_launch(const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se, cudaStream_t st) {
+  const uint32_t stage = static_cast<uint32_t>(kWarps) * a.max_width * kSliceRows * sizeof(double);
+  static int configured = 0;  // this instantiation: largest dynamic smem enabled so far
+  if (static_cast<int>(2 * stage) > configured) {
+    CS_CUDA(cudaFuncSetAttribute(sell_tma_kernel<KIND, JAC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(2 * stage)));
+    configured = static_cast<int>(2 * stage);
+  }
+  sell_tma_kernel<KIND, JAC><<<tma_grid(se - sb), kWarps * 32, 2 * stage, st>>>(a, g, sb, se, stage);
+}
+
 template <int KIND>
 void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,
                  cudaStream_t st) {
+  if (use_tma(a)) {
+    if (jac) tma_launch<KIND, true>(a, g, sb, se, st);
+    else tma_launch<KIND, false>(a, g, sb, se, st);
+    return;
+  }
   const unsigned grid = static_cast<unsigned>(spmv_grid(se - sb));
   if (jac)
     sell_kernel<KIND, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
@@ -205,7 +382,10 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
 
 }  // namespace
 
-int spmv_dot_blocks(int64_t nslices) { return spmv_grid(nslices); }
+int spmv_dot_blocks(int64_t nslices) {
+  const int a = spmv_grid(nslices), b = tma_grid(nslices);
+  return a > b ? a : b;
+}
 
 void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,
                  cudaStream_t st) {

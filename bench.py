@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--nu", type=int, default=30)
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--mode", default="fast", choices=["fast", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the n^3 grid split into z-slabs over N GPUs (default); "
+                         "weak: n^3 per GPU, global n x n x nN")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -220,8 +223,9 @@ def run_reference(args):
     if rank != 0:
         return 0
     n = args.n
-    n_global = n * n * n * world
-    outer = golden_outer(args.stencil, n, args.s, args.nu, world)
+    wz = world if args.scaling == "weak" else 1
+    n_global = n * n * n * wz
+    outer = golden_outer(args.stencil, n, args.s, args.nu, wz)
     lam = (0.0023, 1.5205)  # 27-pt Jacobi spectrum interval at 128^3; sample only
     src = "golden"
     if outer is None:
@@ -229,15 +233,15 @@ def run_reference(args):
     vals = []
     sample = None
     for i in range(args.warmup + args.steps):
-        sample = cpu_sample(args, lam, world)
+        sample = cpu_sample(args, lam, wz)
         if i >= args.warmup:
             vals.append(n_global / (outer * sample["per_outer_s"]) / 1e9)
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (27-point Poisson, b=1, x0=0)",
-            "config": {"workload": f"{args.stencil}-pt Poisson {n}x{n}x{n*world}, s={args.s}, "
+            "config": {"workload": f"{args.stencil}-pt Poisson {n}x{n}x{n*wz}, s={args.s}, "
                        f"nu={args.nu}, Jacobi, tol {args.tol:g}",
                        "outer_iters": outer, "outer_iters_source": src},
             "ms_per_step": outer * sample["per_outer_s"] * 1e3,
@@ -272,8 +276,9 @@ def run_ours(args):
         torch.distributed.broadcast_object_list(obj, src=0)
         ctx.comm_init(world, rank, obj[0])
     n = args.n
+    nz = n * world if args.scaling == "weak" else n
     kind = "poisson27" if args.stencil == 27 else "poisson7"
-    prob = cs.DeviceProblem.generate(kind, n, n, n * world, ctx=ctx).set_precond("jacobi")
+    prob = cs.DeviceProblem.generate(kind, n, n, nz, ctx=ctx).set_precond("jacobi")
     nl, ng = prob.n_local, prob.n_global
     dev = torch.device("cuda", local)
     b = torch.ones(nl, dtype=torch.float64, device=dev)
@@ -356,10 +361,11 @@ def run_ours(args):
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated 27-point Poisson, b=1, x0=0)",
-            "config": {"workload": f"{args.stencil}-pt Poisson {n}^3 per GPU "
-                       f"(global {n}x{n}x{n*world}), s={args.s}, nu={args.nu}, Jacobi, "
+            "config": {"workload": f"{args.stencil}-pt Poisson global {n}x{n}x{nz} "
+                       f"({'strong' if args.scaling == 'strong' else 'weak'} scaling, "
+                       f"{nz // world} z-planes per GPU), s={args.s}, nu={args.nu}, Jacobi, "
                        f"tol {args.tol:g}, {args.mode} algebra",
                        "n_global": ng, "nnz_local": nnz_l, "outer_iters": rep.outer_iters,
                        "converged": rep.converged,

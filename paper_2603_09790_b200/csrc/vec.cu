@@ -61,19 +61,37 @@ __global__ void random_kernel(int64_t n, int64_t offset, uint64_t seed, double* 
 
 // ------------------------------------------------------------------ serial-order Gram
 
-__global__ void serial_gram_kernel(int64_t n, int ku, int kv, const double* __restrict__ u,
-                                   int64_t ldu, const double* __restrict__ v, int64_t ldv,
-                                   double* g, DevState* st) {
+// One warp per Gram entry. Lanes load 32 consecutive (u_l, v_l) pairs
+// coalesced and form the rounded products; the ONE ascending chain
+// acc = acc + u_l*v_l then runs over the 32 products in lane order (shuffles are
+// off the dependency chain), so the entry is bitwise the reference's serial
+// sum while memory is streamed at full width. Next chunk is prefetched.
+__global__ void __launch_bounds__(128)
+    serial_gram_kernel(int64_t n, int ku, int kv, const double* __restrict__ u, int64_t ldu,
+                       const double* __restrict__ v, int64_t ldv, double* g, DevState* st) {
   if (halted(st)) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (e >= ku * kv) return;
   const int i = e % ku, j = e / ku;
   const double* ui = u + i * ldu;
   const double* vj = v + j * ldv;
   double acc = 0.0;
-#pragma unroll 16
-  for (int64_t l = 0; l < n; ++l) acc = __dadd_rn(acc, __dmul_rn(ui[l], vj[l]));
-  g[e] = acc;
+  double pu = lane < n ? ui[lane] : 0.0, pv = lane < n ? vj[lane] : 0.0;
+  for (int64_t l0 = 0; l0 < n; l0 += 32) {
+    const double prod = __dmul_rn(pu, pv);
+    const int64_t nx = l0 + 32 + lane;
+    pu = nx < n ? ui[nx] : 0.0;  // prefetch the next chunk
+    pv = nx < n ? vj[nx] : 0.0;
+    const int cnt = n - l0 < 32 ? static_cast<int>(n - l0) : 32;
+    if (cnt == 32) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, t));
+    } else {
+      for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, t));
+    }
+  }
+  if (lane == 0) g[e] = acc;
 }
 
 // ------------------------------------------------------------------ tree Gram (generic)
@@ -526,7 +544,8 @@ void launch_random_vector(int64_t n, int64_t offset, uint64_t seed, double* out,
 void launch_serial_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, const double* v,
                         int64_t ldv, double* g, DevState* st, cudaStream_t s) {
   const int ne = ku * kv;
-  serial_gram_kernel<<<grid_for(ne, 64), 64, 0, s>>>(n, ku, kv, u, ldu, v, ldv, g, st);
+  serial_gram_kernel<<<grid_for(static_cast<int64_t>(ne) * 32, 128), 128, 0, s>>>(n, ku, kv, u, ldu,
+                                                                                  v, ldv, g, st);
   CS_CUDA(cudaGetLastError());
 }
 

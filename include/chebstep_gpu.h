@@ -96,6 +96,12 @@ typedef struct {
   uint64_t seed;      /* solver.hpp:28 */
   int mode;           /* CS_MODE_* */
   int check_every;    /* outer iterations per host convergence poll (0 = auto) */
+  /* analysis hooks (solver.hpp:30-34); none changes the iterate sequence.
+   * Enabling any of them syncs with the host once per outer iteration. */
+  int collect_gram;          /* W_k and kappa_2(W_k) per outer iteration */
+  int track_true_residual;   /* ||b - A x_k|| / ||b|| (initial + per outer) */
+  const double* error_reference; /* host x* (n_local): A-norm errors, or NULL */
+  int collect_iterates;      /* x_k (initial + per outer) */
 } cs_config;
 
 typedef struct {
@@ -114,6 +120,14 @@ typedef struct {
   int64_t device_allreduces;      /* collectives actually issued (fast mode: 1 per outer) */
   int64_t kernel_launches;        /* kernels launched by this solve */
   double t_lanczos_ms, t_solve_ms;/* CUDA-event times on the solve stream */
+  /* analysis-hook outputs, caller-owned (NULL = not wanted), `cap` entries each;
+   * gram_history holds cap * s*s doubles, iterates cap * n_local doubles. */
+  int n_kappa, n_true, n_aerr, n_iter;
+  double* kappa_w;
+  double* gram_history;
+  double* true_rel_residual;
+  double* a_norm_error;
+  double* iterates;
 } cs_report;
 
 /* ------------------------------------------------------------ errors / info */
@@ -206,6 +220,10 @@ int cs_pcg_s_solve(cs_problem* p, const double* b, const double* x0, const cs_co
                    double* x, cs_report* rep);
 int cs_pcg_solve(cs_problem* p, const double* b, const double* x0, double tol, int max_iter,
                  int mode, double* x, cs_report* rep);
+/* Classical PCG with the PcgConfig fields of a cs_config: tol, max_outer (as
+ * max_iter), mode, error_reference, collect_iterates (solver.hpp:85-90). */
+int cs_pcg_solve_cfg(cs_problem* p, const double* b, const double* x0, const cs_config* cfg,
+                     double* x, cs_report* rep);
 /* Device-resident variants: b, x0, x are device pointers (n_local doubles). */
 int cs_pcg_s_solve_device(cs_problem* p, const double* b, const double* x0,
                           const cs_config* cfg, double* x, cs_report* rep);

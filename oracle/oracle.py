@@ -48,6 +48,14 @@ class OcReport(C.Structure):
                 ("rel_residual", _dp), ("delta_alpha", _dp), ("delta_beta", _dp)]
 
 
+class OcHooks(C.Structure):
+    _fields_ = [("collect_gram", C.c_int), ("track_true_residual", C.c_int),
+                ("collect_iterates", C.c_int), ("error_reference", C.c_void_p), ("cap", C.c_int),
+                ("kappa_w", _dp), ("gram_history", _dp), ("true_rel_residual", _dp),
+                ("a_norm_error", _dp), ("iterates", _dp), ("n_kappa", C.c_int),
+                ("n_true", C.c_int), ("n_aerr", C.c_int), ("n_iter", C.c_int)]
+
+
 class OracleError(RuntimeError):
     def __init__(self, code: int, payload: int, msg: str):
         super().__init__(f"[{code}] {msg}")
@@ -282,6 +290,52 @@ class Oracle:
         self._check(self._f("pcg_s_solve")(a.n, a.rowptr, a.col, a.val, b, x0, precond,
                                             C.byref(cfg), x, C.byref(rep)))
         return x, self._unpack(rep, bufs)
+
+    def pcg_s_solve_hooks(self, a: Csr, *, s=4, tol=1e-6, max_outer=500, nu=30, gram="fgs",
+                          spectrum=None, precond=1, collect_gram=False, track_true_residual=False,
+                          error_reference=None, collect_iterates=False, classical=False):
+        """Reference library only: solve with SolverConfig/PcgConfig analysis hooks."""
+        assert self.which == "ref"
+        b, x0 = np.ones(a.n), np.zeros(a.n)
+        cap = max_outer + 2
+        bufs = {"kappa": np.zeros(cap), "gram": np.zeros(cap * s * s), "true": np.zeros(cap),
+                "aerr": np.zeros(cap), "iter": np.zeros(cap * a.n) if collect_iterates else None}
+        hk = OcHooks()
+        hk.collect_gram, hk.track_true_residual = int(collect_gram), int(track_true_residual)
+        hk.collect_iterates = int(collect_iterates)
+        ref = None
+        if error_reference is not None:
+            ref = np.ascontiguousarray(error_reference, np.float64)
+            hk.error_reference = ref.ctypes.data
+        hk.cap = cap
+        hk.kappa_w, hk.gram_history = (bufs["kappa"].ctypes.data_as(_dp), bufs["gram"].ctypes.data_as(_dp))
+        hk.true_rel_residual = bufs["true"].ctypes.data_as(_dp)
+        hk.a_norm_error = bufs["aerr"].ctypes.data_as(_dp)
+        if collect_iterates:
+            hk.iterates = bufs["iter"].ctypes.data_as(_dp)
+        rep, rb = self._report(cap)
+        x = np.zeros(a.n)
+        if classical:
+            fn = self.lib.ref_pcg_solve_hooks
+            fn.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p, C.c_int, C.c_double,
+                           C.c_int, C.POINTER(OcHooks), _f64p, C.POINTER(OcReport)]
+            self._check(fn(a.n, a.rowptr, a.col, a.val, b, x0, precond, tol, max_outer,
+                           C.byref(hk), x, C.byref(rep)))
+        else:
+            cfg = OcCfg(s, tol, max_outer, nu, 1 if gram == "cholesky" else 0,
+                        1 if spectrum else 0, *(spectrum or (0.0, 0.0)), 40, 1234)
+            fn = self.lib.ref_pcg_s_solve_hooks
+            fn.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p, C.c_int, C.POINTER(OcCfg),
+                           C.POINTER(OcHooks), _f64p, C.POINTER(OcReport)]
+            self._check(fn(a.n, a.rowptr, a.col, a.val, b, x0, precond, C.byref(cfg), C.byref(hk),
+                           x, C.byref(rep)))
+        out = {"kappa": bufs["kappa"][:hk.n_kappa].copy(),
+               "gram": [bufs["gram"][i * s * s:(i + 1) * s * s].reshape(s, s).T.copy()
+                        for i in range(hk.n_kappa)],
+               "true": bufs["true"][:hk.n_true].copy(), "aerr": bufs["aerr"][:hk.n_aerr].copy(),
+               "iter": [bufs["iter"][i * a.n:(i + 1) * a.n].copy() for i in range(hk.n_iter)]
+               if collect_iterates else []}
+        return x, self._unpack(rep, rb), out
 
     def pcg_solve(self, a: Csr, b=None, x0=None, *, tol=1e-6, max_iter=1000, precond=1):
         b = np.ones(a.n) if b is None else np.ascontiguousarray(b, np.float64)

@@ -48,6 +48,26 @@ typedef struct {
   double* delta_beta;
 } oc_report;
 
+/* analysis hooks (solver.hpp:30-34), reference library only */
+typedef struct {
+  int collect_gram, track_true_residual, collect_iterates;
+  const double* error_reference;
+  int cap;                      /* entries per history (gram: cap*s*s, iterates: cap*n) */
+  double* kappa_w;
+  double* gram_history;
+  double* true_rel_residual;
+  double* a_norm_error;
+  double* iterates;
+  int n_kappa, n_true, n_aerr, n_iter;
+} oc_hooks;
+
+int ref_pcg_s_solve_hooks(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                          const double* b, const double* x0, int precond, const oc_cfg* cfg,
+                          oc_hooks* hk, double* x, oc_report* rep);
+int ref_pcg_solve_hooks(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        const double* b, const double* x0, int precond, double tol, int max_iter,
+                        oc_hooks* hk, double* x, oc_report* rep);
+
 #define OC_DECLARE(P)                                                                  \
   int P##poisson27_fill(int64_t nx, int64_t ny, int64_t nz, int64_t* rowptr,           \
                         int64_t* col, double* val);                                   \

@@ -297,6 +297,79 @@ int ref_pcg_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   });
 }
 
+// solver.cpp:78-190 with the analysis hooks of SolverConfig (solver.hpp:30-34)
+static void copy_hooks(const cs::SolveReport& r, oc_hooks* hk, int s, int64_t n) {
+  auto put = [&](const std::vector<double>& src, double* dst, int* len) {
+    *len = static_cast<int>(src.size());
+    if (dst)
+      for (int i = 0; i < *len && i < hk->cap; ++i) dst[i] = src[i];
+  };
+  put(r.kappa_w, hk->kappa_w, &hk->n_kappa);
+  put(r.true_rel_residual, hk->true_rel_residual, &hk->n_true);
+  put(r.a_norm_error, hk->a_norm_error, &hk->n_aerr);
+  if (hk->gram_history)
+    for (size_t i = 0; i < r.gram_history.size() && static_cast<int>(i) < hk->cap; ++i)
+      std::memcpy(hk->gram_history + i * s * s, r.gram_history[i].data.data(),
+                  sizeof(double) * s * s);
+  hk->n_iter = static_cast<int>(r.iterates.size());
+  if (hk->iterates)
+    for (size_t i = 0; i < r.iterates.size() && static_cast<int>(i) < hk->cap; ++i)
+      std::memcpy(hk->iterates + i * n, r.iterates[i].data(), sizeof(double) * n);
+}
+
+int ref_pcg_s_solve_hooks(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                          const double* b, const double* x0, int precond, const oc_cfg* c,
+                          oc_hooks* hk, double* x, oc_report* rep) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    Precond m;
+    make_precond(m, a, precond);
+    cs::SolverConfig cfg;
+    cfg.s = c->s;
+    cfg.tol = c->tol;
+    cfg.max_outer = c->max_outer;
+    cfg.fgs.nu = c->nu;
+    cfg.gram_solver = c->gram == 1 ? cs::GramSolverKind::cholesky : cs::GramSolverKind::fgs;
+    if (c->has_spectrum) {
+      cs::SpectrumEstimate e;
+      e.lambda_min = c->lambda_min;
+      e.lambda_max = c->lambda_max;
+      cfg.spectrum = e;
+    }
+    cfg.lanczos_steps = c->lanczos_steps;
+    cfg.seed = c->seed;
+    cfg.collect_gram = hk->collect_gram != 0;
+    cfg.track_true_residual = hk->track_true_residual != 0;
+    cfg.collect_iterates = hk->collect_iterates != 0;
+    if (hk->error_reference) cfg.error_reference = std::vector<double>(hk->error_reference, hk->error_reference + n);
+    const cs::SolveResult res = cs::pcg_s_solve(a, {b, static_cast<size_t>(n)},
+                                                {x0, static_cast<size_t>(n)}, m.get(), cfg);
+    std::memcpy(x, res.x.data(), sizeof(double) * res.x.size());
+    fill_report(res.report, rep);
+    copy_hooks(res.report, hk, c->s, n);
+  });
+}
+
+int ref_pcg_solve_hooks(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        const double* b, const double* x0, int precond, double tol, int max_iter,
+                        oc_hooks* hk, double* x, oc_report* rep) {
+  return guarded([&] {
+    const cs::CsrMatrix a = make_csr(n, rp, ci, v);
+    Precond m;
+    make_precond(m, a, precond);
+    cs::PcgConfig cfg;
+    cfg.tol = tol;
+    cfg.max_iter = max_iter;
+    cfg.collect_iterates = hk->collect_iterates != 0;
+    if (hk->error_reference) cfg.error_reference = std::vector<double>(hk->error_reference, hk->error_reference + n);
+    const cs::SolveResult res = cs::pcg_solve(a, {b, static_cast<size_t>(n)},
+                                              {x0, static_cast<size_t>(n)}, m.get(), cfg);
+    std::memcpy(x, res.x.data(), sizeof(double) * res.x.size());
+    fill_report(res.report, rep);
+    copy_hooks(res.report, hk, 1, n);
+  });
+}
+
 const char* ref_last_error(int* payload) {
   if (payload) *payload = g_payload;
   return g_msg.c_str();

@@ -44,7 +44,9 @@ class CsConfig(C.Structure):
     _fields_ = [("s", C.c_int), ("tol", C.c_double), ("max_outer", C.c_int), ("nu", C.c_int),
                 ("gram", C.c_int), ("has_spectrum", C.c_int), ("lambda_min", C.c_double),
                 ("lambda_max", C.c_double), ("lanczos_steps", C.c_int), ("seed", C.c_uint64),
-                ("mode", C.c_int), ("check_every", C.c_int)]
+                ("mode", C.c_int), ("check_every", C.c_int),
+                ("collect_gram", C.c_int), ("track_true_residual", C.c_int),
+                ("error_reference", C.c_void_p), ("collect_iterates", C.c_int)]
 
 
 class CsReport(C.Structure):
@@ -55,7 +57,10 @@ class CsReport(C.Structure):
                 ("n_rel", C.c_int), ("n_da", C.c_int), ("n_db", C.c_int),
                 ("rel_residual", _dp), ("delta_alpha", _dp), ("delta_beta", _dp),
                 ("device_allreduces", C.c_int64), ("kernel_launches", C.c_int64),
-                ("t_lanczos_ms", C.c_double), ("t_solve_ms", C.c_double)]
+                ("t_lanczos_ms", C.c_double), ("t_solve_ms", C.c_double),
+                ("n_kappa", C.c_int), ("n_true", C.c_int), ("n_aerr", C.c_int), ("n_iter", C.c_int),
+                ("kappa_w", _dp), ("gram_history", _dp), ("true_rel_residual", _dp),
+                ("a_norm_error", _dp), ("iterates", _dp)]
 
 
 # name -> (restype, argtypes); every symbol of include/chebstep_gpu.h
@@ -103,6 +108,8 @@ SIGNATURES = {
                                  C.POINTER(CsReport)]),
     "cs_pcg_solve": (C.c_int, [_vp, _f64p, _f64p, C.c_double, C.c_int, C.c_int, _f64p,
                                C.POINTER(CsReport)]),
+    "cs_pcg_solve_cfg": (C.c_int, [_vp, _f64p, _f64p, C.POINTER(CsConfig), _f64p,
+                                   C.POINTER(CsReport)]),
     "cs_pcg_s_solve_device": (C.c_int, [_vp, _vp, _vp, C.POINTER(CsConfig), _vp,
                                         C.POINTER(CsReport)]),
     "cs_pcg_solve_device": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, C.c_int, _vp,

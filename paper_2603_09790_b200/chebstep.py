@@ -347,8 +347,9 @@ class DeviceProblem:
         if b.size != self.n_local or x0.size != self.n_local:
             raise DimensionError("pcg_s_solve: vector length mismatch")
         x = np.zeros(self.n_local)
-        rep, bufs = _report(cfg.max_outer + 2)
-        _check(lib.cs_pcg_s_solve(self.handle, b, x0, C.byref(cfg._c()), x, C.byref(rep)))
+        rep, bufs = _report(cfg.max_outer + 2, cfg.s, self.n_local, cfg)
+        cc = cfg._c()
+        _check(lib.cs_pcg_s_solve(self.handle, b, x0, C.byref(cc), x, C.byref(rep)))
         return SolveResult(x, _unpack(rep, bufs))
 
     def pcg_s_solve_device(self, b_ptr: int, x0_ptr: int, x_ptr: int,
@@ -361,12 +362,27 @@ class DeviceProblem:
         return _unpack(rep, bufs)
 
     def pcg_solve(self, b=None, x0=None, tol: float = 1e-6, max_iter: int = 1000,
-                  mode: str = "fast") -> "SolveResult":
+                  mode: str = "fast", cfg: Optional["PcgConfig"] = None) -> "SolveResult":
+        """Classical PCG; cfg (PcgConfig) adds the error_reference / collect_iterates hooks."""
         b = np.ones(self.n_local) if b is None else np.ascontiguousarray(b, np.float64)
         x0 = np.zeros(self.n_local) if x0 is None else np.ascontiguousarray(x0, np.float64)
         x = np.zeros(self.n_local)
-        rep, bufs = _report(max_iter + 2)
-        _check(lib.cs_pcg_solve(self.handle, b, x0, tol, max_iter, _mode(mode), x, C.byref(rep)))
+        if cfg is not None:
+            tol, max_iter = cfg.tol, cfg.max_iter
+        if not (tol >= 0.0) or max_iter < 1:
+            raise InvalidArgumentError("pcg_solve: bad tol/max_iter")
+        cc = CsConfig()
+        lib.cs_config_default(C.byref(cc))
+        cc.tol, cc.max_outer, cc.mode = tol, max_iter, _mode(mode)
+        keep = None
+        if cfg is not None and cfg.error_reference is not None:
+            keep = np.ascontiguousarray(cfg.error_reference, np.float64)
+            cc.error_reference = keep.ctypes.data
+        if cfg is not None:
+            cc.collect_iterates = int(cfg.collect_iterates)
+        rep, bufs = _report(max_iter + 2, 1, self.n_local, cfg)
+        _check(lib.cs_pcg_solve_cfg(self.handle, b, x0, C.byref(cc), x, C.byref(rep)))
+        del keep
         return SolveResult(x, _unpack(rep, bufs))
 
     def pcg_solve_device(self, b_ptr: int, x0_ptr: int, x_ptr: int, tol: float = 1e-6,
@@ -467,6 +483,11 @@ class SolverConfig:
     spectrum: Optional[SpectrumEstimate] = None
     lanczos_steps: int = 40
     seed: int = 1234
+    # analysis hooks (solver.hpp:30-34); none changes the iterates
+    collect_gram: bool = False
+    track_true_residual: bool = False
+    error_reference: Optional[np.ndarray] = None
+    collect_iterates: bool = False
     mode: str = "fast"
     check_every: int = 0
 
@@ -480,6 +501,12 @@ class SolverConfig:
             c.lambda_min, c.lambda_max = self.spectrum.lambda_min, self.spectrum.lambda_max
         c.lanczos_steps, c.seed = self.lanczos_steps, self.seed
         c.mode, c.check_every = _mode(self.mode), self.check_every
+        c.collect_gram = int(self.collect_gram)
+        c.track_true_residual = int(self.track_true_residual)
+        c.collect_iterates = int(self.collect_iterates)
+        if self.error_reference is not None:
+            self._ref_keep = np.ascontiguousarray(self.error_reference, np.float64)
+            c.error_reference = self._ref_keep.ctypes.data
         return c
 
 
@@ -497,6 +524,11 @@ class SolveReport:
     local_update_flops: float = 0.0
     gram_solve_flops: float = 0.0
     spectrum_used: SpectrumEstimate = field(default_factory=SpectrumEstimate)
+    kappa_w: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    gram_history: list = field(default_factory=list)
+    true_rel_residual: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    a_norm_error: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    iterates: list = field(default_factory=list)
     device_allreduces: int = 0
     kernel_launches: int = 0
     t_lanczos_ms: float = 0.0
@@ -509,21 +541,51 @@ class SolveResult:
     report: SolveReport
 
 
-def _report(cap: int):
+def _report(cap: int, s: int = 0, n: int = 0, cfg=None):
     bufs = [np.zeros(cap) for _ in range(3)]
     rep = CsReport()
     rep.cap = cap
     rep.rel_residual, rep.delta_alpha, rep.delta_beta = (b.ctypes.data_as(L._dp) for b in bufs)
+    hooks = {}
+    if cfg is not None:
+        if getattr(cfg, "collect_gram", False):
+            hooks["kappa"] = np.zeros(cap)
+            hooks["gram"] = np.zeros(cap * s * s)
+            rep.kappa_w = hooks["kappa"].ctypes.data_as(L._dp)
+            rep.gram_history = hooks["gram"].ctypes.data_as(L._dp)
+        if getattr(cfg, "track_true_residual", False):
+            hooks["true"] = np.zeros(cap)
+            rep.true_rel_residual = hooks["true"].ctypes.data_as(L._dp)
+        if getattr(cfg, "error_reference", None) is not None:
+            hooks["aerr"] = np.zeros(cap)
+            rep.a_norm_error = hooks["aerr"].ctypes.data_as(L._dp)
+        if getattr(cfg, "collect_iterates", False):
+            hooks["iter"] = np.zeros(cap * n)
+            rep.iterates = hooks["iter"].ctypes.data_as(L._dp)
+    bufs.append((hooks, s, n))
     return rep, bufs
 
 
 def _unpack(rep: CsReport, bufs) -> SolveReport:
-    return SolveReport(
+    out = SolveReport(
         bool(rep.converged), rep.outer_iters, bufs[0][:rep.n_rel].copy(),
         bufs[1][:rep.n_da].copy(), bufs[2][:rep.n_db].copy(), rep.spmv_count, rep.precond_count,
         rep.allreduce_count, rep.local_update_flops, rep.gram_solve_flops,
-        SpectrumEstimate(rep.lambda_min, rep.lambda_max, "lanczos", 0.9, 1.1),
-        rep.device_allreduces, rep.kernel_launches, rep.t_lanczos_ms, rep.t_solve_ms)
+        SpectrumEstimate(rep.lambda_min, rep.lambda_max, "lanczos", 0.9, 1.1))
+    out.device_allreduces, out.kernel_launches = rep.device_allreduces, rep.kernel_launches
+    out.t_lanczos_ms, out.t_solve_ms = rep.t_lanczos_ms, rep.t_solve_ms
+    hooks, s, n = bufs[3] if len(bufs) > 3 else ({}, 0, 0)
+    if "kappa" in hooks:
+        out.kappa_w = hooks["kappa"][:rep.n_kappa].copy()
+        out.gram_history = [hooks["gram"][i * s * s:(i + 1) * s * s].reshape(s, s).T.copy()
+                            for i in range(rep.n_kappa)]
+    if "true" in hooks:
+        out.true_rel_residual = hooks["true"][:rep.n_true].copy()
+    if "aerr" in hooks:
+        out.a_norm_error = hooks["aerr"][:rep.n_aerr].copy()
+    if "iter" in hooks:
+        out.iterates = [hooks["iter"][i * n:(i + 1) * n].copy() for i in range(rep.n_iter)]
+    return out
 
 
 # ---------------------------------------------------------------------------------- solves
@@ -547,7 +609,7 @@ def pcg_s_solve(a: CsrMatrix, b, x0, m: Preconditioner, cfg: Optional[SolverConf
     b = _vec(b, a.n, "pcg_s_solve")
     x0 = _vec(x0, a.n, "pcg_s_solve")
     x = np.zeros(a.n)
-    rep, bufs = _report(cfg.max_outer + 2)
+    rep, bufs = _report(cfg.max_outer + 2, cfg.s, a.n, cfg)
     _check(lib.cs_pcg_s_solve_csr(ctx.handle, a.n, a.row_offsets.ctypes.data,
                                   a.col_indices.ctypes.data, a.values.ctypes.data,
                                   _precond_kind(m), b.ctypes.data, x0.ctypes.data, C.byref(cc),
@@ -557,8 +619,11 @@ def pcg_s_solve(a: CsrMatrix, b, x0, m: Preconditioner, cfg: Optional[SolverConf
 
 @dataclass
 class PcgConfig:
+    """solver.hpp:85-90."""
     tol: float = 1e-6
     max_iter: int = 1000
+    error_reference: Optional[np.ndarray] = None
+    collect_iterates: bool = False
 
 
 def pcg_solve(a: CsrMatrix, b, x0, m: Preconditioner, cfg=None, max_iter: Optional[int] = None,
@@ -571,13 +636,11 @@ def pcg_solve(a: CsrMatrix, b, x0, m: Preconditioner, cfg=None, max_iter: Option
     ctx = ctx or default_context()
     b = _vec(b, a.n, "pcg_solve")
     x0 = _vec(x0, a.n, "pcg_solve")
-    x = np.zeros(a.n)
-    rep, bufs = _report(cfg.max_iter + 2)
-    _check(lib.cs_pcg_solve_csr(ctx.handle, a.n, a.row_offsets.ctypes.data,
-                                a.col_indices.ctypes.data, a.values.ctypes.data, _precond_kind(m),
-                                b.ctypes.data, x0.ctypes.data, cfg.tol, cfg.max_iter,
-                                x.ctypes.data, C.byref(rep)))
-    return SolveResult(x, _unpack(rep, bufs))
+    p = _with_problem(a, m, ctx)
+    try:
+        return p.pcg_solve(b, x0, cfg.tol, cfg.max_iter, "fast", cfg=cfg)
+    finally:
+        p.close()
 
 
 @dataclass

@@ -474,13 +474,53 @@ void fill(SolveReport& r, const cs_report& c, const std::vector<double>& rel,
 }
 }  // namespace
 
+namespace {
+// caller-side buffers for the analysis-hook histories
+struct HookBufs {
+  std::vector<double> kappa, gram, truer, aerr, iter;
+  void attach(cs_report& r, int cap, int s, index_t n, bool g, bool t, bool e, bool it) {
+    if (g) {
+      kappa.assign(cap, 0.0);
+      gram.assign(static_cast<size_t>(cap) * s * s, 0.0);
+      r.kappa_w = kappa.data();
+      r.gram_history = gram.data();
+    }
+    if (t) {
+      truer.assign(cap, 0.0);
+      r.true_rel_residual = truer.data();
+    }
+    if (e) {
+      aerr.assign(cap, 0.0);
+      r.a_norm_error = aerr.data();
+    }
+    if (it) {
+      iter.assign(static_cast<size_t>(cap) * n, 0.0);
+      r.iterates = iter.data();
+    }
+  }
+  void fill(SolveReport& rep, const cs_report& r, int s, index_t n) const {
+    for (int i = 0; i < r.n_kappa && i < static_cast<int>(kappa.size()); ++i) {
+      rep.kappa_w.push_back(kappa[i]);
+      SmallDense w(s, s);
+      std::copy(gram.begin() + static_cast<size_t>(i) * s * s,
+                gram.begin() + static_cast<size_t>(i + 1) * s * s, w.data.begin());
+      rep.gram_history.push_back(std::move(w));
+    }
+    rep.true_rel_residual.assign(truer.begin(),
+                                 truer.begin() + std::min<size_t>(r.n_true, truer.size()));
+    rep.a_norm_error.assign(aerr.begin(), aerr.begin() + std::min<size_t>(r.n_aerr, aerr.size()));
+    for (int i = 0; i < r.n_iter && static_cast<size_t>(i + 1) * n <= iter.size(); ++i)
+      rep.iterates.emplace_back(iter.begin() + static_cast<size_t>(i) * n,
+                                iter.begin() + static_cast<size_t>(i + 1) * n);
+  }
+};
+}  // namespace
+
 SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
                         const Preconditioner& m, const SolverConfig& cfg) {
   cfg.validate();
   if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
     throw DimensionError("pcg_s_solve: vector length mismatch");
-  if (cfg.collect_gram || cfg.track_true_residual || cfg.error_reference || cfg.collect_iterates)
-    throw InvalidArgumentError("pcg_s_solve: analysis hooks are not available on the device path");
   cs_config c;
   cs_config_default(&c);
   c.s = cfg.s;
@@ -496,20 +536,33 @@ SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span
   c.lanczos_steps = cfg.lanczos_steps;
   c.seed = cfg.seed;
   c.mode = mode_code();
+  c.collect_gram = cfg.collect_gram;
+  c.track_true_residual = cfg.track_true_residual;
+  c.collect_iterates = cfg.collect_iterates;
+  if (cfg.error_reference) {
+    if (static_cast<index_t>(cfg.error_reference->size()) != a.n)
+      throw DimensionError("pcg_s_solve: error_reference length mismatch");
+    c.error_reference = cfg.error_reference->data();
+  }
   const std::string_view nm = m.name();
   const int kind = nm == "jacobi" ? CS_PRECOND_JACOBI : nm == "identity" ? CS_PRECOND_IDENTITY : -1;
   if (kind < 0) throw InvalidArgumentError("preconditioner has no device implementation");
   SolveResult out;
   out.x.resize(static_cast<std::size_t>(a.n));
-  std::vector<double> rel(cfg.max_outer + 2), da(cfg.max_outer + 2), db(cfg.max_outer + 2);
+  const int cap = cfg.max_outer + 2;
+  std::vector<double> rel(cap), da(cap), db(cap);
   cs_report r{};
-  r.cap = cfg.max_outer + 2;
+  r.cap = cap;
   r.rel_residual = rel.data();
   r.delta_alpha = da.data();
   r.delta_beta = db.data();
+  HookBufs hb;
+  hb.attach(r, cap, cfg.s, a.n, cfg.collect_gram, cfg.track_true_residual,
+            cfg.error_reference.has_value(), cfg.collect_iterates);
   check(cs_pcg_s_solve_csr(ctx(), a.n, a.row_offsets.data(), a.col_indices.data(),
                            a.values.data(), kind, b.data(), x0.data(), &c, out.x.data(), &r));
   fill(out.report, r, rel, da, db);
+  hb.fill(out.report, r, cfg.s, a.n);
   if (cfg.spectrum) out.report.spectrum_used = *cfg.spectrum;
   else if (r.lambda_max > 0.0) {
     out.report.spectrum_used.low_factor = 0.9;
@@ -523,17 +576,26 @@ SolveResult pcg_solve(const CsrMatrix& a, std::span<const double> b, std::span<c
   if (!(cfg.tol >= 0.0) || cfg.max_iter < 1) throw InvalidArgumentError("pcg_solve: bad tol/max_iter");
   if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
     throw DimensionError("pcg_solve: vector length mismatch");
-  if (cfg.error_reference || cfg.collect_iterates)
-    throw InvalidArgumentError("pcg_solve: analysis hooks are not available on the device path");
   Problem p(a, &m);
+  cs_config c;
+  cs_config_default(&c);
+  c.tol = cfg.tol;
+  c.max_outer = cfg.max_iter;
+  c.mode = mode_code();
+  c.collect_iterates = cfg.collect_iterates;
+  if (cfg.error_reference) c.error_reference = cfg.error_reference->data();
   SolveResult out;
   out.x.resize(static_cast<std::size_t>(a.n));
-  std::vector<double> rel(cfg.max_iter + 2);
+  const int cap = cfg.max_iter + 2;
+  std::vector<double> rel(cap);
   cs_report r{};
-  r.cap = cfg.max_iter + 2;
+  r.cap = cap;
   r.rel_residual = rel.data();
-  check(cs_pcg_solve(p.p, b.data(), x0.data(), cfg.tol, cfg.max_iter, mode_code(), out.x.data(), &r));
+  HookBufs hb;
+  hb.attach(r, cap, 1, a.n, false, false, cfg.error_reference.has_value(), cfg.collect_iterates);
+  check(cs_pcg_solve_cfg(p.p, b.data(), x0.data(), &c, out.x.data(), &r));
   fill(out.report, r, rel, {}, {});
+  hb.fill(out.report, r, 1, a.n);
   out.report.spectrum_used = SpectrumEstimate{};
   return out;
 }

@@ -574,6 +574,22 @@ int cs_pcg_solve(cs_problem* p, const double* b, const double* x0, double tol, i
   });
 }
 
+int cs_pcg_solve_cfg(cs_problem* p, const double* b, const double* x0, const cs_config* cfg,
+                     double* x, cs_report* rep) {
+  return guard([&] {
+    cs_ctx* c = p->ctx;
+    CS_CUDA(cudaSetDevice(c->device));
+    StreamBind bind_stream_(c->stream);
+    const size_t bytes = sizeof(double) * p->n_local;
+    HostIn db(c, b, bytes), dx0(c, x0, bytes);
+    DBuf dx(bytes);
+    pcg_solve_dev(p, db.d.as<double>(), dx0.d.as<double>(), cfg->tol, cfg->max_outer, cfg->mode,
+                  dx.as<double>(), rep, cfg);
+    to_host(c, x, dx.p, bytes);
+    sync(c);
+  });
+}
+
 int cs_pcg_s_solve_csr(cs_ctx* ctx, int64_t n, const int64_t* rowptr, const int64_t* col,
                        const double* val, int precond, const double* b, const double* x0,
                        const cs_config* cfg, double* x, cs_report* rep) {

@@ -28,5 +28,7 @@ void lz_scalar(int which, int j, int steps, LanczosScalars* sc, DevState* st, cu
 
 // host: eigenvalues of the symmetric tridiagonal (d[m], e[m-1]) ascending
 void tridiag_eigenvalues(int m, const double* d, const double* e, double* out);
+// host: eigenvalues of a small dense symmetric matrix (column-major s x s), ascending
+void sym_eigenvalues(int s, const double* w, double* out);
 
 }  // namespace csg

@@ -170,7 +170,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b, const double* x0, const cs_c
 void mpk_unit(cs_problem* p, double* Z, double* P, double* r, double* zpA, double* zpB, int s,
               double lo, double hi, DevState* st);
 void pcg_solve_dev(cs_problem* p, const double* b, const double* x0, double tol, int max_iter,
-                   int mode, double* x, cs_report* rep);
+                   int mode, double* x, cs_report* rep, const cs_config* hooks = nullptr);
 
 // error helpers
 [[noreturn]] void fail(int code, int payload, const std::string& msg);

@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
+#include <vector>
 
 #include "runtime.cuh"
 
@@ -338,6 +340,125 @@ void mpk_unit(cs_problem* p, double* Z, double* P, double* r, double* zpA, doubl
   mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st);
 }
 
+namespace {
+
+// Analysis hooks (solver.hpp:30-34, recorded as in solver.cpp:107-116 and
+// 148-151): after r0 and after every outer update, on the host, without
+// touching the iterates. Reductions follow the solve's mode (serial order in
+// reference mode, so the histories are bitwise the reference's there).
+struct Hooks {
+  cs_problem* p;
+  cs_report* rep;
+  int mode, s;
+  double bnorm;
+  bool gram, truer, aerr, iter;
+  const double* b_dev;
+  DBuf buf;
+  double *t = nullptr, *e = nullptr, *y = nullptr, *ref = nullptr, *dot = nullptr,
+         *partial = nullptr;
+  unsigned* ticket = nullptr;
+
+  Hooks(cs_problem* p_, cs_report* r, const cs_config& cfg, int s_, const double* b)
+      : p(p_), rep(r), mode(cfg.mode), s(s_), bnorm(0.0), b_dev(b) {
+    gram = cfg.collect_gram != 0;
+    truer = cfg.track_true_residual != 0;
+    aerr = cfg.error_reference != nullptr;
+    iter = cfg.collect_iterates != 0;
+    rep->n_kappa = rep->n_true = rep->n_aerr = rep->n_iter = 0;
+    if (!truer && !aerr) return;
+    const int64_t ld = p->ld, n = p->n_local;
+    const size_t part = tree_gram_partial_doubles(n, 1, 1);
+    buf.alloc(sizeof(double) * (3 * ld + n + part + 64));
+    t = buf.as<double>();
+    e = t + ld;
+    y = e + ld;
+    ref = y + ld;
+    dot = ref + n;
+    partial = dot + 8;
+    ticket = reinterpret_cast<unsigned*>(partial + part);
+    CS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), p->ctx->stream));
+    if (aerr)
+      CS_CUDA(cudaMemcpyAsync(ref, cfg.error_reference, sizeof(double) * n,
+                              cudaMemcpyHostToDevice, p->ctx->stream));
+  }
+  bool any() const { return gram || truer || aerr || iter; }
+
+  double global_dot(const double* u, const double* v) {
+    cs_ctx* c = p->ctx;
+    {
+      Launch L(c, CS_PHASE_OTHER);
+      if (mode == CS_MODE_REFERENCE)
+        launch_serial_gram(p->n_local, 1, 1, u, p->ld, v, p->ld, dot, nullptr, c->stream);
+      else
+        launch_tree_gram(p->n_local, 1, 1, u, p->ld, v, p->ld, dot, partial, ticket, nullptr,
+                         c->stream);
+    }
+    allreduce_sum(c, dot, 1);
+    double h = 0.0;
+    CS_CUDA(cudaMemcpyAsync(&h, dot, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    return h;
+  }
+
+  static void push(double* arr, int* len, int cap, double v) {
+    if (arr && *len < cap) arr[*len] = v;
+    ++*len;
+  }
+
+  void record_x(double* x) {
+    cs_ctx* c = p->ctx;
+    const int64_t n = p->n_local;
+    if (iter) {
+      if (rep->iterates && rep->n_iter < rep->cap)
+        CS_CUDA(cudaMemcpyAsync(rep->iterates + static_cast<int64_t>(rep->n_iter) * n, x,
+                                sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      ++rep->n_iter;
+    }
+    if (truer) {  // ||b - A x|| / ||b||   (solver.cpp:111-115)
+      SpmvArgs g;
+      g.x = x;
+      g.y = t;
+      g.b = b_dev;
+      spmv_halo(p, kResid, g, x);
+      push(rep->true_rel_residual, &rep->n_true, rep->cap, std::sqrt(global_dot(t, t)) / bnorm);
+    }
+    if (aerr) {  // sqrt(max(0, e^T A e)), e = x - x*   (solver.cpp:24-29)
+      {
+        Launch L(c, CS_PHASE_OTHER);
+        static const double minus_one = -1.0;
+        DBuf cm(sizeof(double));
+        CS_CUDA(cudaMemcpyAsync(cm.p, &minus_one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        launch_block_update(n, 1, 1, x, ref, cm.as<double>(), e, c->stream);  // e = x + (-1) x*
+        CS_CUDA(cudaStreamSynchronize(c->stream));
+      }
+      SpmvArgs g;
+      g.x = e;
+      g.y = y;
+      spmv_halo(p, kPlain, g, e);
+      const double d = global_dot(e, y);
+      push(rep->a_norm_error, &rep->n_aerr, rep->cap, std::sqrt(0.0 < d ? d : 0.0));
+    }
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+  }
+
+  void record_gram(const double* W) {  // W_k and kappa_2(W_k)  (solver.cpp:148-151)
+    if (!gram) return;
+    std::vector<double> w(static_cast<size_t>(s) * s);
+    CS_CUDA(cudaMemcpyAsync(w.data(), W, sizeof(double) * w.size(), cudaMemcpyDeviceToHost,
+                            p->ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    if (rep->gram_history && rep->n_kappa < rep->cap)
+      std::copy(w.begin(), w.end(), rep->gram_history + static_cast<int64_t>(rep->n_kappa) * s * s);
+    std::vector<double> ev(s);
+    sym_eigenvalues(s, w.data(), ev.data());
+    const double kappa =
+        ev.front() > 0.0 ? ev.back() / ev.front() : std::numeric_limits<double>::infinity();
+    push(rep->kappa_w, &rep->n_kappa, rep->cap, kappa);
+  }
+};
+
+}  // namespace
+
 void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
                     const cs_config& cfg, double* x_dev, cs_report* rep) {
   cs_ctx* c = p->ctx;
@@ -408,6 +529,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   unsigned* ticket = ar.take<unsigned>(8);
   CS_CUDA(cudaMemsetAsync(ticket, 0, 8 * sizeof(unsigned), c->stream));
 
+  Hooks hooks(p, rep, cfg, s, bk.b);
+  hooks.bnorm = bnorm;
   init_state(c, bnorm, 0);
   SmallArgs sa;
   sa.s = s;
@@ -470,6 +593,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     g.st = st;
     spmv_halo(p, kResid, g, bk.x);
   }
+  if (hooks.any()) hooks.record_x(bk.x);  // record_extras() after r0, solver.cpp:122-123
   if (mode == CS_MODE_REFERENCE) {
     gram(bk.r, 1, bk.r, 1, raw + q + s);
     {
@@ -539,7 +663,34 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   CS_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   int issued = 0, slot = 0;
   bool have_prev = false;
-  for (;;) {
+  if (hooks.any()) {  // per-outer host records: one outer at a time
+    for (int k = 1; k <= cfg.max_outer; ++k) {
+      if (mode == CS_MODE_FAST) {
+        ua.beta = k == 1 ? nullptr : beta_d;
+        ua.zw = bk.Z;
+        {
+          Launch L(c, CS_PHASE_UPDATE);
+          launch_fast_update(ua, c->stream);
+        }
+        if (read_state(c).done) break;
+        hooks.record_gram(W);  // W_k (the recurrence's W for this outer's alpha)
+        hooks.record_x(bk.x);
+        mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true);
+        packed_reduce(bk.Q, bk.Z);
+        small(launch_fast_step);
+      } else {
+        outer_ref();
+        const DevState hs = read_state(c);
+        if (hs.outer_iters == k && hs.err == 0ull) {
+          hooks.record_gram(W);
+          hooks.record_x(bk.x);
+        }
+        if (hs.done) break;
+      }
+    }
+    issued = cfg.max_outer;
+  }
+  for (; issued < cfg.max_outer;) {
     for (int bi = 0; bi < batch && issued < cfg.max_outer; ++bi, ++issued) {
       if (mode == CS_MODE_FAST) outer_fast(issued == 0);
       else outer_ref();
@@ -603,7 +754,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
 // ====================================================================== classical PCG
 
 void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, double tol,
-                   int max_iter, int mode, double* x_dev, cs_report* rep) {
+                   int max_iter, int mode, double* x_dev, cs_report* rep, const cs_config* hk) {
   cs_ctx* c = p->ctx;
   CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
@@ -647,6 +798,15 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
     if (rep->rel_residual && rep->cap > 0) rep->rel_residual[0] = 0.0;
     return;
   }
+  cs_config hcfg;
+  std::memset(&hcfg, 0, sizeof hcfg);
+  if (hk) {  // PcgConfig hooks: error_reference, collect_iterates (solver.hpp:85-90)
+    hcfg.error_reference = hk->error_reference;
+    hcfg.collect_iterates = hk->collect_iterates;
+  }
+  hcfg.mode = mode;
+  Hooks hooks(p, rep, hcfg, 1, bv);
+  hooks.bnorm = bnorm;
   init_state(c, bnorm, 0);
   auto serial_dot = [&](const double* u, const double* v, double* out) {
     Launch L(c, CS_PHASE_REDUCE);
@@ -670,6 +830,7 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
     g.st = st;
     spmv_halo(p, kResid, g, xv);
   }
+  if (hooks.any()) hooks.record_x(xv);
   if (serial) {
     serial_dot(rv, rv, dots);
     {
@@ -714,7 +875,7 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
     scalar(2);
     vec(2, false);
   };
-  const int batch = n < (1 << 22) ? 32 : 8;
+  const int batch = hooks.any() ? 1 : (n < (1 << 22) ? 32 : 8);
   volatile int* flag = static_cast<volatile int*>(c->pinned);
   cudaEvent_t ev[2];
   CS_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -722,7 +883,13 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
   int issued = 0, slot = 0;
   bool have_prev = false;
   for (;;) {
-    for (int bi = 0; bi < batch && issued < max_iter; ++bi, ++issued) iteration();
+    for (int bi = 0; bi < batch && issued < max_iter; ++bi, ++issued) {
+      iteration();
+      if (hooks.any()) {  // record_extras() after the x/r update (solver.cpp:245-246)
+        const DevState hs = read_state(c);
+        if (hs.outer_iters == issued + 1 && hs.err == 0ull) hooks.record_x(xv);
+      }
+    }
     CS_CUDA(cudaMemcpyAsync(const_cast<int*>(&flag[slot]), &st->done, sizeof(int),
                             cudaMemcpyDeviceToHost, c->stream));
     CS_CUDA(cudaEventRecord(ev[slot], c->stream));

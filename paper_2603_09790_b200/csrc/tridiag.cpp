@@ -61,4 +61,41 @@ void tridiag_eigenvalues(int m, const double* d, const double* e, double* out) {
   }
 }
 
+// Cyclic Jacobi rotations on a copy of the s x s (s <= 64) Gram matrix; used
+// for kappa_2(W) of the collect_gram hook (the reference calls dsyevd there,
+// solver.cpp:69-74). Converges quadratically; eigenvalues sorted ascending.
+void sym_eigenvalues(int s, const double* w, double* out) {
+  std::vector<double> a(w, w + static_cast<size_t>(s) * s);
+  auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(i) + static_cast<size_t>(j) * s]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int j = 0; j < s; ++j)
+      for (int i = 0; i < s; ++i) {
+        tot += A(i, j) * A(i, j);
+        if (i != j) off += A(i, j) * A(i, j);
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int pp = 0; pp < s - 1; ++pp)
+      for (int q = pp + 1; q < s; ++q) {
+        const double apq = A(pp, q);
+        if (apq == 0.0) continue;
+        const double theta = (A(q, q) - A(pp, pp)) / (2.0 * apq);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(tt * tt + 1.0), sn = tt * c;
+        for (int k = 0; k < s; ++k) {  // columns pp, q
+          const double akp = A(k, pp), akq = A(k, q);
+          A(k, pp) = c * akp - sn * akq;
+          A(k, q) = sn * akp + c * akq;
+        }
+        for (int k = 0; k < s; ++k) {  // rows pp, q
+          const double apk = A(pp, k), aqk = A(q, k);
+          A(pp, k) = c * apk - sn * aqk;
+          A(q, k) = sn * apk + c * aqk;
+        }
+      }
+  }
+  for (int i = 0; i < s; ++i) out[i] = A(i, i);
+  std::sort(out, out + s);
+}
+
 }  // namespace csg

@@ -237,3 +237,45 @@ def test_baseline_config2_reference_mode_bitwise(cs):
     assert abs(np.linalg.norm(fast.x) / g["x_norm"] - 1) < 1e-7
     r = 1.0 - p.spmv(fast.x)
     assert np.linalg.norm(r) / np.sqrt(p.n_global) < 2e-8
+
+
+def test_analysis_hooks_reference_mode(cs, port, ref):
+    """SolverConfig analysis hooks (solver.hpp:30-34): in reference algebra the
+    recorded histories are bitwise the reference library's (kappa_2(W) comes from a
+    different eigensolver: 1e-12 relative)."""
+    o = port.poisson27(14, 12, 10)
+    lam = ref.estimate_interval(o, 1)
+    xs, _ = port.pcg_s_solve(o, s=4, tol=1e-10, spectrum=lam, max_outer=500)
+    x_r, r_r, h_r = ref.pcg_s_solve_hooks(o, s=4, tol=1e-8, spectrum=lam, collect_gram=True,
+                                          track_true_residual=True, error_reference=xs,
+                                          collect_iterates=True)
+    cfg = cs.SolverConfig(s=4, tol=1e-8, mode="reference", spectrum=cs.SpectrumEstimate(*lam),
+                          collect_gram=True, track_true_residual=True, error_reference=xs,
+                          collect_iterates=True)
+    res = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n), cs.JacobiPreconditioner(_csr(cs, o)), cfg)
+    rep = res.report
+    assert res.x.tobytes() == x_r.tobytes()
+    assert rep.true_rel_residual.tobytes() == h_r["true"].tobytes()
+    assert rep.a_norm_error.tobytes() == h_r["aerr"].tobytes()
+    assert len(rep.iterates) == len(h_r["iter"]) == rep.outer_iters + 1
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(rep.iterates, h_r["iter"]))
+    assert len(rep.gram_history) == len(h_r["gram"]) == rep.outer_iters
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(rep.gram_history, h_r["gram"]))
+    np.testing.assert_allclose(rep.kappa_w, h_r["kappa"], rtol=1e-10)
+    # fast algebra: same hooks, counts line up
+    fast = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n), cs.JacobiPreconditioner(_csr(cs, o)),
+                          cs.SolverConfig(s=4, tol=1e-8, collect_gram=True, track_true_residual=True,
+                                          error_reference=xs, collect_iterates=True))
+    fr = fast.report
+    assert len(fr.true_rel_residual) == len(fr.a_norm_error) == len(fr.iterates) == fr.outer_iters + 1
+    assert len(fr.kappa_w) == fr.outer_iters
+    assert fr.true_rel_residual[-1] < 1e-7 and fr.a_norm_error[-1] < fr.a_norm_error[0]
+    # classical PCG hooks (PcgConfig)
+    xp, rp_, hp = ref.pcg_s_solve_hooks(o, tol=1e-8, max_outer=1000, error_reference=xs,
+                                        collect_iterates=True, classical=True)
+    p = cs.DeviceProblem.from_csr(_csr(cs, o)).set_precond("jacobi")
+    pr = p.pcg_solve(cfg=cs.PcgConfig(tol=1e-8, max_iter=1000, error_reference=xs,
+                                      collect_iterates=True), mode="reference")
+    assert pr.x.tobytes() == xp.tobytes()
+    assert pr.report.a_norm_error.tobytes() == hp["aerr"].tobytes()
+    assert len(pr.report.iterates) == len(hp["iter"])

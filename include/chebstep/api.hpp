@@ -209,6 +209,12 @@ struct PoissonSystem {
 };
 /// Assembled on the device (SELL-32) and downloaded; bitwise problems.cpp:13-53.
 PoissonSystem poisson27(const PoissonSpec& spec);
+
+/// Matrix Market coordinate real symmetric, 1-based, expanded to the full
+/// pattern (problems.hpp:28-31); parsed on all host cores.
+CsrMatrix read_matrix_market(const std::string& path, bool require_spd = false);
+/// Lower triangle with round-trip-exact decimal values (problems.hpp:33-34).
+void write_matrix_market(const std::string& path, const CsrMatrix& a);
 /// New 7-point generator with the same conventions (poisson7 = (1,1,1), aniso (1,1,100)).
 PoissonSystem stencil7(const PoissonSpec& spec, double cx = 1.0, double cy = 1.0,
                        double cz = 1.0);

@@ -167,6 +167,30 @@ int cs_halo_map_csr(int64_t row_begin, int64_t row_end, const int64_t* rowptr_lo
                     const int64_t* col_global, int64_t* n_ghost, int64_t* ghost_cols,
                     int64_t ghost_cap, int32_t* col_local);
 
+/* ------------------------------------------------------------ host CSR ingestion (no GPU) */
+/* Library-owned host CSR (int64 offsets/columns, FP64 values). */
+typedef struct cs_csr_host cs_csr_host;
+/* chebstep::read_matrix_market (problems.hpp:28-31, problems.cpp:55-109):
+ * coordinate real symmetric, 1-based, expanded to the full pattern, rows
+ * sorted by column; CS_ERR_PARSE / CS_ERR_INVALID_MATRIX / CS_ERR_NOT_SPD with
+ * the reference's messages. The entry section is parsed by all host cores. */
+int cs_mm_read(const char* path, int require_spd, cs_csr_host** out, int64_t* n, int64_t* nnz);
+/* Rows [row_begin, row_end) of a host CSR: rowptr_local (row_end-row_begin+1,
+ * starting at 0), global columns and values. col/val may be NULL (offsets only). */
+int cs_csr_host_rows(const cs_csr_host* h, int64_t row_begin, int64_t row_end,
+                     int64_t* rowptr_local, int64_t* col, double* val);
+int cs_csr_host_free(cs_csr_host* h);
+/* chebstep::write_matrix_market (problems.hpp:33-34, problems.cpp:111-127):
+ * lower triangle, %.17g values. */
+int cs_mm_write(const char* path, int64_t n, const int64_t* rowptr, const int64_t* col,
+                const double* val);
+/* validate_structure / validate_symmetric / validate_spd_diagonal (csr.hpp:41-47) */
+#define CS_CHECK_STRUCTURE 0
+#define CS_CHECK_SYMMETRIC 1
+#define CS_CHECK_SPD_DIAGONAL 2
+int cs_csr_validate(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                    int check);
+
 /* ------------------------------------------------------------ problems (device-resident) */
 /* Generate a stencil operator directly on the device as SELL-32. With an
  * initialised communicator the rank gets its z-slab of the global nx*ny*nz
@@ -177,6 +201,18 @@ int cs_problem_generate(cs_ctx* ctx, int kind, int64_t nx, int64_t ny, int64_t n
  * layout csr.hpp:12-19) and convert it to SELL-32 on the device. Single rank. */
 int cs_problem_upload_csr(cs_ctx* ctx, int64_t n, const int64_t* rowptr, const int64_t* col,
                           const double* val, cs_problem** out);
+/* Collective over the context's ranks: this rank's row block [row_begin,
+ * row_end) of an n_global x n_global CSR (rowptr_local starts at 0, GLOBAL
+ * column indices). Blocks must be contiguous and ordered by rank. Builds the
+ * ghost list (sorted off-block columns, partition.cpp numbering), the
+ * owner-grouped halo plan (NCCL point-to-point) and the interior slice range
+ * that overlaps the halo. With one rank it equals cs_problem_upload_csr. */
+int cs_problem_upload_csr_block(cs_ctx* ctx, int64_t n_global, int64_t row_begin,
+                                int64_t row_end, const int64_t* rowptr_local,
+                                const int64_t* col_global, const double* val, cs_problem** out);
+/* Matrix Market file -> device problem: every rank parses the file, keeps
+ * its cs_partition_rows(n, 1, nranks, rank) block and uploads it (collective). */
+int cs_problem_read_mm(cs_ctx* ctx, const char* path, int require_spd, cs_problem** out);
 int cs_problem_destroy(cs_problem* p);
 /* n_global, n_local, nnz_local, row_begin, n_ghost, device bytes of the SELL arrays */
 int cs_problem_info(cs_problem* p, int64_t* info6);

@@ -291,6 +291,33 @@ class Oracle:
                                             C.byref(cfg), x, C.byref(rep)))
         return x, self._unpack(rep, bufs)
 
+    # ---------------------------------------------------------------- ingestion (ref only)
+    def mm_read(self, path: str, require_spd: bool = False) -> Csr:
+        assert self.which == "ref"
+        f = self.lib.ref_mm_read
+        f.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                      C.c_void_p, C.c_void_p, C.c_void_p]
+        n, nnz = C.c_int64(), C.c_int64()
+        self._check(f(os.fsencode(path), int(require_spd), C.byref(n), C.byref(nnz), None, None, None))
+        rp = np.zeros(n.value + 1, np.int64)
+        ci = np.zeros(nnz.value, np.int64)
+        v = np.zeros(nnz.value)
+        self._check(f(os.fsencode(path), int(require_spd), C.byref(n), C.byref(nnz),
+                      rp.ctypes.data, ci.ctypes.data, v.ctypes.data))
+        return Csr(n.value, rp, ci, v)
+
+    def mm_write(self, path: str, a: Csr) -> None:
+        assert self.which == "ref"
+        f = self.lib.ref_mm_write
+        f.argtypes = [C.c_char_p, C.c_int64, _i64p, _i64p, _f64p]
+        self._check(f(os.fsencode(path), a.n, a.rowptr, a.col, a.val))
+
+    def csr_validate(self, a: Csr, check: int) -> None:
+        assert self.which == "ref"
+        f = self.lib.ref_csr_validate
+        f.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_int64, C.c_int]
+        self._check(f(a.n, a.rowptr, a.col, a.val, a.col.size, check))
+
     def pcg_s_solve_hooks(self, a: Csr, *, s=4, tol=1e-6, max_outer=500, nu=30, gram="fgs",
                           spectrum=None, precond=1, collect_gram=False, track_true_residual=False,
                           error_reference=None, collect_iterates=False, classical=False):

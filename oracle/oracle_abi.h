@@ -68,6 +68,15 @@ int ref_pcg_solve_hooks(int64_t n, const int64_t* rp, const int64_t* ci, const d
                         const double* b, const double* x0, int precond, double tol, int max_iter,
                         oc_hooks* hk, double* x, oc_report* rep);
 
+/* Matrix Market I/O and CSR validation (problems.cpp:55-127, csr.cpp:58-110),
+ * reference library only. ref_mm_read: call with rp == NULL for n / nnz. */
+int ref_mm_read(const char* path, int require_spd, int64_t* n, int64_t* nnz, int64_t* rp,
+                int64_t* ci, double* v);
+int ref_mm_write(const char* path, int64_t n, const int64_t* rp, const int64_t* ci,
+                 const double* v);
+int ref_csr_validate(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                     int64_t nnz, int check);
+
 #define OC_DECLARE(P)                                                                  \
   int P##poisson27_fill(int64_t nx, int64_t ny, int64_t nz, int64_t* rowptr,           \
                         int64_t* col, double* val);                                   \

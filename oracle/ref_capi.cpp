@@ -370,6 +370,39 @@ int ref_pcg_solve_hooks(int64_t n, const int64_t* rp, const int64_t* ci, const d
   });
 }
 
+int ref_mm_read(const char* path, int require_spd, int64_t* n, int64_t* nnz, int64_t* rp,
+                int64_t* ci, double* v) {
+  return guarded([&] {
+    const cs::CsrMatrix a = cs::read_matrix_market(path, require_spd != 0);
+    *n = a.n;
+    *nnz = a.nnz();
+    if (rp == nullptr) return;
+    std::memcpy(rp, a.row_offsets.data(), sizeof(int64_t) * (a.n + 1));
+    std::memcpy(ci, a.col_indices.data(), sizeof(int64_t) * a.nnz());
+    std::memcpy(v, a.values.data(), sizeof(double) * a.nnz());
+  });
+}
+
+int ref_mm_write(const char* path, int64_t n, const int64_t* rp, const int64_t* ci,
+                 const double* v) {
+  return guarded([&] { cs::write_matrix_market(path, make_csr(n, rp, ci, v)); });
+}
+
+// check: 0 validate_structure, 1 validate_symmetric, 2 validate_spd_diagonal
+int ref_csr_validate(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                     int64_t nnz, int check) {
+  return guarded([&] {
+    cs::CsrMatrix a;
+    a.n = n;
+    a.row_offsets.assign(rp, rp + n + 1);
+    a.col_indices.assign(ci, ci + nnz);
+    a.values.assign(v, v + nnz);
+    if (check == 0) cs::validate_structure(a);
+    else if (check == 1) cs::validate_symmetric(a);
+    else cs::validate_spd_diagonal(a);
+  });
+}
+
 const char* ref_last_error(int* payload) {
   if (payload) *payload = g_payload;
   return g_msg.c_str();

@@ -14,5 +14,6 @@ from .chebstep import (  # noqa: F401
     SolverConfig, SpectrumEstimate, assemble_gram, block_gram, block_update, default_context,
     device_count, estimate_interval, fgs_solve, gram_from_matrix, halo_map_csr, monitor_inexact,
     mpk_chebyshev, partition_rows, pcg_s_solve, pcg_solve, poisson27, random_vector,
-    small_cholesky_solve, spmv, spmv_into, stencil7, tridiag_eigvals)
+    small_cholesky_solve, spmv, spmv_into, stencil7, tridiag_eigvals, read_matrix_market,
+    write_matrix_market, validate_structure, validate_symmetric, validate_spd_diagonal, ParseError)
 from ._lib import LIB_PATH  # noqa: F401

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("CS_LIB") or os.path.join(os.path.dirname(os.path.absp
                                                     "lib", "libchebstep_gpu.so")
 
 CS_OK = 0
+CS_CHECK_STRUCTURE, CS_CHECK_SYMMETRIC, CS_CHECK_SPD_DIAGONAL = 0, 1, 2
 CS_ERR_DIMENSION = 1
 CS_ERR_INVALID_MATRIX = 2
 CS_ERR_NOT_SPD = 3
@@ -86,6 +87,15 @@ SIGNATURES = {
     "cs_problem_generate": (C.c_int, [_vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, _vp,
                                       C.POINTER(_vp)]),
     "cs_problem_upload_csr": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.POINTER(_vp)]),
+    "cs_problem_upload_csr_block": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp,
+                                              C.POINTER(_vp)]),
+    "cs_problem_read_mm": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
+    "cs_mm_read": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_vp), C.POINTER(C.c_int64),
+                             C.POINTER(C.c_int64)]),
+    "cs_csr_host_rows": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp, _vp, _vp]),
+    "cs_csr_host_free": (C.c_int, [_vp]),
+    "cs_mm_write": (C.c_int, [C.c_char_p, C.c_int64, _vp, _vp, _vp]),
+    "cs_csr_validate": (C.c_int, [C.c_int64, _vp, _vp, _vp, C.c_int]),
     "cs_problem_destroy": (C.c_int, [_vp]),
     "cs_problem_info": (C.c_int, [_vp, _i64p]),
     "cs_problem_download_csr": (C.c_int, [_vp, _i64p, _i64p, _f64p]),

@@ -6,9 +6,10 @@
 
 Every .cu/.cpp under csrc/ is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo`` into build/ and
-linked into paper_2603_09790_b200/lib/libchebstep_gpu.so together with NCCL
-(the system libnccl.so.2; inside a torch process the already-loaded
-torch-bundled libnccl.so.2 of the same soname is used).
+linked into paper_2603_09790_b200/lib/libchebstep_gpu.so together with NCCL:
+the torch-bundled libnccl.so.2 (nvidia/nccl in site-packages, rpath'd), so the
+library and torch share ONE NCCL whichever is imported first (the older
+system libnccl.so.2 loaded first would shadow torch's by soname).
 """
 from __future__ import annotations
 
@@ -27,8 +28,16 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "lib", "libchebstep_gpu.so")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+_NCCL = sorted(glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia",
+                                      "nccl")))
+NCCL_DIR = _NCCL[0] if _NCCL and os.path.exists(os.path.join(_NCCL[0], "lib", "libnccl.so.2")) \
+    else None
+NCCL_INC = ["-I" + os.path.join(NCCL_DIR, "include")] if NCCL_DIR else []
+NCCL_LINK = (["-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker",
+              "-rpath," + os.path.join(NCCL_DIR, "lib")] if NCCL_DIR else
+             ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"])
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", *NCCL_INC]
 
 
 def _sources():
@@ -50,7 +59,7 @@ def _stale(target, deps):
 CXX = shutil.which("g++") or "g++"
 CUDA_INC = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
 CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
-            "-I" + CUDA_INC]
+            "-I" + CUDA_INC, *NCCL_INC]
 
 
 EXTRA = [f"-D{d}" for d in os.environ.get("CS_DEFINES", "").split() if d]
@@ -89,8 +98,7 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = True) -> str:
     if errors:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errors))
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-Xlinker", "--no-undefined",
-               "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, *NCCL_LINK, "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

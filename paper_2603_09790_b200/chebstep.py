@@ -18,6 +18,7 @@ Additions beyond the reference API (all optional):
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 import math
 from dataclasses import dataclass, field
@@ -273,6 +274,33 @@ class DeviceProblem:
                                          C.byref(h)))
         return cls(ctx, h)
 
+    @classmethod
+    def from_csr_block(cls, n_global: int, row_begin: int, row_end: int, rowptr_local, col_global,
+                       values, ctx: Optional[Context] = None) -> "DeviceProblem":
+        """Collective: this rank's row block of a general CSR (global columns);
+        builds the owner-grouped halo plan over the context's communicator."""
+        ctx = ctx or default_context()
+        rp = np.ascontiguousarray(rowptr_local, np.int64)
+        ci = np.ascontiguousarray(col_global, np.int64)
+        va = np.ascontiguousarray(values, np.float64)
+        if rp.size != row_end - row_begin + 1:
+            raise DimensionError("rowptr_local must have row_end - row_begin + 1 entries")
+        h = C.c_void_p()
+        _check(lib.cs_problem_upload_csr_block(ctx.handle, n_global, row_begin, row_end,
+                                               rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+                                               C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def read_matrix_market(cls, path: str, require_spd: bool = False,
+                           ctx: Optional[Context] = None) -> "DeviceProblem":
+        """Matrix Market file straight to the device; each rank keeps its
+        cs_partition_rows(n, 1) block (collective when ctx has a communicator)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(lib.cs_problem_read_mm(ctx.handle, os.fsencode(path), int(require_spd), C.byref(h)))
+        return cls(ctx, h)
+
     def close(self):
         if self.handle:
             lib.cs_problem_destroy(self.handle)
@@ -391,6 +419,57 @@ class DeviceProblem:
         _check(lib.cs_pcg_solve_device(self.handle, b_ptr, x0_ptr, tol, max_iter, _mode(mode),
                                        x_ptr, C.byref(rep)))
         return _unpack(rep, bufs)
+
+
+def read_matrix_market(path: str, require_spd: bool = False) -> CsrMatrix:
+    """problems.hpp:28-31 (problems.cpp:55-109): host parse on all cores."""
+    h, n, nnz = C.c_void_p(), C.c_int64(), C.c_int64()
+    _check(lib.cs_mm_read(os.fsencode(path), int(require_spd), C.byref(h), C.byref(n),
+                          C.byref(nnz)))
+    try:
+        rp = np.zeros(n.value + 1, np.int64)
+        ci = np.zeros(nnz.value, np.int64)
+        va = np.zeros(nnz.value, np.float64)
+        _check(lib.cs_csr_host_rows(h, 0, n.value, rp.ctypes.data, ci.ctypes.data, va.ctypes.data))
+    finally:
+        lib.cs_csr_host_free(h)
+    return CsrMatrix(n.value, rp, ci, va)
+
+
+def write_matrix_market(path: str, a: CsrMatrix) -> None:
+    """problems.hpp:33-34 (problems.cpp:111-127): lower triangle, %.17g."""
+    _check(lib.cs_mm_write(os.fsencode(path), a.n, a.row_offsets.ctypes.data,
+                           a.col_indices.ctypes.data, a.values.ctypes.data))
+
+
+def _validate(a: CsrMatrix, check: int) -> None:
+    if check == L.CS_CHECK_SPD_DIAGONAL:  # csr.cpp:100-110 checks no structure first
+        _check(lib.cs_csr_validate(a.n, a.row_offsets.ctypes.data, a.col_indices.ctypes.data,
+                                   a.values.ctypes.data, check))
+        return
+    if a.row_offsets.size != a.n + 1 or a.n < 0:
+        raise InvalidMatrixError("row_offsets length must be n+1")
+    if int(a.row_offsets[0]) != 0:
+        raise InvalidMatrixError("row_offsets[0] must be 0")
+    if a.values.size != a.col_indices.size or int(a.row_offsets[-1]) != a.col_indices.size:
+        raise InvalidMatrixError("row_offsets[n] must equal nnz")
+    _check(lib.cs_csr_validate(a.n, a.row_offsets.ctypes.data, a.col_indices.ctypes.data,
+                               a.values.ctypes.data, check))
+
+
+def validate_structure(a: CsrMatrix) -> None:
+    """csr.cpp:58-79"""
+    _validate(a, L.CS_CHECK_STRUCTURE)
+
+
+def validate_symmetric(a: CsrMatrix) -> None:
+    """csr.cpp:81-98"""
+    _validate(a, L.CS_CHECK_SYMMETRIC)
+
+
+def validate_spd_diagonal(a: CsrMatrix) -> None:
+    """csr.cpp:100-110"""
+    _validate(a, L.CS_CHECK_SPD_DIAGONAL)
 
 
 def poisson27(spec: PoissonSpec, ctx: Optional[Context] = None) -> PoissonSystem:

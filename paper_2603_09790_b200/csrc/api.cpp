@@ -343,6 +343,27 @@ PoissonSystem generated(int kind, const PoissonSpec& spec, const double* coef) {
 }
 }  // namespace
 
+CsrMatrix read_matrix_market(const std::string& path, bool require_spd) {
+  cs_csr_host* h = nullptr;
+  int64_t n = 0, nnz = 0;
+  check(cs_mm_read(path.c_str(), require_spd ? 1 : 0, &h, &n, &nnz));
+  CsrMatrix a;
+  a.n = n;
+  a.row_offsets.resize(static_cast<size_t>(n) + 1);
+  a.col_indices.resize(static_cast<size_t>(nnz));
+  a.values.resize(static_cast<size_t>(nnz));
+  const int rc = cs_csr_host_rows(h, 0, n, a.row_offsets.data(), a.col_indices.data(),
+                                  a.values.data());
+  cs_csr_host_free(h);
+  check(rc);
+  return a;
+}
+
+void write_matrix_market(const std::string& path, const CsrMatrix& a) {
+  check(cs_mm_write(path.c_str(), a.n, a.row_offsets.data(), a.col_indices.data(),
+                    a.values.data()));
+}
+
 PoissonSystem poisson27(const PoissonSpec& spec) { return generated(CS_GEN_POISSON27, spec, nullptr); }
 
 PoissonSystem stencil7(const PoissonSpec& spec, double cx, double cy, double cz) {

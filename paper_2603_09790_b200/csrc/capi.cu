@@ -9,6 +9,7 @@
 #include <functional>
 #include <string>
 
+#include "mmio.hpp"
 #include "runtime.cuh"
 
 namespace csg {
@@ -19,6 +20,8 @@ cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_
                              const double* coef);
 cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, const int64_t* col,
                                const double* val);
+cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin, int64_t row_end,
+                                 const int64_t* rowptr, const int64_t* col, const double* val);
 void problem_set_precond(cs_problem* p, int kind);
 void problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val);
 }  // namespace csg
@@ -196,6 +199,78 @@ int cs_problem_upload_csr(cs_ctx* ctx, int64_t n, const int64_t* rowptr, const i
   return guard([&] {
     need(rowptr, "rowptr");
     *out = problem_upload_csr(ctx, n, rowptr, col, val);
+  });
+}
+
+int cs_problem_upload_csr_block(cs_ctx* ctx, int64_t n_global, int64_t row_begin,
+                                int64_t row_end, const int64_t* rowptr_local,
+                                const int64_t* col_global, const double* val, cs_problem** out) {
+  return guard([&] {
+    need(rowptr_local, "rowptr");
+    *out = problem_upload_block(ctx, n_global, row_begin, row_end, rowptr_local, col_global, val);
+  });
+}
+
+int cs_mm_read(const char* path, int require_spd, cs_csr_host** out, int64_t* n, int64_t* nnz) {
+  return guard([&] {
+    need(path, "path");
+    std::unique_ptr<HostCsr> h(mm_read(path, require_spd != 0));
+    *n = h->n;
+    *nnz = static_cast<int64_t>(h->col.size());
+    *out = reinterpret_cast<cs_csr_host*>(h.release());
+  });
+}
+
+int cs_csr_host_rows(const cs_csr_host* hh, int64_t row_begin, int64_t row_end,
+                     int64_t* rowptr_local, int64_t* col, double* val) {
+  return guard([&] {
+    const HostCsr* h = reinterpret_cast<const HostCsr*>(hh);
+    need(h, "csr");
+    if (row_begin < 0 || row_end < row_begin || row_end > h->n)
+      fail(CS_ERR_DIMENSION, 0, "bad row range");
+    const int64_t b = h->rowptr[row_begin];
+    for (int64_t i = row_begin; i <= row_end; ++i) rowptr_local[i - row_begin] = h->rowptr[i] - b;
+    const int64_t cnt = h->rowptr[row_end] - b;
+    if (col) std::memcpy(col, h->col.data() + b, sizeof(int64_t) * cnt);
+    if (val) std::memcpy(val, h->val.data() + b, sizeof(double) * cnt);
+  });
+}
+
+int cs_csr_host_free(cs_csr_host* h) {
+  return guard([&] { delete reinterpret_cast<HostCsr*>(h); });
+}
+
+int cs_mm_write(const char* path, int64_t n, const int64_t* rowptr, const int64_t* col,
+                const double* val) {
+  return guard([&] {
+    need(path, "path");
+    mm_write(path, n, rowptr, col, val);
+  });
+}
+
+int cs_csr_validate(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                    int check) {
+  return guard([&] {
+    need(rowptr, "rowptr");
+    if (check == CS_CHECK_STRUCTURE) validate_structure_host(n, rowptr, col, val, n + 1, rowptr[n]);
+    else if (check == CS_CHECK_SYMMETRIC) validate_symmetric_host(n, rowptr, col, val);
+    else if (check == CS_CHECK_SPD_DIAGONAL) validate_spd_diagonal_host(n, rowptr, col, val);
+    else fail(CS_ERR_INVALID_ARGUMENT, 0, "unknown check");
+  });
+}
+
+int cs_problem_read_mm(cs_ctx* ctx, const char* path, int require_spd, cs_problem** out) {
+  return guard([&] {
+    need(path, "path");
+    std::unique_ptr<HostCsr> h(mm_read(path, require_spd != 0));
+    int64_t b = 0, e = h->n;
+    if (ctx->nranks > 1 && cs_partition_rows(h->n, 1, ctx->nranks, ctx->rank, &b, &e) != CS_OK)
+      fail(CS_ERR_INVALID_ARGUMENT, 0, "matrix has fewer rows than ranks");
+    std::vector<int64_t> rp(static_cast<size_t>(e - b) + 1);
+    const int64_t off = h->rowptr[b];
+    for (int64_t i = b; i <= e; ++i) rp[i - b] = h->rowptr[i] - off;
+    *out = problem_upload_block(ctx, h->n, b, e, rp.data(), h->col.data() + off,
+                                h->val.data() + off);
   });
 }
 

@@ -23,9 +23,16 @@ void scan_slice_ptr(const int64_t* widths, int64_t nslices, int64_t* slice_ptr, 
 // CSR (device, int64) -> SELL-32; validates offsets and column range into *bad.
 void launch_csr_widths(int64_t n, const int64_t* rowptr, int64_t nslices, int64_t* widths,
                        int* bad, cudaStream_t st);
-void launch_csr_fill(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+// row block [row_begin, row_begin+n) of an n_global CSR with global columns
+// (ghosts: sorted off-block columns, local n + index)
+void launch_csr_fill(int64_t n, int64_t row_begin, int64_t n_global, const int64_t* ghosts,
+                     int64_t n_ghost, const int64_t* rowptr, const int64_t* col, const double* val,
                      int64_t nslices, const int64_t* slice_ptr, double* vals, int32_t* cols,
                      double* diag, int* bad, cudaStream_t st);
+void launch_slice_ghost_flag(int64_t n_local, int64_t nslices, const int64_t* slice_ptr,
+                             const int32_t* cols, unsigned char* flag, cudaStream_t st);
+void launch_halo_gather(int64_t count, const int32_t* idx, const double* x, double* buf,
+                        cudaStream_t st);
 // SELL -> CSR row lengths and fill (global columns via row_begin / ghost map)
 void launch_sell_row_len(const SellView& a, int64_t* len, cudaStream_t st);
 void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* ghost_global,

@@ -76,6 +76,19 @@ void* ctx_scratch(cs_ctx* c, size_t bytes) {
 
 void halo_exchange_on(cs_problem* p, double* col, cudaStream_t st) {
   cs_ctx* c = p->ctx;
+  if (p->general_halo) {
+    double* buf = p->send_buf.as<double>();
+    launch_halo_gather(p->send_off.back(), p->send_idx.as<int32_t>(), col, buf, st);
+    CS_NCCL(ncclGroupStart());
+    for (int q = 0; q < c->nranks; ++q) {
+      const int64_t rc = p->recv_off[q + 1] - p->recv_off[q];
+      const int64_t sc = p->send_off[q + 1] - p->send_off[q];
+      if (rc) CS_NCCL(ncclRecv(col + p->n_local + p->recv_off[q], rc, ncclDouble, q, c->comm, st));
+      if (sc) CS_NCCL(ncclSend(buf + p->send_off[q], sc, ncclDouble, q, c->comm, st));
+    }
+    CS_NCCL(ncclGroupEnd());
+    return;
+  }
   CS_NCCL(ncclGroupStart());
   if (p->ghost_lo > 0) {
     CS_NCCL(ncclRecv(col + p->n_local, p->ghost_lo, ncclDouble, c->rank - 1, c->comm, st));
@@ -92,7 +105,7 @@ void halo_exchange_on(cs_problem* p, double* col, cudaStream_t st) {
 
 void halo_exchange(cs_problem* p, double* col) {
   cs_ctx* c = p->ctx;
-  if (c->nranks == 1 || (p->ghost_lo == 0 && p->ghost_hi == 0)) return;
+  if (c->nranks == 1 || !p->has_halo()) return;
   Launch L(c, CS_PHASE_COMM);
   halo_exchange_on(p, col, c->stream);
 }
@@ -100,7 +113,7 @@ void halo_exchange(cs_problem* p, double* col) {
 void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand) {
   cs_ctx* c = p->ctx;
   const SellView A = p->view();
-  const bool halo = c->nranks > 1 && (p->ghost_lo > 0 || p->ghost_hi > 0);
+  const bool halo = c->nranks > 1 && p->has_halo();
   const bool overlap = halo && kind != kDot && p->slice_int_end > p->slice_int_begin;
   if (!overlap) {
     if (halo) halo_exchange(p, operand);
@@ -384,12 +397,127 @@ cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_
   return p.release();
 }
 
-cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, const int64_t* col,
-                               const double* val) {
-  if (c->nranks > 1)
-    fail(CS_ERR_INVALID_ARGUMENT, 0, "CSR upload is single-rank; use generated problems for P>1");
-  if (n < 0) fail(CS_ERR_DIMENSION, 0, "negative dimension");
-  if (n >= (int64_t{1} << 31)) fail(CS_ERR_INVALID_ARGUMENT, 0, "n exceeds int32 column range");
+namespace {
+
+// Collective halo plan of a general CSR row block (all ranks call): owner
+// ranges by allgather, then every rank tells each owner which of its rows it
+// needs (counts, then the global row ids) -- point-to-point over NCCL.
+void plan_general_halo(cs_problem* p) {
+  cs_ctx* c = p->ctx;
+  const int P = c->nranks, me = c->rank;
+  p->general_halo = true;
+  p->send_off.assign(P + 1, 0);
+  p->recv_off.assign(P + 1, 0);
+  if (P == 1) {
+    if (p->n_ghost) fail(CS_ERR_INVALID_MATRIX, 0, "column index out of range");
+    p->send_idx.alloc(8);
+    p->send_buf.alloc(8);
+    return;
+  }
+  DBuf ranges(sizeof(int64_t) * 2 * (P + 1));
+  const int64_t mine[2] = {p->row_begin, p->row_begin + p->n_local};
+  int64_t* dr = ranges.as<int64_t>();
+  CS_CUDA(cudaMemcpyAsync(dr + 2 * P, mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+  CS_NCCL(ncclAllGather(dr + 2 * P, dr, 2, ncclInt64, c->comm, c->stream));
+  std::vector<int64_t> r(2 * P);
+  CS_CUDA(cudaMemcpyAsync(r.data(), dr, sizeof(int64_t) * 2 * P, cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < P; ++q)
+    if (r[2 * q] != (q ? r[2 * q - 1] : 0) || r[2 * q + 1] < r[2 * q])
+      fail(CS_ERR_INVALID_ARGUMENT, 0, "row blocks must be contiguous and ordered by rank");
+  if (r[2 * P - 1] != p->n_global)
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "row blocks must cover all rows");
+  // ghosts are sorted, owners own ascending row ranges: one segment per owner
+  const std::vector<int64_t>& g = p->ghosts_host;
+  for (int q = 0; q < P; ++q) {
+    const auto hi = std::lower_bound(g.begin(), g.end(), r[2 * q + 1]);
+    p->recv_off[q + 1] = hi - g.begin();
+  }
+  if (p->recv_off[me + 1] != p->recv_off[me])
+    fail(CS_ERR_INVALID_MATRIX, 0, "ghost column inside the owned block");
+  std::vector<int64_t> rcnt(P), scnt(P);
+  for (int q = 0; q < P; ++q) rcnt[q] = p->recv_off[q + 1] - p->recv_off[q];
+  DBuf cnt(sizeof(int64_t) * 2 * P);
+  int64_t* dc = cnt.as<int64_t>();
+  CS_CUDA(cudaMemcpyAsync(dc, rcnt.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, c->stream));
+  CS_NCCL(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    CS_NCCL(ncclSend(dc + q, 1, ncclInt64, q, c->comm, c->stream));
+    CS_NCCL(ncclRecv(dc + P + q, 1, ncclInt64, q, c->comm, c->stream));
+  }
+  CS_NCCL(ncclGroupEnd());
+  CS_CUDA(cudaMemcpyAsync(scnt.data(), dc + P, sizeof(int64_t) * P, cudaMemcpyDeviceToHost,
+                          c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  scnt[me] = 0;
+  for (int q = 0; q < P; ++q) p->send_off[q + 1] = p->send_off[q] + scnt[q];
+  const int64_t ns = p->send_off[P], nr = p->recv_off[P];
+  DBuf req(sizeof(int64_t) * std::max<int64_t>(nr, 1)), got(sizeof(int64_t) * std::max<int64_t>(ns, 1));
+  if (nr)
+    CS_CUDA(cudaMemcpyAsync(req.p, g.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice,
+                            c->stream));
+  CS_NCCL(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (rcnt[q]) CS_NCCL(ncclSend(req.as<int64_t>() + p->recv_off[q], rcnt[q], ncclInt64, q, c->comm, c->stream));
+    if (scnt[q]) CS_NCCL(ncclRecv(got.as<int64_t>() + p->send_off[q], scnt[q], ncclInt64, q, c->comm, c->stream));
+  }
+  CS_NCCL(ncclGroupEnd());
+  std::vector<int64_t> rows(ns);
+  if (ns)
+    CS_CUDA(cudaMemcpyAsync(rows.data(), got.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost,
+                            c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<int32_t> idx(ns);
+  for (int64_t k = 0; k < ns; ++k) {
+    const int64_t l = rows[k] - p->row_begin;
+    if (l < 0 || l >= p->n_local) fail(CS_ERR_GENERIC, 0, "halo request outside the owned block");
+    idx[k] = static_cast<int32_t>(l);
+  }
+  p->send_idx.alloc(sizeof(int32_t) * std::max<int64_t>(ns, 1));
+  p->send_buf.alloc(sizeof(double) * std::max<int64_t>(ns, 1));
+  if (ns)
+    CS_CUDA(cudaMemcpyAsync(p->send_idx.p, idx.data(), sizeof(int32_t) * ns,
+                            cudaMemcpyHostToDevice, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// longest run of slices without ghost columns: computed while the halo flies
+void interior_range(cs_problem* p) {
+  cs_ctx* c = p->ctx;
+  p->slice_int_begin = 0;
+  p->slice_int_end = p->nslices;
+  if (p->n_ghost == 0 || p->nslices == 0) return;
+  DBuf flag(static_cast<size_t>(p->nslices));
+  launch_slice_ghost_flag(p->n_local, p->nslices, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(),
+                          flag.as<unsigned char>(), c->stream);
+  std::vector<unsigned char> f(p->nslices);
+  CS_CUDA(cudaMemcpyAsync(f.data(), flag.p, f.size(), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  int64_t best_b = 0, best_e = 0;
+  for (int64_t s = 0; s < p->nslices;) {
+    if (f[s]) {
+      ++s;
+      continue;
+    }
+    int64_t e = s;
+    while (e < p->nslices && !f[e]) ++e;
+    if (e - s > best_e - best_b) best_b = s, best_e = e;
+    s = e;
+  }
+  p->slice_int_begin = best_b;
+  p->slice_int_end = best_e;
+}
+
+}  // namespace
+
+cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin, int64_t row_end,
+                                 const int64_t* rowptr, const int64_t* col, const double* val) {
+  if (n_global < 0 || row_begin < 0 || row_end < row_begin || row_end > n_global)
+    fail(CS_ERR_DIMENSION, 0, "bad row block");
+  if (c->nranks == 1 && (row_begin != 0 || row_end != n_global))
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "single rank must own every row");
+  const int64_t n = row_end - row_begin;
   if (rowptr[0] != 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[0] must be 0");
   const int64_t nnz = rowptr[n];
   if (nnz < 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[n] must equal nnz");
@@ -397,12 +525,28 @@ cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, cons
   StreamBind bind_stream_(c->stream);
   auto p = std::make_unique<cs_problem>();
   p->ctx = c;
-  p->n_global = p->n_local = n;
-  p->ld = round_up(std::max<int64_t>(n, 1), 32);
+  p->n_global = n_global;
+  p->row_begin = row_begin;
+  p->n_local = n;
+  if (c->nranks > 1) {
+    // sorted unique off-block columns (partition.cpp numbering)
+    std::vector<int64_t>& g = p->ghosts_host;
+    for (int64_t k = 0; k < nnz; ++k)
+      if (col[k] < row_begin || col[k] >= row_end)
+        if (col[k] >= 0 && col[k] < n_global) g.push_back(col[k]);
+    std::sort(g.begin(), g.end());
+    g.erase(std::unique(g.begin(), g.end()), g.end());
+  }
+  p->n_ghost = static_cast<int64_t>(p->ghosts_host.size());
+  if (n + p->n_ghost >= (int64_t{1} << 31))
+    fail(CS_ERR_INVALID_ARGUMENT, 0, "rank block exceeds int32 column range");
+  p->ld = round_up(std::max<int64_t>(n + p->n_ghost, 1), 32);
   p->nslices = (n + kSliceRows - 1) / kSliceRows;
   p->nnz_local = nnz;
-  p->slice_int_begin = 0;
-  p->slice_int_end = p->nslices;
+  p->ghost_global.alloc(sizeof(int64_t) * std::max<int64_t>(p->n_ghost, 1));
+  if (p->n_ghost)
+    CS_CUDA(cudaMemcpyAsync(p->ghost_global.p, p->ghosts_host.data(), sizeof(int64_t) * p->n_ghost,
+                            cudaMemcpyHostToDevice, c->stream));
   DBuf drp(sizeof(int64_t) * (n + 1)), dcol(sizeof(int64_t) * std::max<int64_t>(nnz, 1)),
       dval(sizeof(double) * std::max<int64_t>(nnz, 1)), bad(sizeof(int));
   CS_CUDA(cudaMemcpyAsync(drp.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice,
@@ -424,20 +568,47 @@ cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, cons
   int hbad = 0;
   CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   const int64_t total = read_i64(c, p->slice_ptr.as<int64_t>() + p->nslices);
-  if (hbad) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets must be nondecreasing");
-  p->vals.alloc(sizeof(double) * std::max<int64_t>(total, 1));
-  p->cols.alloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
-  p->diag.alloc(sizeof(double) * std::max<int64_t>(n, 1));
-  if (p->nslices > 0)
-    launch_csr_fill(n, drp.as<int64_t>(), dcol.as<int64_t>(), dval.as<double>(), p->nslices,
-                    p->slice_ptr.as<int64_t>(), p->vals.as<double>(), p->cols.as<int32_t>(),
-                    p->diag.as<double>(), bad.as<int>(), c->stream);
-  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CS_CUDA(cudaStreamSynchronize(c->stream));
-  if (hbad) fail(CS_ERR_INVALID_MATRIX, 0, "column index out of range");
+  // a local validation failure must not leave peers waiting in the halo plan
+  int local_err = hbad ? 1 : 0;
+  if (!local_err) {
+    p->vals.alloc(sizeof(double) * std::max<int64_t>(total, 1));
+    p->cols.alloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
+    p->diag.alloc(sizeof(double) * std::max<int64_t>(n, 1));
+    if (p->nslices > 0)
+      launch_csr_fill(n, row_begin, n_global, p->ghost_global.as<int64_t>(), p->n_ghost,
+                      drp.as<int64_t>(), dcol.as<int64_t>(), dval.as<double>(), p->nslices,
+                      p->slice_ptr.as<int64_t>(), p->vals.as<double>(), p->cols.as<int32_t>(),
+                      p->diag.as<double>(), bad.as<int>(), c->stream);
+    CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    local_err = hbad ? 2 : 0;
+  }
+  if (c->nranks > 1) {
+    // agree on failure before any point-to-point traffic
+    DBuf e(sizeof(int));
+    CS_CUDA(cudaMemcpyAsync(e.p, &local_err, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CS_NCCL(ncclAllReduce(e.p, e.p, 1, ncclInt32, ncclMax, c->comm, c->stream));
+    int any = 0;
+    CS_CUDA(cudaMemcpyAsync(&any, e.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    if (any && !local_err) fail(CS_ERR_INVALID_MATRIX, 0, "invalid row block on another rank");
+  }
+  if (local_err == 1) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets must be nondecreasing");
+  if (local_err == 2) fail(CS_ERR_INVALID_MATRIX, 0, "column index out of range");
+  interior_range(p.get());
+  plan_general_halo(p.get());
   compress_sell(p.get());
-  p->ghost_global.alloc(8);
   return p.release();
+}
+
+cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, const int64_t* col,
+                               const double* val) {
+  if (c->nranks > 1)
+    fail(CS_ERR_INVALID_ARGUMENT, 0,
+         "CSR upload of a whole matrix is single-rank; use cs_problem_upload_csr_block for P>1");
+  if (n < 0) fail(CS_ERR_DIMENSION, 0, "negative dimension");
+  if (n >= (int64_t{1} << 31)) fail(CS_ERR_INVALID_ARGUMENT, 0, "n exceeds int32 column range");
+  return problem_upload_block(c, n, 0, n, rowptr, col, val);
 }
 
 void problem_set_precond(cs_problem* p, int kind) {

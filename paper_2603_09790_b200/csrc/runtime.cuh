@@ -116,6 +116,16 @@ struct cs_problem {
   int64_t slice_int_begin = 0, slice_int_end = 0;  // interior slices (no ghost columns)
   // halo: ghosts = [lower plane (from rank-1) | upper plane (from rank+1)]
   int64_t ghost_lo = 0, ghost_hi = 0, send_lo = 0, send_hi = 0;
+  // general CSR blocks: ghosts grouped by owner rank (ascending global order);
+  // peer q receives x[send_idx[send_off[q] .. send_off[q+1])] and sends its
+  // rows into ghost slots [recv_off[q], recv_off[q+1])
+  bool general_halo = false;
+  std::vector<int64_t> send_off, recv_off;  // nranks + 1 each
+  csg::DBuf send_idx, send_buf;
+  bool has_halo() const {
+    if (!general_halo) return ghost_lo > 0 || ghost_hi > 0;
+    return send_off.back() > 0 || recv_off.back() > 0;
+  }
   int gen_kind = -1;
   int64_t nx = 0, ny = 0, nz = 0;
   csg::DBuf slice_ptr, vals, cols, meta, pat, diag, inv_diag, ghost_global;

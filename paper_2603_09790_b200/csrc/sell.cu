@@ -13,6 +13,7 @@
 //    entries keep ascending GLOBAL column order, so per-row summation order
 //    is partition-invariant.
 //  * CSR -> SELL conversion for uploaded reference CsrMatrix data.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cub/device/device_scan.cuh>
@@ -162,7 +163,24 @@ __device__ double csr_lower_bound_diag(const int64_t* col, const double* val, in
   return val[first];
 }
 
-__global__ void csr_fill_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+// Row block [row_begin, row_begin + n) of an n_global CSR with GLOBAL columns:
+// owned columns map to c - row_begin, off-block columns to n + (index in the
+// sorted ghost list) (partition.cpp numbering); stored order is kept.
+__device__ __forceinline__ int32_t local_col(int64_t c, int64_t row_begin, int64_t n,
+                                             const int64_t* __restrict__ ghosts, int64_t n_ghost) {
+  if (c >= row_begin && c < row_begin + n) return static_cast<int32_t>(c - row_begin);
+  int64_t lo = 0, hi = n_ghost;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ghosts[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return static_cast<int32_t>(n + lo);
+}
+
+__global__ void csr_fill_kernel(int64_t n, int64_t row_begin, int64_t n_global,
+                                const int64_t* __restrict__ ghosts, int64_t n_ghost,
+                                const int64_t* __restrict__ rowptr,
                                 const int64_t* __restrict__ col, const double* __restrict__ val,
                                 int64_t nslices, const int64_t* __restrict__ slice_ptr,
                                 double* vals, int32_t* cols, double* diag_out, int* bad) {
@@ -179,21 +197,43 @@ __global__ void csr_fill_kernel(int64_t n, const int64_t* __restrict__ rowptr,
     const int64_t b = rowptr[row], e = rowptr[row + 1];
     for (int64_t t = b; t < e; ++t, ++k) {
       const int64_t c = col[t];
-      if (c < 0 || c >= n) {
+      if (c < 0 || c >= n_global) {
         atomicExch(bad, 2);
         cp[k * kSliceRows] = -1;
         vp[k * kSliceRows] = 0.0;
         continue;
       }
-      cp[k * kSliceRows] = static_cast<int32_t>(c);
+      cp[k * kSliceRows] = local_col(c, row_begin, n, ghosts, n_ghost);
       vp[k * kSliceRows] = val[t];
     }
-    diag_out[row] = csr_lower_bound_diag(col, val, b, e, row);
+    diag_out[row] = csr_lower_bound_diag(col, val, b, e, row_begin + row);
   }
   for (; k < width; ++k) {
     cp[k * kSliceRows] = -1;
     vp[k * kSliceRows] = 0.0;
   }
+}
+
+// flag[s] = 1 when slice s (explicit SELL-32) references a ghost column
+__global__ void slice_ghost_flag_kernel(int64_t n_local, int64_t nslices,
+                                        const int64_t* __restrict__ slice_ptr,
+                                        const int32_t* __restrict__ cols, unsigned char* flag) {
+  const int64_t slice = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (slice >= nslices) return;
+  const int lane = threadIdx.x & 31;
+  bool g = false;
+  for (int64_t t = slice_ptr[slice] + lane; t < slice_ptr[slice + 1]; t += kSliceRows)
+    g |= cols[t] >= n_local;
+  g = __any_sync(0xffffffffu, g);
+  if (lane == 0) flag[slice] = g ? 1 : 0;
+}
+
+// halo send buffer: buf[k] = x[idx[k]]
+__global__ void halo_gather_kernel(int64_t count, const int32_t* __restrict__ idx,
+                                   const double* __restrict__ x, double* __restrict__ buf) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    buf[k] = x[idx[k]];
 }
 
 // column of slot k of `lane` in slice `slice`, or -1 for an empty slot
@@ -384,11 +424,29 @@ void launch_csr_widths(int64_t n, const int64_t* rowptr, int64_t nslices, int64_
   CS_CUDA(cudaGetLastError());
 }
 
-void launch_csr_fill(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+void launch_csr_fill(int64_t n, int64_t row_begin, int64_t n_global, const int64_t* ghosts,
+                     int64_t n_ghost, const int64_t* rowptr, const int64_t* col, const double* val,
                      int64_t nslices, const int64_t* slice_ptr, double* vals, int32_t* cols,
                      double* diag, int* bad, cudaStream_t st) {
-  csr_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(n, rowptr, col, val, nslices,
-                                                               slice_ptr, vals, cols, diag, bad);
+  csr_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
+      n, row_begin, n_global, ghosts, n_ghost, rowptr, col, val, nslices, slice_ptr, vals, cols,
+      diag, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_slice_ghost_flag(int64_t n_local, int64_t nslices, const int64_t* slice_ptr,
+                             const int32_t* cols, unsigned char* flag, cudaStream_t st) {
+  if (nslices == 0) return;
+  slice_ghost_flag_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(n_local, nslices,
+                                                                       slice_ptr, cols, flag);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_halo_gather(int64_t count, const int32_t* idx, const double* x, double* buf,
+                        cudaStream_t st) {
+  if (count == 0) return;
+  const int64_t blocks = std::min<int64_t>((count + kThreads - 1) / kThreads, 148 * 8);
+  halo_gather_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(count, idx, x, buf);
   CS_CUDA(cudaGetLastError());
 }
 

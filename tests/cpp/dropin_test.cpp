@@ -129,6 +129,30 @@ int main() {
     dim = true;
   }
   EXPECT(dim);
+  // --- Matrix Market round trip: drop-in writer/reader == reference reader
+  {
+    const char* path = "/tmp/dropin_mm_test.mtx";
+    cs::write_matrix_market(path, sys.a);
+    const cs::CsrMatrix back = cs::read_matrix_market(path, true);
+    int64_t rn = 0, rnnz = 0;
+    EXPECT(ref_mm_read(path, 1, &rn, &rnnz, nullptr, nullptr, nullptr) == 0);
+    std::vector<int64_t> rrp(rn + 1), rci(rnnz);
+    std::vector<double> rv(rnnz);
+    EXPECT(ref_mm_read(path, 1, &rn, &rnnz, rrp.data(), rci.data(), rv.data()) == 0);
+    EXPECT(back.n == rn && back.nnz() == rnnz);
+    EXPECT(same_bits(back.row_offsets.data(), rrp.data(), rn + 1));
+    EXPECT(same_bits(back.col_indices.data(), rci.data(), rnnz));
+    EXPECT(same_bits(back.values.data(), rv.data(), rnnz));
+    EXPECT(same_bits(back.values.data(), sys.a.values.data(), nnz));
+    bool parse = false;
+    try {
+      cs::read_matrix_market("/nonexistent/x.mtx");
+    } catch (const cs::ParseError&) {
+      parse = true;
+    }
+    EXPECT(parse);
+    std::remove(path);
+  }
   std::printf("%s (%d failures)\n", failures ? "DROPIN FAIL" : "DROPIN OK", failures);
   return failures ? 1 : 0;
 }

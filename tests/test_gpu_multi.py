@@ -20,23 +20,28 @@ def _gpus():
         return 0
 
 
-@pytest.mark.parametrize("stencil,n,nz", [("poisson27", 40, 48), ("poisson7", 32, 40)])
-def test_multi_gpu_parity(stencil, n, nz):
+@pytest.mark.parametrize("stencil,n,nz,mm", [("poisson27", 40, 48, False),
+                                             ("poisson7", 32, 40, False),
+                                             ("poisson27", 24, 32, True)])
+def test_multi_gpu_parity(stencil, n, nz, mm, tmp_path):
     ng = _gpus()
     if ng < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(ng, 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + 7 * mm),
            os.path.join(ROOT, "tools", "mgpu_check.py"), "--grid", str(n), "--nz", str(nz),
-           "--stencil", stencil]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+           "--stencil", stencil] + (["--mm"] if mm else [])
+    env = dict(os.environ, MGPU_TMP=str(tmp_path))
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     line = [l for l in out.stdout.splitlines() if l.startswith("MGPU ")]
     assert line, out.stdout[-3000:] + out.stderr[-3000:]
     res = json.loads(line[0][5:])
     assert len(res) == world
     for r in res:
         assert r["assembly_bitwise"] and r["ghosts_ok"] and r["spmv_bitwise"], r
+        if mm:
+            assert r["n_ghost"] > 0, r
         assert r["outer_ok"], r
         assert r["x_rel"] <= 1e-8, r
         assert abs(r["pcg_iters"][0] - r["pcg_iters"][1]) <= 1 and r["pcg_x_rel"] <= 1e-8, r

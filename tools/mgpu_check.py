@@ -23,12 +23,42 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+def shuffled(o, seed):
+    """P A P^T for a permutation that shuffles rows inside windows of 4096 and
+    swaps a few rows across the whole range: an irregular but partly local
+    halo. Rows stay sorted by column (reference CsrMatrix invariant)."""
+    from oracle.oracle import Csr
+    rng = np.random.default_rng(seed)
+    perm = np.arange(o.n)
+    for s in range(0, o.n, 4096):
+        rng.shuffle(perm[s:s + 4096])
+    for _ in range(16):
+        i, j = rng.integers(0, o.n, 2)
+        perm[i], perm[j] = perm[j], perm[i]
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(o.n)
+    lens = np.diff(o.rowptr)[perm]
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col = np.empty_like(o.col)
+    val = np.empty_like(o.val)
+    for i in range(o.n):
+        a0, a1 = o.rowptr[perm[i]], o.rowptr[perm[i] + 1]
+        c = inv[o.col[a0:a1]]
+        k = np.argsort(c, kind="stable")
+        col[rp[i]:rp[i + 1]] = c[k]
+        val[rp[i]:rp[i + 1]] = o.val[a0:a1][k]
+    return Csr(o.n, rp, col, val)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=48)
     ap.add_argument("--nz", type=int, default=0)
     ap.add_argument("--s", type=int, default=4)
     ap.add_argument("--stencil", default="poisson27")
+    ap.add_argument("--mm", action="store_true",
+                    help="general CSR path: a locally shuffled operator read from a Matrix "
+                         "Market file (irregular, owner-grouped halo)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -45,18 +75,30 @@ def main():
     n, nz = a.grid, a.nz or a.grid
     port = Oracle("port")
     o = port.poisson27(n, n, nz) if a.stencil == "poisson27" else port.stencil7(n, n, nz)
-    p = cs.DeviceProblem.generate(a.stencil, n, n, nz, ctx=ctx).set_precond("jacobi")
+    if a.mm:
+        o = shuffled(o, seed=7)
+        path = os.path.join(os.environ.get("MGPU_TMP", "/tmp"), f"mgpu_{n}_{nz}_{a.stencil}.mtx")
+        if rank == 0:
+            cs.write_matrix_market(path, cs.CsrMatrix(o.n, o.rowptr, o.col, o.val))
+        dist.barrier()
+        p = cs.DeviceProblem.read_matrix_market(path, True, ctx=ctx).set_precond("jacobi")
+    else:
+        p = cs.DeviceProblem.generate(a.stencil, n, n, nz, ctx=ctx).set_precond("jacobi")
     b0, e0 = p.row_begin, p.row_begin + p.n_local
-    res = {"rank": rank, "rows": [b0, e0]}
+    res = {"rank": rank, "rows": [b0, e0], "n_ghost": p.n_ghost}
     loc = p.to_csr()
     rp = o.rowptr[b0:e0 + 1] - o.rowptr[b0]
     res["assembly_bitwise"] = bool(
         loc.row_offsets.tobytes() == rp.tobytes()
         and loc.col_indices.tobytes() == o.col[o.rowptr[b0]:o.rowptr[e0]].tobytes()
         and loc.values.tobytes() == o.val[o.rowptr[b0]:o.rowptr[e0]].tobytes())
-    plane = n * n
-    want = (list(range(b0 - plane, b0)) if b0 > 0 else []) + \
-        (list(range(e0, e0 + plane)) if e0 < o.n else [])
+    if a.mm:
+        cols = o.col[o.rowptr[b0]:o.rowptr[e0]]
+        want = np.unique(cols[(cols < b0) | (cols >= e0)]).tolist()
+    else:
+        plane = n * n
+        want = (list(range(b0 - plane, b0)) if b0 > 0 else []) + \
+            (list(range(e0, e0 + plane)) if e0 < o.n else [])
     res["ghosts_ok"] = p.ghosts().tolist() == want
     xg = np.random.default_rng(3).standard_normal(o.n)
     y = p.spmv(xg[b0:e0])

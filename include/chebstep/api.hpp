@@ -22,6 +22,8 @@
 #include <utility>
 #include <vector>
 
+typedef struct cs_problem cs_problem;
+
 namespace chebstep {
 
 using index_t = std::int64_t;  // util.hpp:10
@@ -263,6 +265,15 @@ struct GramSystem {
 };
 GramSystem assemble_gram(const VectorBlock& q, const VectorBlock& aq);
 GramSystem gram_from_matrix(const SmallDense& w);
+/// W_c = D^-1/2 W D^-1/2 with an exact unit diagonal (gram.hpp:52-56).
+GramSystem normalize_gram(const GramSystem& g);
+struct FgsRate {
+  double spectral_norm;    // ||L^T (I+L)^{-1}||_2
+  double spectral_radius;  // rho(L^T (I+L)^{-1})
+};
+/// Norm and radius of the FGS residual iteration matrix of a normalized
+/// system (gram.hpp:58-66); host eigensolvers instead of dgesvd/dgeev.
+FgsRate fgs_rate(const GramSystem& g);
 struct FgsConfig {
   int nu = 30;
   bool multi_rhs = true;
@@ -351,6 +362,41 @@ void set_mode(Mode m);
 Mode mode();
 /// CUDA device used by the drop-in entry points (default 0).
 void set_device(int device);
+
+/// Device-resident operator (SELL-32P in HBM + preconditioner), the
+/// boundary's addition for sizes whose host CSR would not fit.
+/// Generated problems are assembled on the device; Matrix Market files are
+/// parsed on the host and uploaded once.
+class DeviceProblem {
+ public:
+  static DeviceProblem poisson27(const PoissonSpec& spec);
+  static DeviceProblem stencil7(const PoissonSpec& spec, double cx = 1.0, double cy = 1.0,
+                                double cz = 1.0);
+  static DeviceProblem from_csr(const CsrMatrix& a);
+  static DeviceProblem read_matrix_market(const std::string& path, bool require_spd = true);
+  void set_precond(const Preconditioner& m);
+  index_t n_global() const { return n_global_; }
+  index_t n_local() const { return n_local_; }
+  index_t nnz_local() const { return nnz_local_; }
+  index_t row_begin() const { return row_begin_; }
+  cs_problem* handle() const { return p_; }
+  ~DeviceProblem();
+  DeviceProblem(DeviceProblem&& o) noexcept;
+  DeviceProblem& operator=(DeviceProblem&& o) noexcept;
+  DeviceProblem(const DeviceProblem&) = delete;
+  DeviceProblem& operator=(const DeviceProblem&) = delete;
+
+ private:
+  explicit DeviceProblem(cs_problem* p);
+  cs_problem* p_ = nullptr;
+  index_t n_global_ = 0, n_local_ = 0, nnz_local_ = 0, row_begin_ = 0;
+};
+
+/// pcg_s_solve / pcg_solve on a device-resident problem (b, x0, x host vectors).
+SolveResult pcg_s_solve(const DeviceProblem& p, std::span<const double> b,
+                        std::span<const double> x0, const SolverConfig& cfg);
+SolveResult pcg_solve(const DeviceProblem& p, std::span<const double> b,
+                      std::span<const double> x0, const PcgConfig& cfg);
 }  // namespace gpu
 
 }  // namespace chebstep

@@ -167,6 +167,16 @@ int cs_halo_map_csr(int64_t row_begin, int64_t row_end, const int64_t* rowptr_lo
                     const int64_t* col_global, int64_t* n_ghost, int64_t* ghost_cols,
                     int64_t ghost_cap, int32_t* col_local);
 
+/* ------------------------------------------------------------ small dense analysis (host) */
+/* chebstep::fgs_rate (gram.hpp:58-66, gram.cpp:148-174) of a NORMALIZED s x s
+ * Gram matrix w (column-major, unit diagonal): largest singular value and
+ * spectral radius of the FGS residual iteration matrix L^T (I+L)^{-1}.
+ * Host eigen/singular solvers replace the reference's dgesvd/dgeev
+ * (agreement ~1e-13 relative). */
+int cs_fgs_rate(int s, const double* w, double* spectral_norm, double* spectral_radius);
+/* kappa_2 of a symmetric s x s matrix (solver.cpp:69-74: dsyevd there). */
+int cs_kappa_sym(int s, const double* w, double* kappa);
+
 /* ------------------------------------------------------------ host CSR ingestion (no GPU) */
 /* Library-owned host CSR (int64 offsets/columns, FP64 values). */
 typedef struct cs_csr_host cs_csr_host;

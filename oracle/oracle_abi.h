@@ -77,6 +77,11 @@ int ref_mm_write(const char* path, int64_t n, const int64_t* rp, const int64_t* 
 int ref_csr_validate(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
                      int64_t nnz, int check);
 
+/* fgs_rate(normalize_gram(gram_from_matrix(w))) (gram.cpp:60-76,148-174) and
+ * kappa_of via dsyevd (solver.cpp:69-74), reference library only */
+int ref_fgs_rate_normalized(int s, const double* w, double* norm, double* radius);
+int ref_sym_eigvals(int s, const double* w, double* out);
+
 #define OC_DECLARE(P)                                                                  \
   int P##poisson27_fill(int64_t nx, int64_t ny, int64_t nz, int64_t* rowptr,           \
                         int64_t* col, double* val);                                   \

@@ -403,6 +403,23 @@ int ref_csr_validate(int64_t n, const int64_t* rp, const int64_t* ci, const doub
   });
 }
 
+int ref_fgs_rate_normalized(int s, const double* w, double* norm, double* radius) {
+  return guarded([&] {
+    cs::SmallDense m(s, s);
+    std::memcpy(m.data.data(), w, sizeof(double) * s * s);
+    const cs::FgsRate r = cs::fgs_rate(cs::normalize_gram(cs::gram_from_matrix(m)));
+    *norm = r.spectral_norm;
+    *radius = r.spectral_radius;
+  });
+}
+
+int ref_sym_eigvals(int s, const double* w, double* out) {
+  return guarded([&] {
+    const auto e = cs::lapack::sym_eigvals(s, std::vector<double>(w, w + s * s));
+    std::memcpy(out, e.data(), sizeof(double) * s);
+  });
+}
+
 const char* ref_last_error(int* payload) {
   if (payload) *payload = g_payload;
   return g_msg.c_str();

@@ -90,6 +90,8 @@ SIGNATURES = {
     "cs_problem_upload_csr_block": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp,
                                               C.POINTER(_vp)]),
     "cs_problem_read_mm": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
+    "cs_fgs_rate": (C.c_int, [C.c_int, _vp, _dp, _dp]),
+    "cs_kappa_sym": (C.c_int, [C.c_int, _vp, _dp]),
     "cs_mm_read": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_vp), C.POINTER(C.c_int64),
                              C.POINTER(C.c_int64)]),
     "cs_csr_host_rows": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp, _vp, _vp]),

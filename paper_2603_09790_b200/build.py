@@ -26,6 +26,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "lib", "libchebstep_gpu.so")
+CLI_SRC = os.path.join(PKG, "cli", "main.cpp")
+CLI_BIN = os.path.join(PKG, "bin", "chebstep")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 _NCCL = sorted(glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia",
@@ -104,6 +106,15 @@ def build(force: bool = False, jobs: int = 8, verbose: bool = True) -> str:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         if verbose:
             print(f"built {LIB}")
+    if not EXTRA and (force or _stale(CLI_BIN, [LIB, CLI_SRC])):
+        os.makedirs(os.path.dirname(CLI_BIN), exist_ok=True)
+        cmd = [CXX, *CXXFLAGS, CLI_SRC, "-o", CLI_BIN, "-L" + os.path.dirname(LIB),
+               "-lchebstep_gpu", "-Wl,-rpath,$ORIGIN/../lib"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print(f"built {CLI_BIN}")
     return LIB
 
 

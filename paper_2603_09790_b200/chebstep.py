@@ -871,8 +871,48 @@ def assemble_gram(q, aq, mode: str = "reference", ctx: Optional[Context] = None)
 
 
 def gram_from_matrix(w) -> GramSystem:
+    """gram.cpp:51-58: square, exactly symmetric, positive finite diagonal."""
     w = np.asarray(w, np.float64)
-    return GramSystem(w.copy(), np.diag(w).copy())
+    if w.ndim != 2 or w.shape[0] != w.shape[1]:
+        raise DimensionError("gram_from_matrix: not square")
+    if not np.array_equal(w, w.T):
+        raise InvalidMatrixError("gram_from_matrix: matrix not symmetric")
+    d = np.diag(w).copy()
+    if not np.all(np.isfinite(d) & (d > 0.0)):
+        raise NotSpdError("gram: non-positive diagonal (basis degeneracy)")
+    return GramSystem(w.copy(), d)
+
+
+def normalize_gram(g: GramSystem) -> GramSystem:
+    """gram.cpp:60-76: D^-1/2 W D^-1/2 with an exact unit diagonal."""
+    inv = 1.0 / np.sqrt(g.diag)
+    w = (g.w * inv[:, None]) * inv[None, :]
+    np.fill_diagonal(w, 1.0)
+    return GramSystem(w, np.ones(g.order()), True)
+
+
+@dataclass
+class FgsRate:
+    spectral_norm: float
+    spectral_radius: float
+
+
+def fgs_rate(g: GramSystem) -> FgsRate:
+    """gram.cpp:148-174 (host eigensolvers instead of dgesvd/dgeev)."""
+    if not g.normalized:
+        raise InvalidArgumentError("fgs_rate: system must be normalized")
+    w = np.asfortranarray(g.w, np.float64)
+    nrm, rad = C.c_double(), C.c_double()
+    _check(lib.cs_fgs_rate(g.order(), w.ctypes.data, C.byref(nrm), C.byref(rad)))
+    return FgsRate(nrm.value, rad.value)
+
+
+def kappa_sym(w) -> float:
+    """kappa_2 of a symmetric matrix as solver.cpp:69-74 computes it."""
+    w = np.asfortranarray(w, np.float64)
+    k = C.c_double()
+    _check(lib.cs_kappa_sym(w.shape[0], w.ctypes.data, C.byref(k)))
+    return k.value
 
 
 @dataclass

@@ -458,6 +458,28 @@ GramSystem gram_from_matrix(const SmallDense& w) {
   return finish(w);
 }
 
+GramSystem normalize_gram(const GramSystem& g) {  // gram.cpp:60-76
+  const int s = g.order();
+  SmallDense wc(s, s);
+  std::vector<double> inv_sqrt(static_cast<size_t>(s));
+  for (int i = 0; i < s; ++i) inv_sqrt[i] = 1.0 / std::sqrt(g.diag[i]);
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < s; ++i)
+      wc.at(i, j) = (i == j) ? 1.0 : g.w.at(i, j) * inv_sqrt[i] * inv_sqrt[j];
+  GramSystem out;
+  out.w = std::move(wc);
+  out.diag.assign(static_cast<size_t>(s), 1.0);
+  out.normalized = true;
+  return out;
+}
+
+FgsRate fgs_rate(const GramSystem& g) {
+  if (!g.normalized) throw InvalidArgumentError("fgs_rate: system must be normalized");
+  FgsRate r{0.0, 0.0};
+  check(cs_fgs_rate(g.order(), g.w.data.data(), &r.spectral_norm, &r.spectral_radius));
+  return r;
+}
+
 FgsResult fgs_solve(const GramSystem& g, const SmallDense& rhs, const FgsConfig& cfg) {
   if (cfg.nu < 1) throw InvalidArgumentError("fgs: nu must be >= 1");
   if (rhs.rows != g.order()) throw DimensionError("fgs: rhs rows mismatch");
@@ -537,11 +559,9 @@ struct HookBufs {
 };
 }  // namespace
 
-SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
-                        const Preconditioner& m, const SolverConfig& cfg) {
+namespace {
+cs_config to_cs(const SolverConfig& cfg, index_t n) {
   cfg.validate();
-  if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
-    throw DimensionError("pcg_s_solve: vector length mismatch");
   cs_config c;
   cs_config_default(&c);
   c.s = cfg.s;
@@ -561,15 +581,19 @@ SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span
   c.track_true_residual = cfg.track_true_residual;
   c.collect_iterates = cfg.collect_iterates;
   if (cfg.error_reference) {
-    if (static_cast<index_t>(cfg.error_reference->size()) != a.n)
+    if (static_cast<index_t>(cfg.error_reference->size()) != n)
       throw DimensionError("pcg_s_solve: error_reference length mismatch");
     c.error_reference = cfg.error_reference->data();
   }
-  const std::string_view nm = m.name();
-  const int kind = nm == "jacobi" ? CS_PRECOND_JACOBI : nm == "identity" ? CS_PRECOND_IDENTITY : -1;
-  if (kind < 0) throw InvalidArgumentError("preconditioner has no device implementation");
+  return c;
+}
+
+// one s-step solve through `call` (fills cs_report), histories + hooks unpacked
+template <class Call>
+SolveResult run_pcgs(const SolverConfig& cfg, index_t n, Call&& call) {
+  cs_config c = to_cs(cfg, n);
   SolveResult out;
-  out.x.resize(static_cast<std::size_t>(a.n));
+  out.x.resize(static_cast<std::size_t>(n));
   const int cap = cfg.max_outer + 2;
   std::vector<double> rel(cap), da(cap), db(cap);
   cs_report r{};
@@ -578,12 +602,11 @@ SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span
   r.delta_alpha = da.data();
   r.delta_beta = db.data();
   HookBufs hb;
-  hb.attach(r, cap, cfg.s, a.n, cfg.collect_gram, cfg.track_true_residual,
+  hb.attach(r, cap, cfg.s, n, cfg.collect_gram, cfg.track_true_residual,
             cfg.error_reference.has_value(), cfg.collect_iterates);
-  check(cs_pcg_s_solve_csr(ctx(), a.n, a.row_offsets.data(), a.col_indices.data(),
-                           a.values.data(), kind, b.data(), x0.data(), &c, out.x.data(), &r));
+  check(call(&c, out.x.data(), &r));
   fill(out.report, r, rel, da, db);
-  hb.fill(out.report, r, cfg.s, a.n);
+  hb.fill(out.report, r, cfg.s, n);
   if (cfg.spectrum) out.report.spectrum_used = *cfg.spectrum;
   else if (r.lambda_max > 0.0) {
     out.report.spectrum_used.low_factor = 0.9;
@@ -592,12 +615,9 @@ SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span
   return out;
 }
 
-SolveResult pcg_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
-                      const Preconditioner& m, const PcgConfig& cfg) {
+template <class Call>
+SolveResult run_pcg(const PcgConfig& cfg, index_t n, Call&& call) {
   if (!(cfg.tol >= 0.0) || cfg.max_iter < 1) throw InvalidArgumentError("pcg_solve: bad tol/max_iter");
-  if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
-    throw DimensionError("pcg_solve: vector length mismatch");
-  Problem p(a, &m);
   cs_config c;
   cs_config_default(&c);
   c.tol = cfg.tol;
@@ -606,20 +626,121 @@ SolveResult pcg_solve(const CsrMatrix& a, std::span<const double> b, std::span<c
   c.collect_iterates = cfg.collect_iterates;
   if (cfg.error_reference) c.error_reference = cfg.error_reference->data();
   SolveResult out;
-  out.x.resize(static_cast<std::size_t>(a.n));
+  out.x.resize(static_cast<std::size_t>(n));
   const int cap = cfg.max_iter + 2;
   std::vector<double> rel(cap);
   cs_report r{};
   r.cap = cap;
   r.rel_residual = rel.data();
   HookBufs hb;
-  hb.attach(r, cap, 1, a.n, false, false, cfg.error_reference.has_value(), cfg.collect_iterates);
-  check(cs_pcg_solve_cfg(p.p, b.data(), x0.data(), &c, out.x.data(), &r));
+  hb.attach(r, cap, 1, n, false, false, cfg.error_reference.has_value(), cfg.collect_iterates);
+  check(call(&c, out.x.data(), &r));
   fill(out.report, r, rel, {}, {});
-  hb.fill(out.report, r, 1, a.n);
+  hb.fill(out.report, r, 1, n);
   out.report.spectrum_used = SpectrumEstimate{};
   return out;
 }
+
+int precond_kind(const Preconditioner& m) {
+  const std::string_view nm = m.name();
+  const int kind = nm == "jacobi" ? CS_PRECOND_JACOBI : nm == "identity" ? CS_PRECOND_IDENTITY : -1;
+  if (kind < 0) throw InvalidArgumentError("preconditioner has no device implementation");
+  return kind;
+}
+}  // namespace
+
+SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
+                        const Preconditioner& m, const SolverConfig& cfg) {
+  cfg.validate();
+  if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
+    throw DimensionError("pcg_s_solve: vector length mismatch");
+  const int kind = precond_kind(m);
+  return run_pcgs(cfg, a.n, [&](const cs_config* c, double* x, cs_report* r) {
+    return cs_pcg_s_solve_csr(ctx(), a.n, a.row_offsets.data(), a.col_indices.data(),
+                              a.values.data(), kind, b.data(), x0.data(), c, x, r);
+  });
+}
+
+SolveResult pcg_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
+                      const Preconditioner& m, const PcgConfig& cfg) {
+  if (!(cfg.tol >= 0.0) || cfg.max_iter < 1) throw InvalidArgumentError("pcg_solve: bad tol/max_iter");
+  if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
+    throw DimensionError("pcg_solve: vector length mismatch");
+  Problem p(a, &m);
+  return run_pcg(cfg, a.n, [&](const cs_config* c, double* x, cs_report* r) {
+    return cs_pcg_solve_cfg(p.p, b.data(), x0.data(), c, x, r);
+  });
+}
+
+// ------------------------------------------------------------------ device-resident problems
+namespace gpu {
+
+DeviceProblem::DeviceProblem(cs_problem* p) : p_(p) {
+  int64_t info[6];
+  check(cs_problem_info(p_, info));
+  n_global_ = info[0], n_local_ = info[1], nnz_local_ = info[2], row_begin_ = info[3];
+}
+DeviceProblem::~DeviceProblem() {
+  if (p_) cs_problem_destroy(p_);
+}
+DeviceProblem::DeviceProblem(DeviceProblem&& o) noexcept { *this = std::move(o); }
+DeviceProblem& DeviceProblem::operator=(DeviceProblem&& o) noexcept {
+  if (this != &o) {
+    if (p_) cs_problem_destroy(p_);
+    p_ = o.p_;
+    n_global_ = o.n_global_, n_local_ = o.n_local_, nnz_local_ = o.nnz_local_;
+    row_begin_ = o.row_begin_;
+    o.p_ = nullptr;
+  }
+  return *this;
+}
+
+DeviceProblem DeviceProblem::poisson27(const PoissonSpec& spec) {
+  cs_problem* p = nullptr;
+  check(cs_problem_generate(ctx(), CS_GEN_POISSON27, spec.nx, spec.ny, spec.nz, nullptr, &p));
+  return DeviceProblem(p);
+}
+DeviceProblem DeviceProblem::stencil7(const PoissonSpec& spec, double cx, double cy, double cz) {
+  const double coef[3] = {cx, cy, cz};
+  cs_problem* p = nullptr;
+  check(cs_problem_generate(ctx(), CS_GEN_STENCIL7, spec.nx, spec.ny, spec.nz, coef, &p));
+  return DeviceProblem(p);
+}
+DeviceProblem DeviceProblem::from_csr(const CsrMatrix& a) {
+  cs_problem* p = nullptr;
+  check(cs_problem_upload_csr(ctx(), a.n, a.row_offsets.data(), a.col_indices.data(),
+                              a.values.data(), &p));
+  return DeviceProblem(p);
+}
+DeviceProblem DeviceProblem::read_matrix_market(const std::string& path, bool require_spd) {
+  cs_problem* p = nullptr;
+  check(cs_problem_read_mm(ctx(), path.c_str(), require_spd ? 1 : 0, &p));
+  return DeviceProblem(p);
+}
+void DeviceProblem::set_precond(const Preconditioner& m) {
+  check(cs_problem_set_precond(p_, precond_kind(m)));
+}
+
+SolveResult pcg_s_solve(const DeviceProblem& p, std::span<const double> b,
+                        std::span<const double> x0, const SolverConfig& cfg) {
+  cfg.validate();
+  if (static_cast<index_t>(b.size()) != p.n_local() || static_cast<index_t>(x0.size()) != p.n_local())
+    throw DimensionError("pcg_s_solve: vector length mismatch");
+  return run_pcgs(cfg, p.n_local(), [&](const cs_config* c, double* x, cs_report* r) {
+    return cs_pcg_s_solve(p.handle(), b.data(), x0.data(), c, x, r);
+  });
+}
+
+SolveResult pcg_solve(const DeviceProblem& p, std::span<const double> b,
+                      std::span<const double> x0, const PcgConfig& cfg) {
+  if (static_cast<index_t>(b.size()) != p.n_local() || static_cast<index_t>(x0.size()) != p.n_local())
+    throw DimensionError("pcg_solve: vector length mismatch");
+  return run_pcg(cfg, p.n_local(), [&](const cs_config* c, double* x, cs_report* r) {
+    return cs_pcg_solve_cfg(p.handle(), b.data(), x0.data(), c, x, r);
+  });
+}
+
+}  // namespace gpu
 
 SolveResult pcg_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
                       const Preconditioner& m, double tol, int max_iter) {

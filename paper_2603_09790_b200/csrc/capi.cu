@@ -7,8 +7,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <limits>
+#include <algorithm>
+#include <cmath>
 #include <string>
 
+#include "lanczos.cuh"
 #include "mmio.hpp"
 #include "runtime.cuh"
 
@@ -208,6 +212,46 @@ int cs_problem_upload_csr_block(cs_ctx* ctx, int64_t n_global, int64_t row_begin
   return guard([&] {
     need(rowptr_local, "rowptr");
     *out = problem_upload_block(ctx, n_global, row_begin, row_end, rowptr_local, col_global, val);
+  });
+}
+
+int cs_fgs_rate(int s, const double* w, double* spectral_norm, double* spectral_radius) {
+  return guard([&] {
+    need(w, "w");
+    if (s < 1 || s > kMaxS) fail(CS_ERR_INVALID_ARGUMENT, 0, "fgs_rate: bad order");
+    const size_t ss = static_cast<size_t>(s);
+    auto W = [&](int i, int j) { return w[i + j * ss]; };
+    // X solves (I + L) X = I column by column (gram.cpp:153-162)
+    std::vector<double> x(ss * ss, 0.0), it(ss * ss, 0.0);
+    for (int c = 0; c < s; ++c) {
+      x[c + c * ss] = 1.0;
+      for (int i = 0; i < s; ++i) {
+        double acc = x[i + c * ss];
+        for (int j = 0; j < i; ++j) acc -= W(i, j) * x[j + c * ss];
+        x[i + c * ss] = acc;
+      }
+    }
+    for (int c = 0; c < s; ++c)  // iteration matrix L^T X (gram.cpp:163-169)
+      for (int i = 0; i < s; ++i) {
+        double acc = 0.0;
+        for (int j = i + 1; j < s; ++j) acc += W(j, i) * x[j + c * ss];
+        it[i + c * ss] = acc;
+      }
+    *spectral_norm = max_singular_value(s, it.data());
+    std::vector<double> mods(ss);
+    general_eig_moduli(s, it.data(), mods.data());
+    *spectral_radius = *std::max_element(mods.begin(), mods.end());
+  });
+}
+
+int cs_kappa_sym(int s, const double* w, double* kappa) {
+  return guard([&] {
+    need(w, "w");
+    if (s < 1 || s > kMaxS) fail(CS_ERR_INVALID_ARGUMENT, 0, "kappa: bad order");
+    std::vector<double> ev(static_cast<size_t>(s));
+    sym_eigenvalues(s, w, ev.data());
+    // solver.cpp:69-74: largest / smallest eigenvalue, inf unless the smallest is > 0
+    *kappa = ev[0] > 0.0 ? ev[s - 1] / ev[0] : std::numeric_limits<double>::infinity();
   });
 }
 

@@ -30,5 +30,8 @@ void lz_scalar(int which, int j, int steps, LanczosScalars* sc, DevState* st, cu
 void tridiag_eigenvalues(int m, const double* d, const double* e, double* out);
 // host: eigenvalues of a small dense symmetric matrix (column-major s x s), ascending
 void sym_eigenvalues(int s, const double* w, double* out);
+// host: largest singular value / eigenvalue moduli of a general s x s matrix
+double max_singular_value(int s, const double* m);
+void general_eig_moduli(int n, const double* m, double* out);
 
 }  // namespace csg

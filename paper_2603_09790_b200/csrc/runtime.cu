@@ -135,8 +135,8 @@ void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand) {
   CS_CUDA(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
   {
     Launch L(c, CS_PHASE_SPMV);
-    launch_spmv(kind, A, g, 0, p->slice_int_begin, c->stream);
-    launch_spmv(kind, A, g, p->slice_int_end, p->nslices, c->stream);
+    // both boundary ranges [ie, nslices) and [0, ib) in one wrapped launch
+    launch_spmv(kind, A, g, p->slice_int_end, p->nslices + p->slice_int_begin, c->stream);
   }
 }
 

@@ -75,9 +75,66 @@ __device__ void fgs_columns_reg(const double* W, int k, const double* rhs, int n
   }
 }
 
+// Fast-mode FGS (same sweep order, reassociated arithmetic): reciprocal of
+// the diagonal instead of a division, and each row's sum is started at the
+// sweep's beginning from the not-yet-updated x_j (j > i) and finished by one
+// FMA per freshly updated x_j -- the dependent chain per row is one FMA plus
+// one multiply instead of s-1 sub/mul pairs and a division.
+template <int S>
+__device__ void fgs_fast_reg(const double* W, int k, const double* rhs, int nu, double* x) {
+  for (int col = threadIdx.x; col < k; col += blockDim.x) {
+    double w[S][S], inv[S], b[S], xc[S], acc[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      b[i] = rhs[i + col * S];
+      xc[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) w[i][j] = W[i + j * S];
+      inv[i] = 1.0 / w[i][i];
+    }
+    for (int sweep = 0; sweep < nu; ++sweep) {
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        acc[i] = b[i];
+#pragma unroll
+        for (int j = i + 1; j < S; ++j) acc[i] = fma(-w[i][j], xc[j], acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        xc[i] = acc[i] * inv[i];
+#pragma unroll
+        for (int r = i + 1; r < S; ++r) acc[r] = fma(-w[r][i], xc[i], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) x[i + col * S] = xc[i];
+  }
+}
+
+__device__ void fgs_fast_generic(int s, const double* W, int k, const double* rhs, int nu,
+                                 double* x) {
+  for (int col = threadIdx.x; col < k; col += blockDim.x) {
+    const double* b = rhs + col * s;
+    double* xc = x + col * s;
+    for (int sweep = 0; sweep < nu; ++sweep)
+      for (int i = 0; i < s; ++i) {
+        double a0 = b[i], a1 = 0.0;
+        int j = 0;
+        for (; j + 1 < s; j += 2) {
+          if (j != i) a0 = fma(-W[i + j * s], xc[j], a0);
+          if (j + 1 != i) a1 = fma(-W[i + (j + 1) * s], xc[j + 1], a1);
+        }
+        if (j < s && j != i) a0 = fma(-W[i + j * s], xc[j], a0);
+        xc[i] = (a0 + a1) / W[i + i * s];
+      }
+  }
+}
+
 // gram.cpp:78-119. Returns 0 or the NotSpd sub-code. x, tmp: s*k.
+// fast = reassociated sweeps (fast algebra only); otherwise the reference's
+// exact operation sequence.
 __device__ int fgs_dev(int s, const double* W, int k, const double* rhs, int nu, double* x,
-                       double* delta, double* tmp) {
+                       double* delta, double* tmp, bool fast = false) {
   for (int i = 0; i < s; ++i)
     if (!(W[i + i * s] > 0.0)) return kSubFgs;
   __shared__ double rn_sh;
@@ -87,6 +144,20 @@ __device__ int fgs_dev(int s, const double* W, int k, const double* rhs, int nu,
   const double rn = rn_sh;
   if (rn == 0.0) {
     *delta = 0.0;
+    return 0;
+  }
+  if (fast) {
+    switch (s) {
+      case 2: fgs_fast_reg<2>(W, k, rhs, nu, x); break;
+      case 3: fgs_fast_reg<3>(W, k, rhs, nu, x); break;
+      case 4: fgs_fast_reg<4>(W, k, rhs, nu, x); break;
+      case 5: fgs_fast_reg<5>(W, k, rhs, nu, x); break;
+      case 6: fgs_fast_reg<6>(W, k, rhs, nu, x); break;
+      case 8: fgs_fast_reg<8>(W, k, rhs, nu, x); break;
+      default: fgs_fast_generic(s, W, k, rhs, nu, x);
+    }
+    __syncthreads();
+    *delta = gram_residual(s, W, k, rhs, x, rn, tmp);
     return 0;
   }
   switch (s) {  // register-resident sweeps for small orders, same operation sequence
@@ -162,8 +233,8 @@ __device__ int chol_dev(int s, const double* W, int k, const double* rhs, double
 }
 
 __device__ int solve_dev(const SmallArgs& a, const double* W, int k, const double* rhs, double* x,
-                         double* delta, double* scratch) {
-  if (a.gram == 0) return fgs_dev(a.s, W, k, rhs, a.nu, x, delta, scratch);
+                         double* delta, double* scratch, bool fast = false) {
+  if (a.gram == 0) return fgs_dev(a.s, W, k, rhs, a.nu, x, delta, scratch, fast);
   return chol_dev(a.s, W, k, rhs, x, delta, scratch, scratch + a.s * a.s);
 }
 
@@ -227,7 +298,7 @@ __global__ void fast_setup_kernel(SmallArgs a) {
     return;
   }
   double delta;
-  const int bad = solve_dev(a, m.W, 1, m.rhs, m.x, &delta, m.scr);
+  const int bad = solve_dev(a, m.W, 1, m.rhs, m.x, &delta, m.scr, true);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, 1);
     return;
@@ -279,7 +350,7 @@ __global__ void fast_step_kernel(SmallArgs a) {
   __syncthreads();
   if (stop) return;
   double delta;
-  int bad = solve_dev(a, m.W, s, m.rhs, m.x, &delta, m.scr);
+  int bad = solve_dev(a, m.W, s, m.rhs, m.x, &delta, m.scr, true);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, k);
     return;
@@ -320,7 +391,7 @@ __global__ void fast_step_kernel(SmallArgs a) {
     if (threadIdx.x == 0) raise(st, 5, kSubAssembly, k + 1);
     return;
   }
-  bad = solve_dev(a, m.Wn, 1, m.rhs, m.x, &delta, m.scr);
+  bad = solve_dev(a, m.Wn, 1, m.rhs, m.x, &delta, m.scr, true);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, k + 1);
     return;

@@ -188,12 +188,16 @@ __global__ void __launch_bounds__(kWarps * 32, CS_SPMV_MINB)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  // virtual slice indices past nslices wrap to the start, so [ie, nslices + ib)
+  // covers both boundary ranges of a halo'd SpMV in one launch
+  const auto phys = [&](int64_t v) { return v >= a.nslices ? v - a.nslices : v; };
   int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   double dotv = 0.0;
-  SliceMeta sm = load_meta(a, slice, slice_end);
+  SliceMeta sm = load_meta(a, phys(slice), slice < slice_end ? a.nslices : 0);
   for (; slice < slice_end; slice += wstride) {
-    const SliceMeta next = load_meta(a, slice + wstride, slice_end);
-    const int64_t row = slice * kSliceRows + lane;
+    const int64_t vn = slice + wstride;
+    const SliceMeta next = load_meta(a, phys(vn), vn < slice_end ? a.nslices : 0);
+    const int64_t row = phys(slice) * kSliceRows + lane;
     const bool own = row < a.n_local;
     EpiOps e;
     if (own) e = epi_load<KIND, JAC>(a, g, row);
@@ -390,6 +394,11 @@ int spmv_dot_blocks(int64_t nslices) {
 void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,
                  cudaStream_t st) {
   if (se <= sb) return;
+  if (se > a.nslices && use_tma(a)) {  // the TMA tiles need contiguous slices
+    launch_spmv(kind, a, g, sb, a.nslices, st);
+    launch_spmv(kind, a, g, a.nslices, se, st);
+    return;
+  }
   const bool jac = a.inv_diag != nullptr;
   switch (kind) {
     case kPlain: launch_kind<kPlain>(false, a, g, sb, se, st); break;

@@ -144,11 +144,11 @@ def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=Tr
     b_spmv = mat_bytes + 2 * v                       # y = A x
     b_resid = mat_bytes + 3 * v                      # r = b - A x
     b_dot = mat_bytes + 2 * v                        # Lanczos t = A v (+ v.t)
+    j = v if jacobi else 0                           # D^-1 read by the epilogue
     if mode == "fast":                               # z_q = 2a D^-1 p_q - 2s z_{q-1} - z_{q-2}
-        b_first = mat_bytes + 3 * v                  # x, p, z
-        b_mid = mat_bytes + 4 * v                    # x, p, z_{q-2}, z
+        b_first = mat_bytes + 3 * v + j              # x, p, z (+ D^-1)
+        b_mid = mat_bytes + 4 * v + j                # x, p, z_{q-2}, z (+ D^-1)
     else:                                            # reference zp recurrence (+ D^-1 vector)
-        j = v if jacobi else 0
         b_first = mat_bytes + 2 * v + v + j + (v if jacobi else 0) + v
         b_mid = mat_bytes + 2 * v + 2 * v + j + (v if jacobi else 0) + v
     b_last = b_spmv
@@ -161,7 +161,7 @@ def outer_bytes_format(mat_bytes, n, s):
     """Per-outer algorithmic bytes of the fast schedule in the stored format:
     s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+5)."""
     v = 8 * n
-    mpk = (mat_bytes + 3 * v) + (s - 2) * (mat_bytes + 4 * v) + (mat_bytes + 2 * v) if s > 1 \
+    mpk = (mat_bytes + 4 * v) + (s - 2) * (mat_bytes + 5 * v) + (mat_bytes + 2 * v) if s > 1 \
         else mat_bytes + 2 * v
     return mpk + v * (3 * s + 1) + v * (6 * s + 5)
 
@@ -374,7 +374,13 @@ def run_ours(args):
                        "allreduces_per_solve": rep.device_allreduces,
                        "l2": "inputs > L2 (matrix %.1f GB/GPU vs 126 MB L2); no flush" %
                              (prob.device_bytes / 1e9),
-                       "parallelism": f"z-slab row partition x{world}"},
+                       "parallelism": f"z-slab row partition x{world}",
+                       "halo": prob.halo_mode,
+                       "matrix_format": {"slices": prob.slices,
+                                         "pattern_slices": prob.pattern_slices,
+                                         "uniform_value_slices": prob.uniform_slices,
+                                         "table_entries": prob.pattern_entries,
+                                         "bytes": prob.device_bytes}},
             "gpu_launches": launches,
             "roofline": roof,
             "solve_roofline": solve_level,

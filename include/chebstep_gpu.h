@@ -224,12 +224,17 @@ int cs_problem_upload_csr_block(cs_ctx* ctx, int64_t n_global, int64_t row_begin
  * its cs_partition_rows(n, 1, nranks, rank) block and uploads it (collective). */
 int cs_problem_read_mm(cs_ctx* ctx, const char* path, int require_spd, cs_problem** out);
 int cs_problem_destroy(cs_problem* p);
-/* n_global, n_local, nnz_local, row_begin, n_ghost, device bytes of the SELL arrays */
-int cs_problem_info(cs_problem* p, int64_t* info6);
+/* info10: n_global, n_local, nnz_local, row_begin, n_ghost, device bytes of the
+ * SELL arrays, slices, pattern-compressed slices, uniform-value slices, pattern
+ * table entries (format) */
+int cs_problem_info(cs_problem* p, int64_t* info10);
 /* Local rows back as CSR with GLOBAL column indices (bit-exact assembly check). */
 int cs_problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val);
 /* Ghost global column list of this rank (n_ghost entries). */
 int cs_problem_ghosts(cs_problem* p, int64_t* ghost_cols);
+/* Halo transport of the last solve on this problem: 0 none (single rank),
+ * 1 NCCL send/recv, 2 NVLink peer-memory stores from the producing kernels. */
+int cs_problem_halo_mode(cs_problem* p, int* mode);
 int cs_problem_set_precond(cs_problem* p, int kind);
 int cs_problem_inv_diag(cs_problem* p, double* out);
 

@@ -100,6 +100,7 @@ SIGNATURES = {
     "cs_csr_validate": (C.c_int, [C.c_int64, _vp, _vp, _vp, C.c_int]),
     "cs_problem_destroy": (C.c_int, [_vp]),
     "cs_problem_info": (C.c_int, [_vp, _i64p]),
+    "cs_problem_halo_mode": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "cs_problem_download_csr": (C.c_int, [_vp, _i64p, _i64p, _f64p]),
     "cs_problem_ghosts": (C.c_int, [_vp, _i64p]),
     "cs_problem_set_precond": (C.c_int, [_vp, C.c_int]),

@@ -246,11 +246,19 @@ class DeviceProblem:
 
     def __init__(self, ctx: Context, handle):
         self.ctx, self.handle = ctx, handle
-        info = np.zeros(6, np.int64)
+        info = np.zeros(10, np.int64)
         _check(lib.cs_problem_info(handle, info))
         (self.n_global, self.n_local, self.nnz_local, self.row_begin, self.n_ghost,
-         self.device_bytes) = (int(v) for v in info)
+         self.device_bytes, self.slices, self.pattern_slices, self.uniform_slices,
+         self.pattern_entries) = (int(v) for v in info)
         self.precond = "identity"
+
+    @property
+    def halo_mode(self) -> str:
+        """Halo transport of the last solve: "none", "nccl" or "nvlink-p2p"."""
+        m = C.c_int(0)
+        _check(lib.cs_problem_halo_mode(self.handle, C.byref(m)))
+        return ("none", "nccl", "nvlink-p2p")[m.value]
 
     @classmethod
     def generate(cls, kind: str, nx: int, ny: int, nz: int, coef=(1.0, 1.0, 1.0),

@@ -323,6 +323,7 @@ int cs_problem_destroy(cs_problem* p) {
     if (p) {
       cudaSetDevice(p->ctx->device);
       cudaStreamSynchronize(p->ctx->stream);
+      p2p_teardown(p);
       delete p;
     }
   });
@@ -335,9 +336,17 @@ int cs_problem_info(cs_problem* p, int64_t* info) {
     info[2] = p->nnz_local;
     info[3] = p->row_begin;
     info[4] = p->n_ghost;
-    info[5] = static_cast<int64_t>(p->vals.bytes + p->cols.bytes + p->pat.bytes + p->meta.bytes +
-                                   p->slice_ptr.bytes);
+    info[5] = static_cast<int64_t>(p->vals.bytes + p->cols.bytes + p->pat.bytes + p->pval.bytes +
+                                   p->meta.bytes + p->slice_ptr.bytes);
+    info[6] = p->nslices;
+    info[7] = p->compressed_slices;
+    info[8] = p->uniform_slices;
+    info[9] = p->pattern_entries;
   });
+}
+
+int cs_problem_halo_mode(cs_problem* p, int* mode) {
+  return guard([&] { *mode = p->ctx->nranks == 1 ? 0 : p->p2p ? 2 : 1; });
 }
 
 int cs_problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val) {

@@ -1,7 +1,7 @@
 // common.cuh -- shared device/host definitions of libchebstep_gpu (sm_100a).
 //
 // Data layout in HBM:
-//  * Matrix: SELL-32. Rows are grouped in slices of 32 consecutive rows; a
+//  * Matrix: SELL-32 (compressed to SELL-32P / SELL-32PU, see SellView). Rows are grouped in slices of 32 consecutive rows; a
 //    slice stores its nonzeros column-major by slot (slot k of lane l at
 //    vals[slice_ptr[s] + k*32 + l]), padded to the slice's widest row with
 //    val = 0, col = -1. Columns are int32 local indices (owned rows
@@ -42,8 +42,28 @@ struct DevState {
 // int32 columns at cols[meta[s] + 32k + lane]. meta[s] < 0: the slice's rows share
 // one sorted relative-offset pattern -- slot k of lane l is column row_l + off_k
 // if bit l of mask_k is set (else an empty slot), with {off_k, mask_k} at
-// pat[-meta[s]-1 + k]. Either way a row's entries are visited in its stored
+// pat[pat_index(meta) + k]. Either way a row's entries are visited in its stored
 // (ascending) column order, so sums are bitwise the CSR row-serial sums.
+// Uniform-value slices (pat_uniform(meta) = U > 0, "SELL-32PU"): every row of the
+// slice that has an entry at offset off_k stores the same FP64 value (bitwise),
+// so the slice keeps NO value slots: its U slots carry {off_k, mask_k} in pat and
+// the value in pval[pat_index(meta) + k]. Slices with an identical (pattern,
+// values) table share one table (global dedupe; the tables come first in
+// pat/pval), so a constant-coefficient stencil streams no matrix bytes beyond
+// meta: a 27-point operator has at most 27 distinct tables, staged once per
+// block in shared memory. Lossless: every product v * x[c] uses the stored v,
+// the result is bitwise unchanged.
+constexpr int kPatShift = 40;
+constexpr int64_t kPatIdxMask = (int64_t{1} << kPatShift) - 1;
+constexpr int kUniformMaxSlots = 1 << 20;
+__host__ __device__ inline int64_t pat_index(int64_t meta) { return (-meta - 1) & kPatIdxMask; }
+__host__ __device__ inline int pat_uniform(int64_t meta) {
+  return static_cast<int>((-meta - 1) >> kPatShift);
+}
+__host__ __device__ inline int64_t make_pat_meta(int64_t idx, int uniform_slots) {
+  return -((static_cast<int64_t>(uniform_slots) << kPatShift) | idx) - 1;
+}
+
 struct SellView {
   int64_t n_local;
   int64_t nslices;
@@ -52,8 +72,12 @@ struct SellView {
   const int32_t* __restrict__ cols;
   const int64_t* __restrict__ meta;
   const int2* __restrict__ pat;
+  const double* __restrict__ pval;      // uniform-slice values (parallel to pat)
   const double* __restrict__ inv_diag;  // nullptr for identity
-  int max_width;                        // widest slice (slots)
+  int max_width;                        // widest slice (value slots)
+  int uniform;                          // nonzero: some slices are uniform-value
+  int uniform_all;                      // nonzero: every slice is uniform-value
+  int64_t table_entries;                // uniform tables occupy pat/pval[0, table_entries)
 };
 
 __host__ __device__ inline unsigned long long make_err(int code, int payload) {

@@ -1,6 +1,7 @@
 // runtime.cu -- device context, device-resident problems, halo exchange,
 // collectives and launch/timing accounting.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "runtime.cuh"
@@ -147,6 +148,151 @@ void allreduce_sum(cs_ctx* c, double* dev, size_t count) {
   CS_NCCL(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, c->comm, c->stream));
 }
 
+// ------------------------------------------------------------------ NVLink peer-memory halo
+
+namespace {
+struct PeerInfo {
+  cudaIpcMemHandle_t ws, sig;
+  uint64_t gen;
+  int64_t z_off, ld, n_local, ghost_lo;
+  unsigned char uuid[16];
+  int32_t ok, pad;
+};
+
+void fill_push(const cs_problem* p, SpmvArgs& g, int col) {
+  if (p->ghost_lo > 0) {  // my first plane -> rank-1's upper ghost plane
+    const cs_problem::PeerMap& m = p->peer[0];
+    g.push_lo = static_cast<double*>(m.ws) + m.ghost_off + static_cast<int64_t>(col) * m.ld;
+    g.send_lo = p->send_lo;
+    g.sig_lo = static_cast<unsigned long long*>(m.sig) + 1;  // its "from upper" counter
+  }
+  if (p->ghost_hi > 0) {  // my last plane -> rank+1's lower ghost plane
+    const cs_problem::PeerMap& m = p->peer[1];
+    g.push_hi = static_cast<double*>(m.ws) + m.ghost_off + static_cast<int64_t>(col) * m.ld;
+    g.hi_begin = p->n_local - p->send_hi;
+    g.sig_hi = static_cast<unsigned long long*>(m.sig) + 0;  // its "from lower" counter
+  }
+}
+}  // namespace
+
+void p2p_teardown(cs_problem* p) {
+  for (auto& m : p->peer) {
+    if (m.ws) cudaIpcCloseMemHandle(m.ws);
+    if (m.sig) cudaIpcCloseMemHandle(m.sig);
+    m = cs_problem::PeerMap{};
+  }
+  cudaGetLastError();
+  p->p2p = false;
+}
+
+bool p2p_setup(cs_problem* p, double* Z) {
+  cs_ctx* c = p->ctx;
+  p->p2p = false;
+  p->p2p_epoch = 0;
+  if (c->nranks == 1 || p->general_halo) return false;
+  const char* env = std::getenv("CS_P2P_HALO");
+  int ok = (env == nullptr || std::atoi(env) != 0) && !p->ws.pooled && p->ws.p != nullptr;
+  if (ok && p->sig.p == nullptr) {
+    StreamBind plain(nullptr);  // IPC export needs a cudaMalloc allocation
+    p->sig.alloc(64);
+  }
+  // receive counters restart at 0 for this solve; the exchange below orders the
+  // reset before any peer's first push
+  if (p->sig.p) CS_CUDA(cudaMemsetAsync(p->sig.p, 0, 64, c->stream));
+  PeerInfo mine{};
+  if (ok) {
+    ok = cudaIpcGetMemHandle(&mine.ws, p->ws.p) == cudaSuccess &&
+         cudaIpcGetMemHandle(&mine.sig, p->sig.p) == cudaSuccess;
+    cudaGetLastError();
+  }
+  mine.gen = p->ws_gen;
+  mine.z_off = Z - p->ws.as<double>();
+  mine.ld = p->ld;
+  mine.n_local = p->n_local;
+  mine.ghost_lo = p->ghost_lo;
+  {
+    cudaDeviceProp prop;
+    CS_CUDA(cudaGetDeviceProperties(&prop, c->device));
+    std::memcpy(mine.uuid, prop.uuid.bytes, 16);
+  }
+  mine.ok = ok;
+  DBuf dev(3 * sizeof(PeerInfo));
+  PeerInfo* d = dev.as<PeerInfo>();
+  CS_CUDA(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+  CS_NCCL(ncclGroupStart());
+  if (p->ghost_lo > 0) {
+    CS_NCCL(ncclSend(d, sizeof(PeerInfo), ncclChar, c->rank - 1, c->comm, c->stream));
+    CS_NCCL(ncclRecv(d + 1, sizeof(PeerInfo), ncclChar, c->rank - 1, c->comm, c->stream));
+  }
+  if (p->ghost_hi > 0) {
+    CS_NCCL(ncclSend(d, sizeof(PeerInfo), ncclChar, c->rank + 1, c->comm, c->stream));
+    CS_NCCL(ncclRecv(d + 2, sizeof(PeerInfo), ncclChar, c->rank + 1, c->comm, c->stream));
+  }
+  CS_NCCL(ncclGroupEnd());
+  PeerInfo got[3];
+  CS_CUDA(cudaMemcpyAsync(got, d, sizeof got, cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int side = 0; side < 2 && ok; ++side) {
+    const bool present = side == 0 ? p->ghost_lo > 0 : p->ghost_hi > 0;
+    if (!present) continue;
+    const PeerInfo& in = got[1 + side];
+    // ranks sharing one GPU must not spin on each other (no co-scheduling
+    // guarantee between their kernels): those fall back to NCCL
+    if (!in.ok || std::memcmp(in.uuid, mine.uuid, 16) == 0) {
+      ok = 0;
+      break;
+    }
+    cs_problem::PeerMap& m = p->peer[side];
+    if (m.ws == nullptr || m.gen != in.gen) {
+      if (m.ws) cudaIpcCloseMemHandle(m.ws);
+      if (m.sig) cudaIpcCloseMemHandle(m.sig);
+      m = cs_problem::PeerMap{};
+      if (cudaIpcOpenMemHandle(&m.ws, in.ws, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+          cudaIpcOpenMemHandle(&m.sig, in.sig, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      m.gen = in.gen;
+    }
+    m.ld = in.ld;
+    // rank-1 holds my first plane in its upper ghost slots; rank+1 my last in its lower
+    m.ghost_off = in.z_off + in.n_local + (side == 0 ? in.ghost_lo : 0);
+  }
+  // every rank takes the same path
+  DBuf e(sizeof(int));
+  CS_CUDA(cudaMemcpyAsync(e.p, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CS_NCCL(ncclAllReduce(e.p, e.p, 1, ncclInt32, ncclMin, c->comm, c->stream));
+  int all = 0;
+  CS_CUDA(cudaMemcpyAsync(&all, e.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  p->p2p = all != 0;
+  return p->p2p;
+}
+
+void spmv_p2p(cs_problem* p, int kind, SpmvArgs g, int push_col) {
+  cs_ctx* c = p->ctx;
+  const SellView A = p->view();
+  ++p->p2p_epoch;
+  if (push_col >= 0) fill_push(p, g, push_col);
+  {
+    Launch L(c, CS_PHASE_SPMV);
+    launch_spmv(kind, A, g, p->slice_int_begin, p->slice_int_end, c->stream);
+  }
+  g.wait_ctr = p->sig.as<unsigned long long>();
+  g.want_lo = p->p2p_epoch * static_cast<unsigned long long>(p->ghost_lo);
+  g.want_hi = p->p2p_epoch * static_cast<unsigned long long>(p->ghost_hi);
+  Launch L(c, CS_PHASE_SPMV);
+  launch_spmv(kind, A, g, p->slice_int_end, p->nslices + p->slice_int_begin, c->stream);
+}
+
+void p2p_push(cs_problem* p, const double* src, int col, DevState* st) {
+  SpmvArgs g;
+  fill_push(p, g, col);
+  Launch L(p->ctx, CS_PHASE_COMM);
+  launch_halo_push(g, src, p->n_local, st, p->ctx->stream);
+}
+
 std::string format_device_error(unsigned long long word, int) {
   const int code = static_cast<int>((word >> 32) & 0xff);
   const int sub = static_cast<int>((word >> 40) & 0xff);
@@ -164,6 +310,8 @@ std::string format_device_error(unsigned long long word, int) {
         return "gram solve failed at outer iteration " + k +
                ": cholesky: non-positive pivot (basis breakdown)";
       return "pcg: non-positive curvature at iteration " + k;
+    case CS_ERR_NCCL:
+      return "halo exchange: peer ghost planes did not arrive (peer-memory halo timeout)";
     case CS_ERR_GENERIC:
       if (sub == 1) return "estimate_interval: degenerate start vector";
       return "estimate_interval: non-finite value";
@@ -278,55 +426,110 @@ int64_t read_i64(cs_ctx* c, const int64_t* dev) {
 
 // Convert the freshly assembled explicit SELL-32 into SELL-32P (common.cuh):
 // pattern-compressed slices drop their 4 B/slot column stream.
-void compress_sell(cs_problem* p) {
+void compress_sell(cs_problem* p, int dedupe = 1) {
   cs_ctx* c = p->ctx;
   const int64_t ns = p->nslices;
-  DBuf cnt(sizeof(int64_t) * 3 * std::max<int64_t>(ns, 1));
-  DBuf ptrs(sizeof(int64_t) * 3 * (ns + 1));
+  const int64_t nn = std::max<int64_t>(ns, 1);
+  DBuf cnt(sizeof(int64_t) * 7 * nn);
+  DBuf ptrs(sizeof(int64_t) * 4 * (ns + 1));
+  DBuf keys(sizeof(unsigned long long) * 2 * nn), slcs(sizeof(int32_t) * 3 * nn);
   int64_t* val_cnt = cnt.as<int64_t>();
-  int64_t* pat_cnt = val_cnt + ns;
-  int64_t* col_cnt = pat_cnt + ns;
+  int64_t* pat_cnt = val_cnt + nn;
+  int64_t* col_cnt = pat_cnt + nn;
+  int64_t* kind = col_cnt + nn;
+  int64_t* tab_cnt = kind + nn;
+  int64_t* headpos = tab_cnt + nn;
+  int64_t* slice_tab = headpos + nn;
   int64_t* new_ptr = ptrs.as<int64_t>();
   int64_t* pat_ptr = new_ptr + (ns + 1);
   int64_t* col_ptr = pat_ptr + (ns + 1);
-  launch_compress_plan(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), val_cnt, pat_cnt,
-                       col_cnt, c->stream);
-  size_t tb = 0;
+  int64_t* tab_ptr = col_ptr + (ns + 1);
+  unsigned long long* hash = keys.as<unsigned long long>();
+  unsigned long long* hash_sorted = hash + nn;
+  int32_t* iota = slcs.as<int32_t>();
+  int32_t* slc_sorted = iota + nn;
+  int32_t* slice_rep = slc_sorted + nn;
+  launch_compress_plan(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), p->vals.as<double>(),
+                       val_cnt, pat_cnt, col_cnt, kind, hash, dedupe, c->stream);
+  // uniform tables: sort (hash, slice), one table per group of equal hashes
+  launch_iota_i32(ns, iota, c->stream);
+  size_t tb = 0, tm = 0, ts = 0;
   scan_slice_ptr(val_cnt, ns, new_ptr, nullptr, &tb, c->stream);
-  DBuf tmp(tb);
-  for (int64_t* pair : {val_cnt, pat_cnt, col_cnt}) {
-    int64_t* out = pair == val_cnt ? new_ptr : pair == pat_cnt ? pat_ptr : col_ptr;
+  if (ns > 0) {
+    scan_max_i64(headpos, ns, headpos, nullptr, &tm, c->stream);
+    sort_tables(hash, hash_sorted, iota, slc_sorted, ns, nullptr, &ts, c->stream);
+  }
+  DBuf tmp(std::max({tb, tm, ts}));
+  if (ns > 0) {
+    sort_tables(hash, hash_sorted, iota, slc_sorted, ns, tmp.p, &ts, c->stream);
+    launch_table_heads(ns, hash_sorted, slc_sorted, kind, tab_cnt, headpos, c->stream);
+    scan_max_i64(headpos, ns, headpos, tmp.p, &tm, c->stream);
+  }
+  for (int64_t* pair : {val_cnt, pat_cnt, col_cnt, tab_cnt}) {
+    int64_t* out = pair == val_cnt ? new_ptr : pair == pat_cnt ? pat_ptr
+                 : pair == col_cnt ? col_ptr : tab_ptr;
     if (ns > 0) scan_slice_ptr(pair, ns, out, tmp.p, &tb, c->stream);
     else CS_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), c->stream));
   }
+  // tab_ptr is indexed by sorted position: exclusive offsets of the heads
+  launch_table_assign(ns, hash_sorted, slc_sorted, headpos, tab_ptr, slice_tab, slice_rep,
+                      c->stream);
   const int64_t nval = read_i64(c, new_ptr + ns);
-  const int64_t npat = read_i64(c, pat_ptr + ns);
+  const int64_t nvpat = read_i64(c, pat_ptr + ns);
   const int64_t ncol = read_i64(c, col_ptr + ns);
+  const int64_t ntab = read_i64(c, tab_ptr + ns);
+  const int64_t npat = ntab + nvpat;  // [uniform tables | value-pattern slices]
   DBuf nvals(sizeof(double) * std::max<int64_t>(nval, 1));
   DBuf ncols(sizeof(int32_t) * std::max<int64_t>(ncol, 1));
-  p->pat.alloc(sizeof(int2) * std::max<int64_t>(npat, 1));
-  p->meta.alloc(sizeof(int64_t) * std::max<int64_t>(ns, 1));
+  DBuf npatb(sizeof(int2) * std::max<int64_t>(npat, 1));
+  DBuf npval(sizeof(double) * std::max<int64_t>(npat, 1));
+  DBuf nmeta(sizeof(int64_t) * nn);
   launch_compress_fill(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), p->vals.as<double>(),
-                       new_ptr, pat_ptr, col_ptr, nvals.as<double>(), ncols.as<int32_t>(),
-                       p->pat.as<int2>(), p->meta.as<int64_t>(), c->stream);
+                       kind, slice_tab, slice_rep, new_ptr, pat_ptr, ntab, col_ptr,
+                       nvals.as<double>(), ncols.as<int32_t>(), npatb.as<int2>(),
+                       npval.as<double>(), nmeta.as<int64_t>(), c->stream);
+  DBuf bad(sizeof(int));
+  CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  launch_compress_verify(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(),
+                         p->vals.as<double>(), kind, slice_tab, npatb.as<int2>(),
+                         npval.as<double>(), bad.as<int>(), c->stream);
+  int hbad = 0;
+  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  if (hbad) {
+    if (!dedupe) fail(CS_ERR_GENERIC, 0, "SELL-32PU conversion failed verification");
+    compress_sell(p, 0);  // hash collision: one table per uniform slice
+    return;
+  }
   DBuf nptr(sizeof(int64_t) * (ns + 1));
   CS_CUDA(cudaMemcpyAsync(nptr.p, new_ptr, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToDevice,
                           c->stream));
-  CS_CUDA(cudaStreamSynchronize(c->stream));
-  p->vals = std::move(nvals);
-  p->cols = std::move(ncols);
-  p->slice_ptr = std::move(nptr);
-  int64_t nc = 0, wmax = 0;
+  int64_t nc = 0, nu = 0, wmax = 0;
   {
-    std::vector<int64_t> h(ns), w(ns);
+    std::vector<int64_t> k(ns), w(ns);
     if (ns) {
-      CS_CUDA(cudaMemcpy(h.data(), pat_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost));
-      CS_CUDA(cudaMemcpy(w.data(), val_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost));
+      CS_CUDA(cudaMemcpyAsync(k.data(), kind, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost,
+                              c->stream));
+      CS_CUDA(cudaMemcpyAsync(w.data(), val_cnt, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost,
+                              c->stream));
     }
-    for (int64_t v : h) nc += v > 0;
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    for (int64_t v : k) {
+      nc += (v & 0xff) != 0;
+      nu += (v & 0xff) == 2;
+    }
     for (int64_t v : w) wmax = std::max(wmax, v / kSliceRows);
   }
+  p->vals = std::move(nvals);
+  p->cols = std::move(ncols);
+  p->pat = std::move(npatb);
+  p->pval = std::move(npval);
+  p->meta = std::move(nmeta);
+  p->slice_ptr = std::move(nptr);
   p->compressed_slices = nc;
+  p->uniform_slices = nu;
+  p->pattern_entries = npat;
+  p->table_entries = ntab;
   p->max_width = static_cast<int>(wmax);
 }
 

@@ -128,15 +128,30 @@ struct cs_problem {
   }
   int gen_kind = -1;
   int64_t nx = 0, ny = 0, nz = 0;
-  csg::DBuf slice_ptr, vals, cols, meta, pat, diag, inv_diag, ghost_global;
-  int64_t compressed_slices = 0;
+  csg::DBuf slice_ptr, vals, cols, meta, pat, pval, diag, inv_diag, ghost_global;
+  int64_t compressed_slices = 0, uniform_slices = 0, pattern_entries = 0, table_entries = 0;
   int max_width = 0;
   std::vector<int64_t> ghosts_host;
   int precond = CS_PRECOND_IDENTITY;
   // cached solve workspace and Lanczos basis (reused across solves)
   int ws_s = -1;
+  uint64_t ws_gen = 0;  // bumped whenever ws is (re)allocated
   csg::DBuf ws;
   csg::DBuf lz;
+  // NVLink peer-memory halo of the fast MPK (z-slab problems):
+  // the neighbours' workspaces and receive counters mapped by CUDA IPC
+  struct PeerMap {
+    uint64_t gen = 0;               // peer ws generation of the mapping
+    void* ws = nullptr;             // mapped peer workspace base
+    void* sig = nullptr;            // mapped peer receive counters
+    int64_t ghost_off = 0;          // element offset of my plane in the peer's Z column 0
+    int64_t ld = 0;                 // peer column stride (elements)
+  };
+  PeerMap peer[2];                  // [rank-1, rank+1]
+  csg::DBuf sig;                    // my receive counters [from rank-1, from rank+1] (IPC-exported)
+  int64_t z_off = 0;                // element offset of Z in ws
+  bool p2p = false;                 // peer mappings valid for the current ws
+  unsigned long long p2p_epoch = 0; // halo exchanges consumed in the current solve
   csg::SellView view() const {
     csg::SellView v;
     v.n_local = n_local;
@@ -146,6 +161,10 @@ struct cs_problem {
     v.cols = cols.as<int32_t>();
     v.meta = meta.as<int64_t>();
     v.pat = pat.as<int2>();
+    v.pval = pval.as<double>();
+    v.uniform = uniform_slices > 0;
+    v.uniform_all = uniform_slices == nslices && nslices > 0;
+    v.table_entries = table_entries;
     v.max_width = max_width;
     v.inv_diag = precond == CS_PRECOND_JACOBI ? inv_diag.as<double>() : nullptr;
     return v;
@@ -169,6 +188,17 @@ void collect_timing(cs_ctx* c);
 void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand_col);
 void halo_exchange(cs_problem* p, double* col);
 void allreduce_sum(cs_ctx* c, double* dev, size_t count);
+// NVLink halo: map the neighbours' workspaces (collective over the communicator;
+// every rank calls it once per solve after its workspace is final). Returns
+// whether the peer-memory path is on for this solve (all ranks agree).
+bool p2p_setup(cs_problem* p, double* Z);
+void p2p_teardown(cs_problem* p);
+// SpMV of the fast MPK through the peer-memory halo: interior slices, then the
+// boundary slices after this exchange's ghost planes arrived; push_col (or
+// nullptr) is the Z column whose boundary rows the epilogue pushes.
+void spmv_p2p(cs_problem* p, int kind, SpmvArgs g, int push_col);
+// push Z column `col`'s boundary rows (the z_0 halo after the update pass)
+void p2p_push(cs_problem* p, const double* src, int col, DevState* st);
 // scratch region of the context, grown on demand
 void* ctx_scratch(cs_ctx* c, size_t bytes);
 

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.cuh"
@@ -236,13 +237,26 @@ __global__ void halo_gather_kernel(int64_t count, const int32_t* __restrict__ id
     buf[k] = x[idx[k]];
 }
 
+// slots of slice `slice` (value slots, or the pattern length of a uniform slice)
+__device__ __forceinline__ int slot_count(const SellView& a, int64_t slice) {
+  const int64_t m = a.meta[slice];
+  if (m < 0 && pat_uniform(m) > 0) return pat_uniform(m);
+  return static_cast<int>((a.slice_ptr[slice + 1] - a.slice_ptr[slice]) >> 5);
+}
+
 // column of slot k of `lane` in slice `slice`, or -1 for an empty slot
-__device__ __forceinline__ int32_t slot_col(const SellView& a, int64_t slice, int64_t base, int k,
-                                            int lane, int64_t row) {
+__device__ __forceinline__ int32_t slot_col(const SellView& a, int64_t slice, int k, int lane,
+                                            int64_t row) {
   const int64_t m = a.meta[slice];
   if (m >= 0) return a.cols[m + k * kSliceRows + lane];
-  const int2 e = a.pat[-m - 1 + k];
+  const int2 e = a.pat[pat_index(m) + k];
   return ((e.y >> lane) & 1) ? static_cast<int32_t>(row + e.x) : -1;
+}
+
+__device__ __forceinline__ double slot_val(const SellView& a, int64_t slice, int k, int lane) {
+  const int64_t m = a.meta[slice];
+  if (m < 0 && pat_uniform(m) > 0) return a.pval[pat_index(m) + k];
+  return a.vals[a.slice_ptr[slice] + k * kSliceRows + lane];
 }
 
 __global__ void sell_row_len_kernel(SellView a, int64_t* len) {
@@ -250,11 +264,10 @@ __global__ void sell_row_len_kernel(SellView a, int64_t* len) {
   if (row >= a.n_local) return;
   const int64_t slice = row >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t base = a.slice_ptr[slice];
-  const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
+  const int width = slot_count(a, slice);
   int cnt = 0;
   for (int k = 0; k < width; ++k)
-    if (slot_col(a, slice, base, k, lane, row) >= 0) ++cnt;
+    if (slot_col(a, slice, k, lane, row) >= 0) ++cnt;
   len[row] = cnt;
 }
 
@@ -266,112 +279,240 @@ __global__ void sell_to_csr_kernel(SellView a, int64_t row_begin,
   if (row >= a.n_local) return;
   const int64_t slice = row >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t base = a.slice_ptr[slice];
-  const int width = static_cast<int>((a.slice_ptr[slice + 1] - base) >> 5);
+  const int width = slot_count(a, slice);
   int64_t o = rowptr[row];
   for (int k = 0; k < width; ++k) {
-    const int32_t c = slot_col(a, slice, base, k, lane, row);
+    const int32_t c = slot_col(a, slice, k, lane, row);
     if (c < 0) continue;
     col[o] = c < a.n_local ? row_begin + c : ghost_global[c - a.n_local];
-    val[o] = a.vals[base + k * kSliceRows + lane];
+    val[o] = slot_val(a, slice, k, lane);
     ++o;
   }
 }
 
-// ---------------------------------------------------------------- SELL-32 -> SELL-32P
+// ---------------------------------------------------------------- SELL-32 -> SELL-32P(U)
 // A slice is pattern-compressed when every row's columns are strictly ascending
 // and the union U of the rows' relative offsets (col - row) is small enough that
 // 32U value slots + U pattern entries cost less than 32W values + 32W columns.
-// The union is built by a warp-wide merge of the 32 sorted offset lists.
+// It is uniform-value (no value slots at all) when, in addition, every union
+// entry carries one bitwise-identical value across the rows that hold it.
+// Uniform slices are deduplicated globally: a 64-bit hash of each slice's
+// (offset, mask, value) table is sorted, equal hashes share one table (the
+// first slice of the group writes it), and a verify pass compares every
+// slice's own table against the shared one exactly (a collision disables the
+// dedupe and the conversion is redone). The union is built by a warp-wide
+// merge of the 32 sorted offset lists.
 constexpr int kSentinel = 0x7fffffff;
+constexpr unsigned long long kNoTable = ~0ull;
+enum SliceKind : int64_t { kExplicit = 0, kValuePattern = 1, kUniform = 2 };
 
-__device__ __forceinline__ int lane_offset(const int32_t* cols, int64_t base, int idx, int len,
-                                           int64_t row) {
-  return idx < len ? static_cast<int>(cols[base + idx * kSliceRows] - row) : kSentinel;
+// Merge cursor over one slice's 32 sorted rows (one lane per row).
+struct PatWalk {
+  const int32_t* cols;
+  const double* vals;
+  int64_t base, row;
+  int len, idx, width;
+  bool sorted;
+  __device__ void init(const int64_t* slice_ptr, const int32_t* c, const double* v, int64_t slice,
+                       int lane) {
+    cols = c, vals = v;
+    row = slice * kSliceRows + lane;
+    base = slice_ptr[slice] + lane;
+    width = static_cast<int>((slice_ptr[slice + 1] - slice_ptr[slice]) >> 5);
+    len = 0, idx = 0;
+    sorted = true;
+    int32_t prev = -1;
+    for (int k = 0; k < width; ++k) {
+      const int32_t col = cols[base + k * kSliceRows];
+      if (col < 0) break;  // trailing padding
+      if (col <= prev) sorted = false;
+      prev = col;
+      ++len;
+    }
+  }
+  // next union entry: offset, lane mask, the value of the lowest holding lane
+  // and whether every holding lane stores that value bitwise; false at the end
+  __device__ bool next(int& off, unsigned& mask, unsigned long long& vbits, bool& uni) {
+    const int cur = idx < len ? static_cast<int>(cols[base + idx * kSliceRows] - row) : kSentinel;
+    off = __reduce_min_sync(0xffffffffu, cur);
+    if (off == kSentinel) return false;
+    const bool hit = cur == off;
+    mask = __ballot_sync(0xffffffffu, hit);
+    const unsigned long long mine =
+        hit ? static_cast<unsigned long long>(__double_as_longlong(vals[base + idx * kSliceRows]))
+            : 0ull;
+    vbits = __shfl_sync(0xffffffffu, mine, __ffs(mask) - 1);
+    uni = __all_sync(0xffffffffu, !hit || mine == vbits);
+    if (hit) ++idx;
+    return true;
+  }
+};
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long h, unsigned long long v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h ^= h >> 31;
+  h *= 0xbf58476d1ce4e5b9ull;
+  return h ^ (h >> 29);
 }
 
 __global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
-                                     const int32_t* __restrict__ cols, int64_t* val_cnt,
-                                     int64_t* pat_cnt, int64_t* col_cnt, int allow) {
+                                     const int32_t* __restrict__ cols,
+                                     const double* __restrict__ vals, int64_t* val_cnt,
+                                     int64_t* pat_cnt, int64_t* col_cnt, int64_t* kind,
+                                     unsigned long long* hash, int allow, int allow_uniform,
+                                     int dedupe) {
   const int lane = threadIdx.x & 31;
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices) return;
-  const int64_t row = slice * kSliceRows + lane;
-  const int64_t base = slice_ptr[slice] + lane;
-  const int W = static_cast<int>((slice_ptr[slice + 1] - slice_ptr[slice]) >> 5);
-  int len = 0;
-  bool sorted = true;
-  int32_t prev = -1;
-  for (int k = 0; k < W; ++k) {
-    const int32_t c = cols[base + k * kSliceRows];
-    if (c < 0) break;  // trailing padding
-    if (c <= prev) sorted = false;
-    prev = c;
-    ++len;
-  }
-  bool ok = __all_sync(0xffffffffu, sorted) && W > 0 && allow;
+  PatWalk w;
+  w.init(slice_ptr, cols, vals, slice, lane);
+  const int W = w.width;
+  bool ok = __all_sync(0xffffffffu, w.sorted) && W > 0 && allow;
+  bool uni = ok && allow_uniform;
   int U = 0;
+  unsigned long long h = 0x243f6a8885a308d3ull;
   if (ok) {
-    int idx = 0;
-    for (;;) {
-      const int cur = lane_offset(cols, base, idx, len, row);
-      const int m = __reduce_min_sync(0xffffffffu, cur);
-      if (m == kSentinel) break;
+    int off;
+    unsigned mask;
+    unsigned long long vb;
+    bool u;
+    while (w.next(off, mask, vb, u)) {
       ++U;
-      if (264 * U > 384 * W) {
+      uni = uni && u && U <= kUniformMaxSlots;
+      if (uni) h = mix64(mix64(mix64(h, static_cast<unsigned>(off)), mask), vb);
+      if (!uni && 264 * U > 384 * W) {
         ok = false;
         break;
       }
-      if (cur == m) ++idx;
     }
   }
   if (lane == 0) {
-    val_cnt[slice] = static_cast<int64_t>(kSliceRows) * (ok ? U : W);
-    pat_cnt[slice] = ok ? U : 0;
-    col_cnt[slice] = ok ? 0 : static_cast<int64_t>(kSliceRows) * W;
+    const int64_t k = !ok ? kExplicit : !uni ? kValuePattern : kUniform;
+    kind[slice] = k | (static_cast<int64_t>(U) << 8);
+    val_cnt[slice] = k == kExplicit ? int64_t{kSliceRows} * W
+                     : k == kValuePattern ? int64_t{kSliceRows} * U
+                                          : 0;
+    pat_cnt[slice] = k == kValuePattern ? U : 0;
+    col_cnt[slice] = k == kExplicit ? int64_t{kSliceRows} * W : 0;
+    // uniform: table hash (top bit clear); dedupe off: the slice index (unique)
+    h = mix64(h, static_cast<unsigned long long>(U)) >> 1;
+    hash[slice] = k != kUniform ? kNoTable
+                  : dedupe      ? h
+                                : static_cast<unsigned long long>(slice);
   }
+}
+
+// sorted position i: entries of a new table group (first of equal hashes)
+__global__ void table_heads_kernel(int64_t n, const unsigned long long* __restrict__ key,
+                                   const int32_t* __restrict__ slc,
+                                   const int64_t* __restrict__ kind, int64_t* tab_cnt,
+                                   int64_t* headpos) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool head = key[i] != kNoTable && (i == 0 || key[i] != key[i - 1]);
+  tab_cnt[i] = head ? (kind[slc[i]] >> 8) : 0;
+  headpos[i] = head ? i : -1;
+}
+
+// per slice: table offset and the representative (first) slice of its group
+__global__ void table_assign_kernel(int64_t n, const unsigned long long* __restrict__ key,
+                                    const int32_t* __restrict__ slc,
+                                    const int64_t* __restrict__ headpos,
+                                    const int64_t* __restrict__ tab_ptr, int64_t* slice_tab,
+                                    int32_t* slice_rep) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t s = slc[i];
+  if (key[i] == kNoTable) {
+    slice_tab[s] = -1;
+    slice_rep[s] = -1;
+    return;
+  }
+  const int64_t hp = headpos[i];
+  slice_tab[s] = tab_ptr[hp];
+  slice_rep[s] = slc[hp];
 }
 
 __global__ void compress_fill_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
                                      const int32_t* __restrict__ cols,
                                      const double* __restrict__ vals,
+                                     const int64_t* __restrict__ kind,
+                                     const int64_t* __restrict__ slice_tab,
+                                     const int32_t* __restrict__ slice_rep,
                                      const int64_t* __restrict__ new_ptr,
-                                     const int64_t* __restrict__ pat_ptr,
+                                     const int64_t* __restrict__ pat_ptr, int64_t pat_base,
                                      const int64_t* __restrict__ col_ptr, double* nvals,
-                                     int32_t* ncols, int2* pat, int64_t* meta) {
+                                     int32_t* ncols, int2* pat, double* pval, int64_t* meta) {
   const int lane = threadIdx.x & 31;
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices) return;
-  const int64_t row = slice * kSliceRows + lane;
+  const int64_t k = kind[slice] & 0xff;
+  const int U = static_cast<int>(kind[slice] >> 8);
   const int64_t base = slice_ptr[slice] + lane;
   const int W = static_cast<int>((slice_ptr[slice + 1] - slice_ptr[slice]) >> 5);
-  const int64_t nb = new_ptr[slice] + lane;
-  const int64_t U = pat_ptr[slice + 1] - pat_ptr[slice];
-  if (U > 0) {
-    int len = 0;
-    for (int k = 0; k < W; ++k) {
-      if (cols[base + k * kSliceRows] < 0) break;
-      ++len;
-    }
-    int idx = 0;
-    for (int u = 0; u < U; ++u) {
-      const int cur = lane_offset(cols, base, idx, len, row);
-      const int m = __reduce_min_sync(0xffffffffu, cur);
-      const bool hit = cur == m;
-      const unsigned mask = __ballot_sync(0xffffffffu, hit);
-      nvals[nb + u * kSliceRows] = hit ? vals[base + idx * kSliceRows] : 0.0;
-      if (lane == 0) pat[pat_ptr[slice] + u] = make_int2(m, static_cast<int>(mask));
-      if (hit) ++idx;
-    }
-    if (lane == 0) meta[slice] = -pat_ptr[slice] - 1;
-  } else {
+  if (k == kExplicit) {
+    const int64_t nb = new_ptr[slice] + lane;
     const int64_t cb = col_ptr[slice] + lane;
-    for (int k = 0; k < W; ++k) {
-      nvals[nb + k * kSliceRows] = vals[base + k * kSliceRows];
-      ncols[cb + k * kSliceRows] = cols[base + k * kSliceRows];
+    for (int q = 0; q < W; ++q) {
+      nvals[nb + q * kSliceRows] = vals[base + q * kSliceRows];
+      ncols[cb + q * kSliceRows] = cols[base + q * kSliceRows];
     }
     if (lane == 0) meta[slice] = col_ptr[slice];
+    return;
   }
+  if (k == kUniform && slice_rep[slice] != slice) {  // shares its group's table
+    if (lane == 0) meta[slice] = make_pat_meta(slice_tab[slice], U);
+    return;
+  }
+  PatWalk w;
+  w.init(slice_ptr, cols, vals, slice, lane);
+  const int64_t pb = k == kUniform ? slice_tab[slice] : pat_base + pat_ptr[slice];
+  const int64_t nb = new_ptr[slice] + lane;
+  int off;
+  unsigned mask;
+  unsigned long long vb;
+  bool u;
+  for (int q = 0; q < U && w.next(off, mask, vb, u); ++q) {
+    if (lane == 0) {
+      pat[pb + q] = make_int2(off, static_cast<int>(mask));
+      pval[pb + q] = k == kUniform ? __longlong_as_double(static_cast<long long>(vb)) : 0.0;
+    }
+    if (k == kValuePattern) {
+      // w.idx was advanced past this entry on the holding lanes
+      const bool hit = (mask >> lane) & 1u;
+      nvals[nb + q * kSliceRows] = hit ? vals[base + (w.idx - 1) * kSliceRows] : 0.0;
+    }
+  }
+  if (lane == 0) meta[slice] = make_pat_meta(pb, k == kUniform ? U : 0);
+}
+
+// every uniform slice against the table it points at, exactly
+__global__ void compress_verify_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
+                                       const int32_t* __restrict__ cols,
+                                       const double* __restrict__ vals,
+                                       const int64_t* __restrict__ kind,
+                                       const int64_t* __restrict__ slice_tab,
+                                       const int2* __restrict__ pat,
+                                       const double* __restrict__ pval, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (slice >= nslices || (kind[slice] & 0xff) != kUniform) return;
+  const int U = static_cast<int>(kind[slice] >> 8);
+  const int64_t pb = slice_tab[slice];
+  PatWalk w;
+  w.init(slice_ptr, cols, vals, slice, lane);
+  int off;
+  unsigned mask;
+  unsigned long long vb;
+  bool u;
+  bool same = true;
+  int q = 0;
+  for (; q < U && w.next(off, mask, vb, u); ++q) {
+    const int2 e = pat[pb + q];
+    same = same && e.x == off && static_cast<unsigned>(e.y) == mask &&
+           static_cast<unsigned long long>(__double_as_longlong(pval[pb + q])) == vb;
+  }
+  if (lane == 0 && (!same || q != U)) atomicExch(bad, 1);
 }
 
 __global__ void inv_diag_kernel(int64_t n, const double* __restrict__ diag, double* inv, int* bad) {
@@ -463,22 +604,78 @@ void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* gho
 }
 
 void launch_compress_plan(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                          int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt, cudaStream_t st) {
+                          const double* vals, int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt,
+                          int64_t* kind, unsigned long long* hash, int dedupe, cudaStream_t st) {
   if (nslices == 0) return;
-  // CS_SELL_EXPLICIT=1 keeps every slice explicit (format A/B experiments)
-  static const int allow = std::getenv("CS_SELL_EXPLICIT") ? 0 : 1;
-  compress_plan_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(nslices, slice_ptr, cols,
-                                                                    val_cnt, pat_cnt, col_cnt, allow);
+  // CS_SELL_EXPLICIT=1 keeps every slice explicit; CS_SELL_VALUES=1 keeps the value
+  // slots (no uniform-value slices) -- format A/B experiments, read per conversion
+  const int allow = std::getenv("CS_SELL_EXPLICIT") ? 0 : 1;
+  const int allow_uniform = std::getenv("CS_SELL_VALUES") ? 0 : 1;
+  compress_plan_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
+      nslices, slice_ptr, cols, vals, val_cnt, pat_cnt, col_cnt, kind, hash, allow, allow_uniform,
+      dedupe);
   CS_CUDA(cudaGetLastError());
 }
 
+void scan_max_i64(const int64_t* in, int64_t n, int64_t* out, void* tmp, size_t* tmp_bytes,
+                  cudaStream_t st) {
+  CS_CUDA(cub::DeviceScan::InclusiveScan(tmp, *tmp_bytes, in, out, ::cuda::maximum<>{}, n, st));
+}
+
+void sort_tables(const unsigned long long* key_in, unsigned long long* key_out,
+                 const int32_t* val_in, int32_t* val_out, int64_t n, void* tmp, size_t* tmp_bytes,
+                 cudaStream_t st) {
+  CS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, *tmp_bytes, key_in, key_out, val_in, val_out,
+                                          static_cast<int>(n), 0, 64, st));
+}
+
+void launch_table_heads(int64_t n, const unsigned long long* key, const int32_t* slc,
+                        const int64_t* kind, int64_t* tab_cnt, int64_t* headpos, cudaStream_t st) {
+  if (n == 0) return;
+  table_heads_kernel<<<grid_for(n), kThreads, 0, st>>>(n, key, slc, kind, tab_cnt, headpos);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_table_assign(int64_t n, const unsigned long long* key, const int32_t* slc,
+                         const int64_t* headpos, const int64_t* tab_ptr, int64_t* slice_tab,
+                         int32_t* slice_rep, cudaStream_t st) {
+  if (n == 0) return;
+  table_assign_kernel<<<grid_for(n), kThreads, 0, st>>>(n, key, slc, headpos, tab_ptr, slice_tab,
+                                                        slice_rep);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_iota_i32(int64_t n, int32_t* out, cudaStream_t st);
+
 void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                          const double* vals, const int64_t* new_ptr, const int64_t* pat_ptr,
-                          const int64_t* col_ptr, double* nvals, int32_t* ncols, int2* pat,
-                          int64_t* meta, cudaStream_t st) {
+                          const double* vals, const int64_t* kind, const int64_t* slice_tab,
+                          const int32_t* slice_rep, const int64_t* new_ptr, const int64_t* pat_ptr,
+                          int64_t pat_base, const int64_t* col_ptr, double* nvals, int32_t* ncols,
+                          int2* pat, double* pval, int64_t* meta, cudaStream_t st) {
   if (nslices == 0) return;
   compress_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
-      nslices, slice_ptr, cols, vals, new_ptr, pat_ptr, col_ptr, nvals, ncols, pat, meta);
+      nslices, slice_ptr, cols, vals, kind, slice_tab, slice_rep, new_ptr, pat_ptr, pat_base,
+      col_ptr, nvals, ncols, pat, pval, meta);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_compress_verify(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
+                            const double* vals, const int64_t* kind, const int64_t* slice_tab,
+                            const int2* pat, const double* pval, int* bad, cudaStream_t st) {
+  if (nslices == 0) return;
+  compress_verify_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
+      nslices, slice_ptr, cols, vals, kind, slice_tab, pat, pval, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
+__global__ void iota_i32_kernel(int64_t n, int32_t* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<int32_t>(i);
+}
+
+void launch_iota_i32(int64_t n, int32_t* out, cudaStream_t st) {
+  if (n == 0) return;
+  iota_i32_kernel<<<grid_for(n), kThreads, 0, st>>>(n, out);
   CS_CUDA(cudaGetLastError());
 }
 

@@ -263,7 +263,13 @@ Blocks workspace(cs_problem* p, int s) {
   const size_t vecs = static_cast<size_t>(4 * s + 5);
   if (p->ws_s != s) {
     p->ws.release();
-    p->ws.alloc(sizeof(double) * vecs * ld);
+    {
+      // multi-GPU: a plain cudaMalloc allocation, exportable to the neighbours
+      // for the peer-memory halo (pool allocations cannot be IPC-mapped)
+      StreamBind plain(p->ctx->nranks > 1 ? nullptr : g_alloc_stream);
+      p->ws.alloc(sizeof(double) * vecs * ld);
+    }
+    ++p->ws_gen;
     CS_CUDA(cudaMemsetAsync(p->ws.p, 0, sizeof(double) * vecs * ld, p->ctx->stream));
     p->ws_s = s;
   }
@@ -283,7 +289,7 @@ Blocks workspace(cs_problem* p, int s) {
 
 // MPK steps 1..s on a basis whose z_0 is already in Z column 0 (mpk.cpp:53-69).
 void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int pending,
-               DevState* st, bool fast = false) {
+               DevState* st, bool fast = false, bool p2p = false) {
   const int64_t ld = p->ld;
   const double alpha = 2.0 / (hi - lo);           // mpk.hpp:22
   const double sigma = (hi + lo) / (hi - lo);     // mpk.hpp:23-25
@@ -316,7 +322,8 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     g.pending = pending;
     g.st = st;
     const int kind = fast ? (q == 1 ? kMpkFirstF : kMpkMidF) : (q == 1 ? kMpkFirst : kMpkMid);
-    spmv_halo(p, kind, g, zcol(q - 1));
+    if (p2p) spmv_p2p(p, kind, g, q);  // z_q's boundary rows go straight to the neighbours
+    else spmv_halo(p, kind, g, zcol(q - 1));
   }
   SpmvArgs g;
   g.x = zcol(s - 1);
@@ -324,7 +331,8 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
   g.col = s - 1;
   g.pending = pending;
   g.st = st;
-  spmv_halo(p, kMpkLast, g, zcol(s - 1));
+  if (p2p) spmv_p2p(p, kMpkLast, g, -1);
+  else spmv_halo(p, kMpkLast, g, zcol(s - 1));
 }
 
 }  // namespace
@@ -620,6 +628,9 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   }
 
   // ---- outer iterations
+  // multi-GPU fast algebra: halo planes move by NVLink peer stores from the
+  // producing kernels (no NCCL on the SpMV path); collective, every rank calls it
+  const bool p2p = mode == CS_MODE_FAST && !hooks.any() && c->nranks > 1 && p2p_setup(p, bk.Z);
   auto outer_fast = [&](bool first) {
     ua.beta = first ? nullptr : beta_d;
     ua.zw = bk.Z;  // z_0 = M^-1 r_k for the next MPK
@@ -627,7 +638,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
       Launch L(c, CS_PHASE_UPDATE);
       launch_fast_update(ua, c->stream);
     }
-    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true);
+    if (p2p) p2p_push(p, bk.Z, 0, st);
+    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true, p2p);
     packed_reduce(bk.Q, bk.Z);
     small(launch_fast_step);
   };

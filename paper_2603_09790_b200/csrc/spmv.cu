@@ -22,6 +22,8 @@
 //              z_q = 2a D^-1 p_q - 2s z_{q-1} - z_{q-2}  (first step: a, -s, no z_{q-2});
 //              D = a_ii and z_{q-1}[row] are picked up by the row loop itself, so
 //              the step reads/writes 24n fewer bytes than the reference recurrence.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace csg {
@@ -30,6 +32,9 @@ namespace {
 constexpr int kWarps = 8;  // warps per 256-thread block
 #ifndef CS_SPMV_MINB
 #define CS_SPMV_MINB 8  // 32 registers: full occupancy (64 warps / SM)
+#endif
+#ifndef CS_SPMV_UNI_MINB
+#define CS_SPMV_UNI_MINB 6  // uniform-table kernel: 40 registers, 48 warps / SM
 #endif
 #ifndef CS_SPMV_PERSIST
 #define CS_SPMV_PERSIST 1
@@ -46,20 +51,54 @@ struct SliceMeta {
   int64_t base, end, meta;
 };
 
+template <bool UNI = false>
 __device__ __forceinline__ SliceMeta load_meta(const SellView& a, int64_t slice, int64_t se) {
-  SliceMeta m{0, 0, 0};
+  SliceMeta m{0, 0, make_pat_meta(0, 0)};
   if (slice < se) {
-    m.base = a.slice_ptr[slice];
-    m.end = a.slice_ptr[slice + 1];
+    if constexpr (!UNI) {  // uniform slices have no value slots
+      m.base = a.slice_ptr[slice];
+      m.end = a.slice_ptr[slice + 1];
+    }
     m.meta = a.meta[slice];
   }
   return m;
 }
 
+// Uniform-table slot staged in shared memory: one 16-byte broadcast load per slot.
+struct __align__(16) SlotRec {
+  int off;
+  unsigned mask;
+  double v;
+};
+constexpr int kStabMax = 1024;  // staged table entries per block (16 KB)
+
+__device__ __forceinline__ int stage_tables(const SellView& a, SlotRec* stab) {
+  const int staged = a.table_entries < kStabMax ? static_cast<int>(a.table_entries) : kStabMax;
+  for (int i = threadIdx.x; i < staged; i += blockDim.x) {
+    const int2 e = __ldg(a.pat + i);
+    stab[i] = SlotRec{e.x, static_cast<unsigned>(e.y), __ldg(a.pval + i)};
+  }
+  __syncthreads();
+  return staged;
+}
+
 // One row of one slice: sum_k v_k * x[c_k] in stored order, acc = acc + v*x.
+template <bool UNI>
 __device__ __forceinline__ double row_sum(const SellView& a, const double* __restrict__ x,
-                                          const SliceMeta& sm, int64_t row, int lane) {
+                                          const SliceMeta& sm, int64_t row, int lane,
+                                          const SlotRec* stab, int staged) {
   double acc = 0.0;
+  if constexpr (UNI) {  // every slice uniform, every table staged (host-checked)
+    const SlotRec* t = stab + pat_index(sm.meta);
+    const int U = pat_uniform(sm.meta);
+    const double* xr = x + row;
+#pragma unroll 9
+    for (int k = 0; k < U; ++k) {
+      const SlotRec e = t[k];
+      if ((e.mask >> lane) & 1u) acc = __dadd_rn(acc, __dmul_rn(e.v, __ldg(xr + e.off)));
+    }
+    return acc;
+  }
   const int width = static_cast<int>((sm.end - sm.base) >> 5);
   const double* vp = a.vals + sm.base + lane;
   if (sm.meta >= 0) {  // explicit int32 columns
@@ -70,9 +109,37 @@ __device__ __forceinline__ double row_sum(const SellView& a, const double* __res
       const double v = __ldcs(vp + k * kSliceRows);
       if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
     }
+  } else if (const int U = pat_uniform(sm.meta); U > 0) {  // uniform values, no value slots
+    const int64_t pi = pat_index(sm.meta);
+    if (pi + U <= staged) {  // table in shared memory
+      const SlotRec* t = stab + pi;
+      const double* xr = x + row;
+#pragma unroll 9
+      for (int k = 0; k < U; ++k) {
+        const SlotRec e = t[k];
+        if ((e.mask >> lane) & 1u) acc = __dadd_rn(acc, __dmul_rn(e.v, __ldg(xr + e.off)));
+      }
+    } else if (U <= 32) {
+      // lane k holds table entry k; {off, mask, value} of every slot arrive by shuffle
+      const int2 pl = lane < U ? __ldg(a.pat + pi + lane) : make_int2(0, 0);
+      const double pv = lane < U ? __ldg(a.pval + pi + lane) : 0.0;
+#pragma unroll 9
+      for (int k = 0; k < U; ++k) {
+        const int off = __shfl_sync(0xffffffffu, pl.x, k);
+        const unsigned msk = static_cast<unsigned>(__shfl_sync(0xffffffffu, pl.y, k));
+        const double v = __shfl_sync(0xffffffffu, pv, k);
+        if ((msk >> lane) & 1u) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + row + off)));
+      }
+    } else {
+      for (int k = 0; k < U; ++k) {
+        const int2 e = __ldg(a.pat + pi + k);
+        const double v = __ldg(a.pval + pi + k);
+        if ((e.y >> lane) & 1) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + row + e.x)));
+      }
+    }
   } else if (width <= 32) {  // shared relative-offset pattern: column = row + off_k
     // lane k holds pattern entry k; every slot's {off, mask} arrives by shuffle
-    const int2* pp = a.pat + (-sm.meta - 1);
+    const int2* pp = a.pat + pat_index(sm.meta);
     const int2 pl = lane < width ? __ldg(pp + lane) : make_int2(0, 0);
 #pragma unroll 9
     for (int k = 0; k < width; ++k) {
@@ -82,7 +149,7 @@ __device__ __forceinline__ double row_sum(const SellView& a, const double* __res
       if ((msk >> lane) & 1u) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + row + off)));
     }
   } else {  // wide pattern: broadcast entry loads
-    const int2* pp = a.pat + (-sm.meta - 1);
+    const int2* pp = a.pat + pat_index(sm.meta);
     for (int k = 0; k < width; ++k) {
       const int2 e = __ldg(pp + k);
       const double v = __ldcs(vp + k * kSliceRows);
@@ -119,7 +186,7 @@ __device__ __forceinline__ EpiOps epi_load(const SellView& a, const SpmvArgs& g,
 
 template <int KIND, bool JAC>
 __device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double acc,
-                                          const EpiOps& e, double& dotv) {
+                                          const EpiOps& e, double& dotv, double& zv) {
   if constexpr (KIND == kPlain) {
     g.y[row] = acc;
   } else if constexpr (KIND == kResid) {
@@ -142,6 +209,7 @@ __device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double
     double z = fma(g.cb, e.exd, g.ca * dp);
     if constexpr (KIND == kMpkMidF) z = fma(g.cc, e.e2, z);
     g.zout[row] = z;
+    zv = z;
     if (!isfinite(z)) report(g, g.col);
   } else if constexpr (KIND == kMpkLast) {
     g.y[row] = acc;
@@ -177,34 +245,135 @@ __device__ __forceinline__ void dot_finish(const SpmvArgs& g, double dotv) {
   }
 }
 
+// ------------------------------------------------------------------ NVLink halo
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// thread 0 of every block: wait for this step's ghost planes (bounded: a peer
+// that never signals turns into a CS_ERR_NCCL error instead of a hung GPU)
+__device__ __noinline__ void halo_wait(const unsigned long long* ctr, unsigned long long want_lo,
+                                       unsigned long long want_hi, DevState* st) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(ctr) < want_lo || ld_acquire_sys(ctr + 1) < want_hi) {
+    __nanosleep(100);
+    if (globaltimer() - t0 > 20ull * 1000000000ull) {
+      if (st != nullptr) {
+        atomicCAS(&st->err, 0ull, make_err(11 /*CS_ERR_NCCL*/, 0));
+        st->done = 1;
+      }
+      return;
+    }
+  }
+}
+
+// producer side, per row: copy z into the neighbour's ghost slot
+__device__ __forceinline__ void halo_push_row(const SpmvArgs& g, int64_t row, double z) {
+  if (g.push_lo != nullptr && row < g.send_lo) g.push_lo[row] = z;
+  if (g.push_hi != nullptr && row >= g.hi_begin) g.push_hi[row - g.hi_begin] = z;
+}
+
+// producer side, per warp after its last row: publish the pushed row counts
+// (every lane fences its own remote stores, then lane 0 releases the counts)
+__device__ __forceinline__ void halo_signal(const SpmvArgs& g, unsigned long long cnt_lo,
+                                            unsigned long long cnt_hi, int lane) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    cnt_lo += __shfl_xor_sync(0xffffffffu, cnt_lo, off);
+    cnt_hi += __shfl_xor_sync(0xffffffffu, cnt_hi, off);
+  }
+  if (cnt_lo == 0 && cnt_hi == 0) return;  // warp-uniform after the butterfly
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) {
+    if (cnt_lo) red_release_sys(g.sig_lo, cnt_lo);
+    if (cnt_hi) red_release_sys(g.sig_hi, cnt_hi);
+  }
+}
+
+__global__ void __launch_bounds__(256) halo_push_kernel(SpmvArgs g, const double* __restrict__ col,
+                                                        int64_t n_local, DevState* st) {
+  if (st != nullptr && *(volatile int*)&st->done) return;
+  const int64_t nlo = g.push_lo ? g.send_lo : 0;
+  const int64_t nhi = g.push_hi ? n_local - g.hi_begin : 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t total = nlo + nhi;
+  unsigned long long cl = 0, ch = 0;
+  // whole warps iterate together (trip count rounded up) so the warp shuffles see all lanes
+  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t base = w0; base < total; base += stride) {
+    const int64_t i = base + (threadIdx.x & 31);
+    if (i < nlo) {
+      g.push_lo[i] = col[i];
+      ++cl;
+    } else if (i < total) {
+      const int64_t r = i - nlo;
+      g.push_hi[r] = col[g.hi_begin + r];
+      ++ch;
+    }
+  }
+  halo_signal(g, cl, ch, threadIdx.x & 31);
+}
+
 // ------------------------------------------------------------------ LDG kernel
 // Persistent warps walk slices with a grid stride; the next slice's metadata
 // and the epilogue operands of the current rows are loaded ahead of the row
 // sums so that their latency overlaps the value/x stream.
-template <int KIND, bool JAC>
-__global__ void __launch_bounds__(kWarps * 32, CS_SPMV_MINB)
+template <int KIND, bool JAC, bool UNI>
+__global__ void __launch_bounds__(kWarps * 32, UNI ? CS_SPMV_UNI_MINB : CS_SPMV_MINB)
     sell_kernel(SellView a, SpmvArgs g, int64_t slice_begin, int64_t slice_end) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
+  if (g.wait_ctr != nullptr) {
+    if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
+  const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
+  unsigned long long cnt_lo = 0, cnt_hi = 0;
+  __shared__ SlotRec stab[kStabMax];
+  const int staged = a.uniform ? stage_tables(a, stab) : 0;
   // virtual slice indices past nslices wrap to the start, so [ie, nslices + ib)
   // covers both boundary ranges of a halo'd SpMV in one launch
   const auto phys = [&](int64_t v) { return v >= a.nslices ? v - a.nslices : v; };
   int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   double dotv = 0.0;
-  SliceMeta sm = load_meta(a, phys(slice), slice < slice_end ? a.nslices : 0);
+  SliceMeta sm = load_meta<UNI>(a, phys(slice), slice < slice_end ? a.nslices : 0);
   for (; slice < slice_end; slice += wstride) {
     const int64_t vn = slice + wstride;
-    const SliceMeta next = load_meta(a, phys(vn), vn < slice_end ? a.nslices : 0);
+    const SliceMeta next = load_meta<UNI>(a, phys(vn), vn < slice_end ? a.nslices : 0);
     const int64_t row = phys(slice) * kSliceRows + lane;
     const bool own = row < a.n_local;
     EpiOps e;
     if (own) e = epi_load<KIND, JAC>(a, g, row);
-    const double acc = row_sum(a, g.x, sm, row, lane);
-    if (own) epi_store<KIND, JAC>(g, row, acc, e, dotv);
+    const double acc = row_sum<UNI>(a, g.x, sm, row, lane, stab, staged);
+    if (own) {
+      double zv = 0.0;
+      epi_store<KIND, JAC>(g, row, acc, e, dotv, zv);
+      if constexpr (kPush) {
+        if (push) {
+          halo_push_row(g, row, zv);
+          cnt_lo += g.push_lo != nullptr && row < g.send_lo;
+          cnt_hi += g.push_hi != nullptr && row >= g.hi_begin;
+        }
+      }
+    }
     sm = next;
   }
+  if constexpr (kPush)
+    if (push) halo_signal(g, cnt_lo, cnt_hi, lane);
   if constexpr (KIND == kDot) dot_finish(g, dotv);
 }
 
@@ -292,7 +461,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       const int64_t m = a.meta[slice];
       if (own) e = epi_load<KIND, JAC>(a, g, row);
       if (m < 0) {
-        const int2* pp = a.pat + (-m - 1);
+        const int2* pp = a.pat + pat_index(m);
         const int2 pl = lane < width ? __ldg(pp + lane) : make_int2(0, 0);
 #pragma unroll
         for (int k = 0; k < kXMax; ++k) {
@@ -325,7 +494,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #pragma unroll
       for (int k = 0; k < kXMax; ++k)
         if ((valid >> k) & 1u) acc = __dadd_rn(acc, __dmul_rn(vs[k * kSliceRows], xv[k]));
-      if (own) epi_store<KIND, JAC>(g, row, acc, e, dotv);
+      double zv;
+      if (own) epi_store<KIND, JAC>(g, row, acc, e, dotv, zv);
     }
     __syncthreads();  // every warp is done reading stage st
     if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) {
@@ -341,10 +511,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #define CS_SPMV_TMA 0  // measured slower on B200 (16 warps/SM at 128 regs); DESIGN.md 3
 #endif
 
-int spmv_grid(int64_t nslices) {
+int spmv_grid(int64_t nslices, bool uni = false) {
   const int64_t want = (nslices + kWarps - 1) / kWarps;
   if (!CS_SPMV_PERSIST) return static_cast<int>(want > 0 ? want : 1);
-  const int64_t cap = 148 * (64 / kWarps);  // one wave of resident blocks at full occupancy
+  // one wave of resident blocks at the kernel's occupancy
+  const int64_t cap = 148 * (uni ? CS_SPMV_UNI_MINB : CS_SPMV_MINB);
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
@@ -354,7 +525,9 @@ int tma_grid(int64_t nslices) {
   return static_cast<int>(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
 }
 
-bool use_tma(const SellView& a) { return CS_SPMV_TMA && a.max_width > 0 && a.max_width <= kXMax; }
+bool use_tma(const SellView& a) {
+  return CS_SPMV_TMA && !a.uniform && a.max_width > 0 && a.max_width <= kXMax;
+}
 
 template <int KIND, bool JAC>
 void tma_launch(const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se, cudaStream_t st) {
@@ -377,14 +550,27 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
     else tma_launch<KIND, false>(a, g, sb, se, st);
     return;
   }
-  const unsigned grid = static_cast<unsigned>(spmv_grid(se - sb));
-  if (jac)
-    sell_kernel<KIND, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
-  else
-    sell_kernel<KIND, false><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
+  const bool uni = a.uniform && a.uniform_all && a.table_entries <= kStabMax;
+  const unsigned grid = static_cast<unsigned>(spmv_grid(se - sb, uni));
+  if (uni) {
+    if (jac) sell_kernel<KIND, true, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
+    else sell_kernel<KIND, false, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
+  } else {
+    if (jac) sell_kernel<KIND, true, false><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
+    else sell_kernel<KIND, false, false><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
+  }
 }
 
 }  // namespace
+
+void launch_halo_push(const SpmvArgs& g, const double* col, int64_t n_local, DevState* st,
+                      cudaStream_t s) {
+  const int64_t rows = (g.push_lo ? g.send_lo : 0) + (g.push_hi ? n_local - g.hi_begin : 0);
+  if (rows == 0) return;
+  const int64_t blocks = std::min<int64_t>((rows + 255) / 256, 148 * 4);
+  halo_push_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(g, col, n_local, st);
+  CS_CUDA(cudaGetLastError());
+}
 
 int spmv_dot_blocks(int64_t nslices) {
   const int a = spmv_grid(nslices), b = tma_grid(nslices);

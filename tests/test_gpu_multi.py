@@ -1,6 +1,7 @@
 """Multi-GPU parity (needs >= 2 GPUs; skipped otherwise): runs
 tools/mgpu_check.py under torchrun, one rank per GPU, z-slab partition with
-NCCL halo exchange and one NCCL allreduce per outer iteration."""
+the NVLink peer-memory halo (and the NCCL halo, bitwise the same) and one NCCL
+allreduce per outer iteration."""
 import json
 import os
 import subprocess
@@ -43,6 +44,9 @@ def test_multi_gpu_parity(stencil, n, nz, mm, tmp_path):
         if mm:
             assert r["n_ghost"] > 0, r
         assert r["outer_ok"], r
+        assert r["transport_bitwise"], r
+        assert r["halo_mode"] == ("nccl" if mm else "nvlink-p2p"), r
+        assert r["halo_mode_off"] == "nccl", r
         assert r["x_rel"] <= 1e-8, r
         assert abs(r["pcg_iters"][0] - r["pcg_iters"][1]) <= 1 and r["pcg_x_rel"] <= 1e-8, r
         assert r["lambda_rel"] < 1e-9, r

@@ -8,8 +8,9 @@ its GPU. Checks, per rank, against the CPU oracle (test infrastructure):
   * partitioned assembly: local rows with global columns == the oracle's rows, bitwise;
   * ghost list == the neighbour planes;
   * distributed SpMV (NCCL halo exchange + SELL kernel) == oracle rows, bitwise;
-  * distributed fast-mode PCG-S (one NCCL allreduce per outer iteration):
-    outer count within +-1 of the oracle, x within 1e-8 relative;
+  * distributed fast-mode PCG-S (one NCCL allreduce per outer iteration, halo
+    planes by NVLink peer stores): outer count within +-1 of the oracle, x
+    within 1e-8 relative, and bitwise equal to the same solve with the NCCL halo;
   * classical PCG on the same slabs.
 Rank 0 prints one JSON line with every verdict.
 """
@@ -113,6 +114,15 @@ def main():
     res["outer_ok"] = abs(sol.report.outer_iters - r_o.outer_iters) <= 1
     res["x_rel"] = float(np.linalg.norm(x - x_o) / np.linalg.norm(x_o))
     res["allreduces"] = sol.report.device_allreduces
+    res["halo_mode"] = p.halo_mode
+    # the same solve with the NCCL halo: the transport must not change a bit
+    os.environ["CS_P2P_HALO"] = "0"
+    sol_n = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000,
+                                              spectrum=sol.report.spectrum_used))
+    os.environ.pop("CS_P2P_HALO")
+    res["halo_mode_off"] = p.halo_mode
+    res["transport_bitwise"] = bool(sol_n.x.tobytes() == sol.x.tobytes()
+                                    and sol_n.report.outer_iters == sol.report.outer_iters)
     res["lambda_rel"] = abs(sol.report.spectrum_used.lambda_min / r_o.lambda_min - 1)
     pc = p.pcg_solve(tol=1e-8, max_iter=5000)
     xp, rpcg = port.pcg_solve(o, tol=1e-8, max_iter=5000)

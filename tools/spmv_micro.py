@@ -13,10 +13,12 @@ p = cs.DeviceProblem.generate(a.stencil, a.n, a.n, a.n).set_precond("jacobi")
 n, mat = p.n_local, p.device_bytes
 v = 8 * n
 res = {}
+print(f"format: slices={p.slices} pattern={p.pattern_slices} uniform={p.uniform_slices} "
+      f"table_entries={p.pattern_entries} bytes={mat}")
 for kind, byts in (("plain", mat + 2 * v), ("mpk_ref", mat + 7 * v), ("mpk_fast", mat + 5 * v),
                    ("pack8", 25 * v), ("update8", 54 * v)):
     ms = p.bench_spmv(kind, 20)
     res[kind] = (round(ms, 4), round(byts / (ms / 1e3) / 1e9))
 print(f"{os.environ.get('CS_LIB', 'default')} {a.stencil} {a.n}^3 mat {mat/p.nnz_local:.2f} B/nnz "
-      f"explicit={bool(os.environ.get('CS_SELL_EXPLICIT'))}: " +
+      f"explicit={bool(os.environ.get('CS_SELL_EXPLICIT'))} values={bool(os.environ.get('CS_SELL_VALUES'))}: " +
       " ".join(f"{k}={v[0]}ms/{v[1]}GB/s" for k, v in res.items()))

@@ -325,26 +325,48 @@ def run_ours(args):
     value = ng * args.steps / (t_max / 1e3) / 1e9
     ms_step = t_max / args.steps
 
-    # roofline of the dominant kernel (SpMV fused with the MPK epilogue)
+    # roofline per hot kernel family, the dominant one as "roofline"
     nnz_l = prob.nnz_local
     mat = prob.device_bytes
     alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode)
-    spmv_ms = phases["spmv"][0]
-    alg_t = sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps, args.mode)[0]
-                for r in reps_t)
-    achieved = alg_t / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
+    v8 = 8 * nl
+    outers_t = sum(r.outer_iters for r in reps_t)
+    alg_phase = {
+        "spmv": sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps,
+                                   args.mode)[0] for r in reps_t),
+        # Q, Z, AQ, P, x, r, D^-1 read; Q, AQ, x, r, z_0 written (one launch per outer)
+        "update": outers_t * v8 * (6 * args.s + 6),
+        # Q, Z, P, r read once (one launch per outer + the setup one)
+        "reduce": (outers_t + len(reps_t)) * v8 * (3 * args.s + 1),
+    }
+    names = {"spmv": "sell_kernel<kMpk*> (SELL-32PU FP64 SpMV + fused MPK epilogue)",
+             "update": "update_kernel<s,beta,xr,z0> (Q, AQ, x, r, z_0 update pass)",
+             "reduce": "pack_kernel<s> (packed Gram/projection block, DMMA)"}
     peak, peak_src = measured_peak()
-    tr = ncu_traffic()
-    roof = {"kernel": "sell_kernel<kMpk*> (SELL-32 FP64 SpMV + fused MPK epilogue)",
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak if achieved else None,
-            "traffic": tr.get("bytes_per_launch") if tr else None,
-            "traffic_alg_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
-            "peak_source": peak_src,
-            "spmv_share_of_step": spmv_ms / t_inst if t_inst > 0 else None,
+    tr = ncu_traffic() or {}
+    kern = {}
+    for ph, byts in alg_phase.items():
+        ms = phases[ph][0]
+        if ms <= 0:
+            continue
+        ach = byts / (ms / 1e3) / 1e9
+        t = tr.get(ph) or {}
+        kern[ph] = {"kernel": names[ph], "ms_per_solve": ms / len(reps_t),
+                    "share_of_step": ms / t_inst if t_inst > 0 else None,
+                    "achieved": ach, "frac": ach / peak,
+                    "alg_bytes_per_solve": byts / len(reps_t),
+                    "traffic": t.get("bytes_per_launch"),
+                    "traffic_alg_per_launch": t.get("alg_bytes_per_launch")}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_solve"])
+    d = kern[dom]
+    roof = {"kernel": d["kernel"], "bound": "hbm", "achieved": d["achieved"], "peak": peak,
+            "unit": "GB/s", "frac": d["frac"], "traffic": d["traffic"],
+            "traffic_alg_per_launch": d["traffic_alg_per_launch"], "peak_source": peak_src,
+            "share_of_step": d["share_of_step"],
             "measured": "CUDA events around every launch of K instrumented solves run right "
                         "after the timed region (instrumentation overhead %.1f%%)" %
                         (100 * (t_inst / t_ms - 1) if t_ms > 0 else 0),
+            "kernels": kern,
             "alg_bytes_per_spmv": b_spmv,
             "matrix_bytes": mat, "matrix_bytes_per_nnz": mat / nnz_l,
             "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}

@@ -283,21 +283,30 @@ __device__ __forceinline__ void halo_push_row(const SpmvArgs& g, int64_t row, do
   if (g.push_hi != nullptr && row >= g.hi_begin) g.push_hi[row - g.hi_begin] = z;
 }
 
-// producer side, per warp after its last row: publish the pushed row counts
-// (every lane fences its own remote stores, then lane 0 releases the counts)
+// producer side, once per block after its last row (every thread of the block
+// must call it): the block's pushed row counts are summed in shared memory and
+// thread 0 publishes them with one release reduction per peer. The barrier
+// orders every thread's remote stores before that release (cumulativity), so
+// no per-thread system fence is needed: __threadfence_system() would be
+// MEMBAR.SC.SYS + CCTL.IVALL, which also wipes the SM's L1 under the SpMV.
 __device__ __forceinline__ void halo_signal(const SpmvArgs& g, unsigned long long cnt_lo,
-                                            unsigned long long cnt_hi, int lane) {
+                                            unsigned long long cnt_hi) {
+  __shared__ unsigned long long blk_cnt[2];
+  if (threadIdx.x == 0) blk_cnt[0] = blk_cnt[1] = 0ull;
+  __syncthreads();
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     cnt_lo += __shfl_xor_sync(0xffffffffu, cnt_lo, off);
     cnt_hi += __shfl_xor_sync(0xffffffffu, cnt_hi, off);
   }
-  if (cnt_lo == 0 && cnt_hi == 0) return;  // warp-uniform after the butterfly
-  __threadfence_system();
-  __syncwarp();
-  if (lane == 0) {
-    if (cnt_lo) red_release_sys(g.sig_lo, cnt_lo);
-    if (cnt_hi) red_release_sys(g.sig_hi, cnt_hi);
+  if ((threadIdx.x & 31) == 0 && (cnt_lo | cnt_hi)) {
+    atomicAdd(&blk_cnt[0], cnt_lo);
+    atomicAdd(&blk_cnt[1], cnt_hi);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blk_cnt[0]) red_release_sys(g.sig_lo, blk_cnt[0]);
+    if (blk_cnt[1]) red_release_sys(g.sig_hi, blk_cnt[1]);
   }
 }
 
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(256) halo_push_kernel(SpmvArgs g, const double
       ++ch;
     }
   }
-  halo_signal(g, cl, ch, threadIdx.x & 31);
+  halo_signal(g, cl, ch);
 }
 
 // ------------------------------------------------------------------ LDG kernel
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(kWarps * 32, UNI ? CS_SPMV_UNI_MINB : CS_SPMV_
     sm = next;
   }
   if constexpr (kPush)
-    if (push) halo_signal(g, cnt_lo, cnt_hi, lane);
+    if (push) halo_signal(g, cnt_lo, cnt_hi);
   if constexpr (KIND == kDot) dot_finish(g, dotv);
 }
 

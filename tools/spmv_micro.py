@@ -8,6 +8,8 @@ import paper_2603_09790_b200 as cs  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=256)
 ap.add_argument("--stencil", default="poisson27")
+ap.add_argument("--kinds", default="plain,mpk_ref,mpk_fast,pack8,update8")
+ap.add_argument("--reps", type=int, default=20)
 a = ap.parse_args()
 p = cs.DeviceProblem.generate(a.stencil, a.n, a.n, a.n).set_precond("jacobi")
 n, mat = p.n_local, p.device_bytes
@@ -17,7 +19,9 @@ print(f"format: slices={p.slices} pattern={p.pattern_slices} uniform={p.uniform_
       f"table_entries={p.pattern_entries} bytes={mat}")
 for kind, byts in (("plain", mat + 2 * v), ("mpk_ref", mat + 7 * v), ("mpk_fast", mat + 5 * v),
                    ("pack8", 25 * v), ("update8", 54 * v)):
-    ms = p.bench_spmv(kind, 20)
+    if kind not in a.kinds.split(","):
+        continue
+    ms = p.bench_spmv(kind, a.reps)
     res[kind] = (round(ms, 4), round(byts / (ms / 1e3) / 1e9))
 print(f"{os.environ.get('CS_LIB', 'default')} {a.stencil} {a.n}^3 mat {mat/p.nnz_local:.2f} B/nnz "
       f"explicit={bool(os.environ.get('CS_SELL_EXPLICIT'))} values={bool(os.environ.get('CS_SELL_VALUES'))}: " +

@@ -64,6 +64,32 @@ __host__ __device__ inline int64_t make_pat_meta(int64_t idx, int uniform_slots)
   return -((static_cast<int64_t>(uniform_slots) << kPatShift) | idx) - 1;
 }
 
+// Uniform-table slot {offset, lane mask, value} (16 bytes; SELL-32PU tables).
+struct __align__(16) SlotRec {
+  int off;
+  unsigned mask;
+  double v;
+};
+
+// Constant-diagonal classes ("CDIA"): when every slice of a
+// contiguous slice range [s0, s1) is uniform-value and the union of their
+// tables has <= 32 relative offsets, each carrying ONE value, the range is a
+// constant-coefficient stencil in relative-offset space (the DIA format with
+// constant diagonals). Its table {off_j, v_j} (sorted by offset) travels as a
+// kernel parameter -- every access is an immediate constant-bank operand -- and
+// each row keeps only a 32-bit participation word (bit j: the row has an entry
+// at off_j). Rows visit their entries in ascending offset = stored column order.
+constexpr int kCdiaMax = 32;
+struct CdiaTable {
+  int n;
+  int off[kCdiaMax];
+  double v[kCdiaMax];
+};
+struct CdiaClass {  // host side
+  int64_t s0, s1;
+  CdiaTable t;
+};
+
 struct SellView {
   int64_t n_local;
   int64_t nslices;
@@ -78,6 +104,9 @@ struct SellView {
   int uniform;                          // nonzero: some slices are uniform-value
   int uniform_all;                      // nonzero: every slice is uniform-value
   int64_t table_entries;                // uniform tables occupy pat/pval[0, table_entries)
+  const uint32_t* pbits;                // CDIA participation words (device), or nullptr
+  const CdiaClass* cdia;                // CDIA classes (HOST pointer; launchers only)
+  int ncdia;
 };
 
 __host__ __device__ inline unsigned long long make_err(int code, int payload) {

@@ -57,6 +57,10 @@ void launch_table_assign(int64_t n, const unsigned long long* key, const int32_t
                          const int64_t* headpos, const int64_t* tab_ptr, int64_t* slice_tab,
                          int32_t* slice_rep, cudaStream_t st);
 void launch_iota_i32(int64_t n, int32_t* out, cudaStream_t st);
+// CDIA participation words (see CdiaClass); *bad = 1 if a table offset is missing
+void launch_cdia_bits(int64_t nslices, int ncls, const int64_t* starts, const int32_t* offs,
+                      const int32_t* nofs, const int64_t* meta, const int2* pat, uint32_t* bits,
+                      int* bad, cudaStream_t st);
 void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
                           const double* vals, const int64_t* kind, const int64_t* slice_tab,
                           const int32_t* slice_rep, const int64_t* new_ptr, const int64_t* pat_ptr,

@@ -1,6 +1,8 @@
 // runtime.cu -- device context, device-resident problems, halo exchange,
 // collectives and launch/timing accounting.
 #include <algorithm>
+#include <cmath>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -426,6 +428,102 @@ int64_t read_i64(cs_ctx* c, const int64_t* dev) {
 
 // Convert the freshly assembled explicit SELL-32 into SELL-32P (common.cuh):
 // pattern-compressed slices drop their 4 B/slot column stream.
+// Constant-diagonal classes over an all-uniform matrix (see CdiaClass): greedy
+// left-to-right merge of consecutive slices' tables while the union stays
+// <= 32 offsets with one value each; then per-row participation words.
+void build_cdia(cs_problem* p) {
+  cs_ctx* c = p->ctx;
+  p->cdia.clear();
+  p->pbits.release();
+  const int64_t ns = p->nslices;
+  const char* env = std::getenv("CS_SELL_CDIA");
+  if (ns == 0 || p->uniform_slices != ns || (env && std::atoi(env) == 0)) return;
+  std::vector<int64_t> meta(ns);
+  std::vector<int2> pat(p->table_entries);
+  std::vector<double> pval(p->table_entries);
+  CS_CUDA(cudaMemcpyAsync(meta.data(), p->meta.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost,
+                          c->stream));
+  CS_CUDA(cudaMemcpyAsync(pat.data(), p->pat.p, sizeof(int2) * pat.size(), cudaMemcpyDeviceToHost,
+                          c->stream));
+  CS_CUDA(cudaMemcpyAsync(pval.data(), p->pval.p, sizeof(double) * pval.size(),
+                          cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  constexpr int kMaxClasses = 64;
+  std::vector<CdiaClass> cls;
+  std::vector<std::pair<int, double>> cur;  // sorted by offset
+  int64_t s0 = 0, last_tab = -1;
+  auto flush = [&](int64_t s1) {
+    CdiaClass k{};
+    k.s0 = s0;
+    k.s1 = s1;
+    k.t.n = static_cast<int>(cur.size());
+    for (size_t j = 0; j < cur.size(); ++j) {
+      k.t.off[j] = cur[j].first;
+      k.t.v[j] = cur[j].second;
+    }
+    cls.push_back(k);
+  };
+  for (int64_t sl = 0; sl < ns; ++sl) {
+    const int64_t ti = pat_index(meta[sl]);
+    if (ti == last_tab) continue;  // same table as the previous slice
+    const int U = pat_uniform(meta[sl]);
+    std::vector<std::pair<int, double>> merged = cur;
+    bool ok = true;
+    for (int k = 0; k < U && ok; ++k) {
+      const int off = pat[ti + k].x;
+      const double v = pval[ti + k];
+      auto it = std::lower_bound(merged.begin(), merged.end(), std::make_pair(off, -HUGE_VAL),
+                                 [](const auto& a, const auto& b) { return a.first < b.first; });
+      if (it != merged.end() && it->first == off) {
+        if (std::memcmp(&it->second, &v, sizeof v) != 0) ok = false;  // bitwise
+      } else {
+        merged.insert(it, {off, v});
+      }
+    }
+    if (ok && merged.size() <= static_cast<size_t>(kCdiaMax)) {
+      cur.swap(merged);
+    } else {
+      if (U > kCdiaMax) return;  // one table alone does not fit
+      flush(sl);
+      if (static_cast<int>(cls.size()) >= kMaxClasses) return;
+      s0 = sl;
+      cur.clear();
+      for (int k = 0; k < U; ++k) cur.push_back({pat[ti + k].x, pval[ti + k]});
+    }
+    last_tab = ti;
+  }
+  flush(ns);
+  // participation words on the device
+  std::vector<int64_t> starts(cls.size());
+  std::vector<int32_t> offs(cls.size() * kCdiaMax, 0);
+  std::vector<int32_t> nofs(cls.size());
+  for (size_t k = 0; k < cls.size(); ++k) {
+    starts[k] = cls[k].s0;
+    nofs[k] = cls[k].t.n;
+    for (int j = 0; j < cls[k].t.n; ++j) offs[k * kCdiaMax + j] = cls[k].t.off[j];
+  }
+  DBuf d_starts(sizeof(int64_t) * starts.size()), d_offs(sizeof(int32_t) * offs.size()),
+      d_n(sizeof(int32_t) * nofs.size());
+  CS_CUDA(cudaMemcpyAsync(d_starts.p, starts.data(), d_starts.bytes, cudaMemcpyHostToDevice,
+                          c->stream));
+  CS_CUDA(cudaMemcpyAsync(d_offs.p, offs.data(), d_offs.bytes, cudaMemcpyHostToDevice, c->stream));
+  CS_CUDA(cudaMemcpyAsync(d_n.p, nofs.data(), d_n.bytes, cudaMemcpyHostToDevice, c->stream));
+  p->pbits.alloc(sizeof(uint32_t) * ns * kSliceRows);
+  DBuf bad(sizeof(int));
+  CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  launch_cdia_bits(ns, static_cast<int>(cls.size()), d_starts.as<int64_t>(), d_offs.as<int32_t>(),
+                   d_n.as<int32_t>(), p->meta.as<int64_t>(), p->pat.as<int2>(),
+                   p->pbits.as<uint32_t>(), bad.as<int>(), c->stream);
+  int hbad = 0;
+  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  if (hbad) {
+    p->pbits.release();
+    return;
+  }
+  p->cdia = std::move(cls);
+}
+
 void compress_sell(cs_problem* p, int dedupe = 1) {
   cs_ctx* c = p->ctx;
   const int64_t ns = p->nslices;
@@ -531,6 +629,7 @@ void compress_sell(cs_problem* p, int dedupe = 1) {
   p->pattern_entries = npat;
   p->table_entries = ntab;
   p->max_width = static_cast<int>(wmax);
+  build_cdia(p);
 }
 
 }  // namespace

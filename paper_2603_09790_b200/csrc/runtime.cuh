@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <array>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -128,7 +129,8 @@ struct cs_problem {
   }
   int gen_kind = -1;
   int64_t nx = 0, ny = 0, nz = 0;
-  csg::DBuf slice_ptr, vals, cols, meta, pat, pval, diag, inv_diag, ghost_global;
+  csg::DBuf slice_ptr, vals, cols, meta, pat, pval, pbits, diag, inv_diag, ghost_global;
+  std::vector<csg::CdiaClass> cdia;
   int64_t compressed_slices = 0, uniform_slices = 0, pattern_entries = 0, table_entries = 0;
   int max_width = 0;
   std::vector<int64_t> ghosts_host;
@@ -165,6 +167,9 @@ struct cs_problem {
     v.uniform = uniform_slices > 0;
     v.uniform_all = uniform_slices == nslices && nslices > 0;
     v.table_entries = table_entries;
+    v.pbits = cdia.empty() ? nullptr : pbits.as<uint32_t>();
+    v.cdia = cdia.data();
+    v.ncdia = static_cast<int>(cdia.size());
     v.max_width = max_width;
     v.inv_diag = precond == CS_PRECOND_JACOBI ? inv_diag.as<double>() : nullptr;
     return v;

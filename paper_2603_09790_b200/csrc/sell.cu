@@ -668,6 +668,52 @@ void launch_compress_verify(int64_t nslices, const int64_t* slice_ptr, const int
   CS_CUDA(cudaGetLastError());
 }
 
+// CDIA participation words: per slice (one warp), its class by binary search
+// over the class starts, then every table entry's offset located in the
+// class's sorted offsets; lane l collects bit j for each entry it holds.
+__global__ void cdia_bits_kernel(int64_t nslices, int ncls, const int64_t* __restrict__ starts,
+                                 const int32_t* __restrict__ offs, const int32_t* __restrict__ nofs,
+                                 const int64_t* __restrict__ meta, const int2* __restrict__ pat,
+                                 uint32_t* bits, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (slice >= nslices) return;
+  int lo = 0, hi = ncls - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (starts[mid] <= slice) lo = mid;
+    else hi = mid - 1;
+  }
+  const int32_t* co = offs + lo * kCdiaMax;
+  const int cn = nofs[lo];
+  const int64_t m = meta[slice];
+  const int64_t pi = pat_index(m);
+  const int U = pat_uniform(m);
+  uint32_t w = 0;
+  bool ok = true;
+  for (int k = 0; k < U; ++k) {
+    const int2 e = pat[pi + k];
+    int j = 0;
+    while (j < cn && co[j] != e.x) ++j;
+    if (j == cn) {
+      ok = false;
+      break;
+    }
+    if ((static_cast<unsigned>(e.y) >> lane) & 1u) w |= 1u << j;
+  }
+  if (!ok && lane == 0) atomicExch(bad, 1);
+  bits[slice * kSliceRows + lane] = w;
+}
+
+void launch_cdia_bits(int64_t nslices, int ncls, const int64_t* starts, const int32_t* offs,
+                      const int32_t* nofs, const int64_t* meta, const int2* pat, uint32_t* bits,
+                      int* bad, cudaStream_t st) {
+  if (nslices == 0) return;
+  cdia_bits_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(nslices, ncls, starts, offs, nofs,
+                                                                meta, pat, bits, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
 __global__ void iota_i32_kernel(int64_t n, int32_t* out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = static_cast<int32_t>(i);

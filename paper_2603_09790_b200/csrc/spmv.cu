@@ -33,8 +33,11 @@ constexpr int kWarps = 8;  // warps per 256-thread block
 #ifndef CS_SPMV_MINB
 #define CS_SPMV_MINB 8  // 32 registers: full occupancy (64 warps / SM)
 #endif
-#ifndef CS_SPMV_UNI_MINB
-#define CS_SPMV_UNI_MINB 6  // uniform-table kernel: 40 registers, 48 warps / SM
+#ifndef CS_CD_KB
+#define CS_CD_KB 9  // CDIA gathers in flight per batch
+#endif
+#ifndef CS_SPMV_CD_MINB
+#define CS_SPMV_CD_MINB 4  // CDIA kernel: 64 registers (all x gathers of a row in flight)
 #endif
 #ifndef CS_SPMV_PERSIST
 #define CS_SPMV_PERSIST 1
@@ -64,13 +67,7 @@ __device__ __forceinline__ SliceMeta load_meta(const SellView& a, int64_t slice,
   return m;
 }
 
-// Uniform-table slot staged in shared memory: one 16-byte broadcast load per slot.
-struct __align__(16) SlotRec {
-  int off;
-  unsigned mask;
-  double v;
-};
-constexpr int kStabMax = 1024;  // staged table entries per block (16 KB)
+constexpr int kStabMax = 1024;  // uniform-table entries staged per block (16 KB)
 
 __device__ __forceinline__ int stage_tables(const SellView& a, SlotRec* stab) {
   const int staged = a.table_entries < kStabMax ? static_cast<int>(a.table_entries) : kStabMax;
@@ -83,22 +80,60 @@ __device__ __forceinline__ int stage_tables(const SellView& a, SlotRec* stab) {
 }
 
 // One row of one slice: sum_k v_k * x[c_k] in stored order, acc = acc + v*x.
-template <bool UNI>
+// CDIA row: the class table is a kernel parameter, so t.off[k] / t.v[k] are
+// immediate constant-bank operands of the unrolled loop (no table loads at all;
+// ncu showed shared-memory table broadcasts costing as many L1 wavefronts as
+// the x gathers, and register-indexed constant loads saturating the ADU pipe).
+// N > 0: the class has exactly N offsets (compile time: no per-slot bound
+// tests; the common stencils, 7 and 27). N == 0: runtime t.n.
+// Gathers are issued in batches of kB (a batch's loads in flight together),
+// then the batch's products are added in slot order. Slices whose 32 rows all
+// hold every entry (a stencil's interior) skip the per-slot predicates; bits at
+// or above t.n are zero by construction.
+template <int N>
+__device__ __forceinline__ double row_sum_cdia(const CdiaTable& t, const double* __restrict__ x,
+                                               int r32, uint32_t bits) {
+  constexpr int kB = N > 0 ? (CS_CD_KB < N ? CS_CD_KB : N) : 8;
+  constexpr int kMax = N > 0 ? N : kCdiaMax;
+  const int n = N > 0 ? N : t.n;
+  double acc = 0.0;
+  const uint32_t full = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+  if (__all_sync(0xffffffffu, bits == full)) {
+#pragma unroll
+    for (int c = 0; c < kMax; c += kB) {
+      if (N == 0 && c >= n) break;
+      double xv[kB];
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        if (c + j < kMax && (N > 0 || c + j < n)) xv[j] = __ldg(x + (r32 + t.off[c + j]));
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        if (c + j < kMax && (N > 0 || c + j < n))
+          acc = __dadd_rn(acc, __dmul_rn(t.v[c + j], xv[j]));
+    }
+    return acc;
+  }
+#pragma unroll
+  for (int c = 0; c < kMax; c += kB) {
+    if (N == 0 && c >= n) break;
+    double xv[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const bool on = c + j < kMax && ((bits >> (c + j)) & 1u);
+      xv[j] = on ? __ldg(x + (r32 + t.off[c + j])) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j)
+      if (c + j < kMax && ((bits >> (c + j)) & 1u))
+        acc = __dadd_rn(acc, __dmul_rn(t.v[c + j], xv[j]));
+  }
+  return acc;
+}
+
 __device__ __forceinline__ double row_sum(const SellView& a, const double* __restrict__ x,
                                           const SliceMeta& sm, int64_t row, int lane,
                                           const SlotRec* stab, int staged) {
   double acc = 0.0;
-  if constexpr (UNI) {  // every slice uniform, every table staged (host-checked)
-    const SlotRec* t = stab + pat_index(sm.meta);
-    const int U = pat_uniform(sm.meta);
-    const double* xr = x + row;
-#pragma unroll 9
-    for (int k = 0; k < U; ++k) {
-      const SlotRec e = t[k];
-      if ((e.mask >> lane) & 1u) acc = __dadd_rn(acc, __dmul_rn(e.v, __ldg(xr + e.off)));
-    }
-    return acc;
-  }
   const int width = static_cast<int>((sm.end - sm.base) >> 5);
   const double* vp = a.vals + sm.base + lane;
   if (sm.meta >= 0) {  // explicit int32 columns
@@ -338,9 +373,10 @@ __global__ void __launch_bounds__(256) halo_push_kernel(SpmvArgs g, const double
 // Persistent warps walk slices with a grid stride; the next slice's metadata
 // and the epilogue operands of the current rows are loaded ahead of the row
 // sums so that their latency overlaps the value/x stream.
-template <int KIND, bool JAC, bool UNI>
-__global__ void __launch_bounds__(kWarps * 32, UNI ? CS_SPMV_UNI_MINB : CS_SPMV_MINB)
-    sell_kernel(SellView a, SpmvArgs g, int64_t slice_begin, int64_t slice_end) {
+template <int KIND, bool JAC, int CDN>
+__global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_SPMV_MINB)
+    sell_kernel(SellView a, SpmvArgs g, int64_t slice_begin, int64_t slice_end,
+                const __grid_constant__ CdiaTable t) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
   if (g.wait_ctr != nullptr) {
     if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
@@ -352,22 +388,35 @@ __global__ void __launch_bounds__(kWarps * 32, UNI ? CS_SPMV_UNI_MINB : CS_SPMV_
   constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
   unsigned long long cnt_lo = 0, cnt_hi = 0;
-  __shared__ SlotRec stab[kStabMax];
-  const int staged = a.uniform ? stage_tables(a, stab) : 0;
+  constexpr bool CD = CDN != 0;
+  __shared__ SlotRec stab[CD ? 1 : kStabMax];
+  const int staged = !CD && a.uniform ? stage_tables(a, stab) : 0;
   // virtual slice indices past nslices wrap to the start, so [ie, nslices + ib)
   // covers both boundary ranges of a halo'd SpMV in one launch
   const auto phys = [&](int64_t v) { return v >= a.nslices ? v - a.nslices : v; };
+  // The next slice's metadata (table path) or participation word (CDIA path:
+  // ncu put 20% of the stall samples on the first test of a just-loaded word)
+  // is loaded one iteration ahead, so its latency overlaps this slice.
   int64_t slice = slice_begin + static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   double dotv = 0.0;
-  SliceMeta sm = load_meta<UNI>(a, phys(slice), slice < slice_end ? a.nslices : 0);
+  SliceMeta sm{};
+  uint32_t bits = 0;
+  if constexpr (!CD) sm = load_meta(a, phys(slice), slice < slice_end ? a.nslices : 0);
+  else if (slice < slice_end) bits = __ldcs(a.pbits + phys(slice) * kSliceRows + lane);
   for (; slice < slice_end; slice += wstride) {
     const int64_t vn = slice + wstride;
-    const SliceMeta next = load_meta<UNI>(a, phys(vn), vn < slice_end ? a.nslices : 0);
+    SliceMeta next{};
+    uint32_t bits_next = 0;
+    if constexpr (!CD) next = load_meta(a, phys(vn), vn < slice_end ? a.nslices : 0);
+    else if (vn < slice_end) bits_next = __ldcs(a.pbits + phys(vn) * kSliceRows + lane);
     const int64_t row = phys(slice) * kSliceRows + lane;
     const bool own = row < a.n_local;
     EpiOps e;
     if (own) e = epi_load<KIND, JAC>(a, g, row);
-    const double acc = row_sum<UNI>(a, g.x, sm, row, lane, stab, staged);
+    double acc;
+    if constexpr (CD)
+      acc = row_sum_cdia<(CDN > 0 ? CDN : 0)>(t, g.x, static_cast<int>(row), bits);
+    else acc = row_sum(a, g.x, sm, row, lane, stab, staged);
     if (own) {
       double zv = 0.0;
       epi_store<KIND, JAC>(g, row, acc, e, dotv, zv);
@@ -380,6 +429,7 @@ __global__ void __launch_bounds__(kWarps * 32, UNI ? CS_SPMV_UNI_MINB : CS_SPMV_
       }
     }
     sm = next;
+    bits = bits_next;
   }
   if constexpr (kPush)
     if (push) halo_signal(g, cnt_lo, cnt_hi);
@@ -520,11 +570,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #define CS_SPMV_TMA 0  // measured slower on B200 (16 warps/SM at 128 regs); DESIGN.md 3
 #endif
 
-int spmv_grid(int64_t nslices, bool uni = false) {
+int spmv_grid(int64_t nslices, bool cd = false) {
   const int64_t want = (nslices + kWarps - 1) / kWarps;
   if (!CS_SPMV_PERSIST) return static_cast<int>(want > 0 ? want : 1);
   // one wave of resident blocks at the kernel's occupancy
-  const int64_t cap = 148 * (uni ? CS_SPMV_UNI_MINB : CS_SPMV_MINB);
+  const int64_t cap = 148 * (cd ? CS_SPMV_CD_MINB : CS_SPMV_MINB);
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
@@ -559,15 +609,38 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
     else tma_launch<KIND, false>(a, g, sb, se, st);
     return;
   }
-  const bool uni = a.uniform && a.uniform_all && a.table_entries <= kStabMax;
-  const unsigned grid = static_cast<unsigned>(spmv_grid(se - sb, uni));
-  if (uni) {
-    if (jac) sell_kernel<KIND, true, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
-    else sell_kernel<KIND, false, true><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
-  } else {
-    if (jac) sell_kernel<KIND, true, false><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
-    else sell_kernel<KIND, false, false><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se);
+  // CDIA: one launch per (class x physical range) piece; kDot finalises one sum
+  // per launch, so a multi-piece kDot takes the table kernel instead
+  if (a.ncdia > 0) {
+    int64_t piece[2][2] = {{sb, se < a.nslices ? se : a.nslices}, {0, se - a.nslices}};
+    int count = 0;
+    for (auto& r : piece)
+      for (int k = 0; k < a.ncdia; ++k)
+        count += std::max(r[0], a.cdia[k].s0) < std::min(r[1], a.cdia[k].s1);
+    if (KIND != kDot || count == 1) {
+      for (auto& r : piece)
+        for (int k = 0; k < a.ncdia; ++k) {
+          const int64_t lo = std::max(r[0], a.cdia[k].s0), hi = std::min(r[1], a.cdia[k].s1);
+          if (lo >= hi) continue;
+          const unsigned grid = static_cast<unsigned>(spmv_grid(hi - lo, true));
+          const CdiaTable& t = a.cdia[k].t;
+#define CSG_CD(N)                                                                        \
+  do {                                                                                   \
+    if (jac) sell_kernel<KIND, true, N><<<grid, kWarps * 32, 0, st>>>(a, g, lo, hi, t);  \
+    else sell_kernel<KIND, false, N><<<grid, kWarps * 32, 0, st>>>(a, g, lo, hi, t);     \
+  } while (0)
+          if (t.n == 27) CSG_CD(27);
+          else if (t.n == 7) CSG_CD(7);
+          else CSG_CD(-1);
+#undef CSG_CD
+        }
+      return;
+    }
   }
+  const unsigned grid = static_cast<unsigned>(spmv_grid(se - sb));
+  const CdiaTable none{};
+  if (jac) sell_kernel<KIND, true, 0><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se, none);
+  else sell_kernel<KIND, false, 0><<<grid, kWarps * 32, 0, st>>>(a, g, sb, se, none);
 }
 
 }  // namespace

@@ -135,7 +135,8 @@ def nnz_of(stencil, nx, ny, nz):
     return n + 2 * ((nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1))
 
 
-def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=True):
+def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=True,
+                   diag_stream=True):
     """Algorithmic bytes of every SpMV-phase kernel of one solve:
     the matrix in the format actually stored (SELL-32P: FP64 value slots +
     per-slice column/pattern/meta bytes) read once, x read once, each output
@@ -144,7 +145,7 @@ def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=Tr
     b_spmv = mat_bytes + 2 * v                       # y = A x
     b_resid = mat_bytes + 3 * v                      # r = b - A x
     b_dot = mat_bytes + 2 * v                        # Lanczos t = A v (+ v.t)
-    j = v if jacobi else 0                           # D^-1 read by the epilogue
+    j = v if jacobi and diag_stream else 0          # D^-1 read by the epilogue
     if mode == "fast":                               # z_q = 2a D^-1 p_q - 2s z_{q-1} - z_{q-2}
         b_first = mat_bytes + 3 * v + j              # x, p, z (+ D^-1)
         b_mid = mat_bytes + 4 * v + j                # x, p, z_{q-2}, z (+ D^-1)
@@ -157,13 +158,14 @@ def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=Tr
     return b_resid + lanczos_steps * b_dot + mpks * per_mpk, b_spmv
 
 
-def outer_bytes_format(mat_bytes, n, s):
+def outer_bytes_format(mat_bytes, n, s, diag_stream=True):
     """Per-outer algorithmic bytes of the fast schedule in the stored format:
-    s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+5)."""
+    s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+6)."""
     v = 8 * n
-    mpk = (mat_bytes + 4 * v) + (s - 2) * (mat_bytes + 5 * v) + (mat_bytes + 2 * v) if s > 1 \
-        else mat_bytes + 2 * v
-    return mpk + v * (3 * s + 1) + v * (6 * s + 5)
+    j = v if diag_stream else 0
+    mpk = (mat_bytes + 3 * v + j) + (s - 2) * (mat_bytes + 4 * v + j) + (mat_bytes + 2 * v) \
+        if s > 1 else mat_bytes + 2 * v
+    return mpk + v * (3 * s + 1) + v * (6 * s + 6)
 
 
 def outer_bytes(nnz, n, s):
@@ -328,12 +330,14 @@ def run_ours(args):
     # roofline per hot kernel family, the dominant one as "roofline"
     nnz_l = prob.nnz_local
     mat = prob.device_bytes
-    alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode)
+    dstream = not prob.cdia_uniform_diag  # CDIA: 1/a_ii is a kernel constant
+    alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode,
+                                 diag_stream=dstream)
     v8 = 8 * nl
     outers_t = sum(r.outer_iters for r in reps_t)
     alg_phase = {
         "spmv": sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps,
-                                   args.mode)[0] for r in reps_t),
+                                   args.mode, diag_stream=dstream)[0] for r in reps_t),
         # Q, Z, AQ, P, x, r, D^-1 read; Q, AQ, x, r, z_0 written (one launch per outer)
         "update": outers_t * v8 * (6 * args.s + 6),
         # Q, Z, P, r read once (one launch per outer + the setup one)
@@ -372,7 +376,7 @@ def run_ours(args):
             "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}
     # whole-solve bandwidth against B_outer
     solve_outer_ms = rep.t_solve_ms / max(rep.outer_iters, 1)
-    b_out = outer_bytes_format(mat, nl, args.s)
+    b_out = outer_bytes_format(mat, nl, args.s, dstream)
     b_survey = outer_bytes(nnz_l, nl, args.s)
     solve_level = {"t_outer_ms": solve_outer_ms, "B_outer_GB": b_out / 1e9,
                    "achieved_GBps": b_out / (solve_outer_ms / 1e3) / 1e9,
@@ -402,6 +406,8 @@ def run_ours(args):
                                          "pattern_slices": prob.pattern_slices,
                                          "uniform_value_slices": prob.uniform_slices,
                                          "table_entries": prob.pattern_entries,
+                                         "cdia_classes": prob.cdia_classes,
+                                         "cdia_uniform_diag": bool(prob.cdia_uniform_diag),
                                          "bytes": prob.device_bytes}},
             "gpu_launches": launches,
             "roofline": roof,

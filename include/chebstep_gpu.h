@@ -224,10 +224,11 @@ int cs_problem_upload_csr_block(cs_ctx* ctx, int64_t n_global, int64_t row_begin
  * its cs_partition_rows(n, 1, nranks, rank) block and uploads it (collective). */
 int cs_problem_read_mm(cs_ctx* ctx, const char* path, int require_spd, cs_problem** out);
 int cs_problem_destroy(cs_problem* p);
-/* info10: n_global, n_local, nnz_local, row_begin, n_ghost, device bytes of the
+/* info12: n_global, n_local, nnz_local, row_begin, n_ghost, device bytes of the
  * SELL arrays, slices, pattern-compressed slices, uniform-value slices, pattern
- * table entries (format) */
-int cs_problem_info(cs_problem* p, int64_t* info10);
+ * table entries, constant-diagonal (CDIA) classes, 1 if every CDIA class has a
+ * uniform diagonal (format) */
+int cs_problem_info(cs_problem* p, int64_t* info12);
 /* Local rows back as CSR with GLOBAL column indices (bit-exact assembly check). */
 int cs_problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val);
 /* Ghost global column list of this rank (n_ghost entries). */
@@ -262,6 +263,10 @@ int cs_estimate_interval(cs_problem* p, int steps, uint64_t seed, int mode, doub
  * (reference recurrence), 2 = fused MPK middle step (fast recurrence),
  * 3 = packed one-allreduce reduction (s = 8), 4 = fused update pass (s = 8).
  * Average ms per launch. */
+/* Kernel micro-benchmarks (CUDA events, ms per launch): 0 SpMV, 1 reference MPK
+ * step, 2 fast MPK step, 3 packed reduction (s=8), 4 update pass (s=8); multi-GPU
+ * (collective, after one solve): 5 peer-memory z_0 push, 6 fast MPK step through
+ * the peer-memory halo. */
 int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch);
 
 /* ------------------------------------------------------------ solves */

@@ -246,11 +246,11 @@ class DeviceProblem:
 
     def __init__(self, ctx: Context, handle):
         self.ctx, self.handle = ctx, handle
-        info = np.zeros(10, np.int64)
+        info = np.zeros(12, np.int64)
         _check(lib.cs_problem_info(handle, info))
         (self.n_global, self.n_local, self.nnz_local, self.row_begin, self.n_ghost,
          self.device_bytes, self.slices, self.pattern_slices, self.uniform_slices,
-         self.pattern_entries) = (int(v) for v in info)
+         self.pattern_entries, self.cdia_classes, self.cdia_uniform_diag) = (int(v) for v in info)
         self.precond = "identity"
 
     @property
@@ -364,7 +364,8 @@ class DeviceProblem:
 
     def bench_spmv(self, kind: str = "plain", reps: int = 20) -> float:
         """Average ms of one SpMV-family launch timed alone (CUDA events)."""
-        k = {"plain": 0, "mpk_ref": 1, "mpk_fast": 2, "pack8": 3, "update8": 4}[kind]
+        k = {"plain": 0, "mpk_ref": 1, "mpk_fast": 2, "pack8": 3, "update8": 4,
+             "p2p_push": 5, "p2p_mpk": 6}[kind]
         ms = C.c_double()
         _check(lib.cs_bench_spmv(self.handle, k, reps, C.byref(ms)))
         return ms.value

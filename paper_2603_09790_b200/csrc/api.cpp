@@ -327,7 +327,7 @@ namespace {
 PoissonSystem generated(int kind, const PoissonSpec& spec, const double* coef) {
   cs_problem* p = nullptr;
   check(cs_problem_generate(ctx(), kind, spec.nx, spec.ny, spec.nz, coef, &p));
-  int64_t info[10];
+  int64_t info[12];
   cs_problem_info(p, info);
   PoissonSystem sys;
   sys.a.n = info[1];
@@ -676,7 +676,7 @@ SolveResult pcg_solve(const CsrMatrix& a, std::span<const double> b, std::span<c
 namespace gpu {
 
 DeviceProblem::DeviceProblem(cs_problem* p) : p_(p) {
-  int64_t info[10];
+  int64_t info[12];
   check(cs_problem_info(p_, info));
   n_global_ = info[0], n_local_ = info[1], nnz_local_ = info[2], row_begin_ = info[3];
 }

@@ -336,12 +336,16 @@ int cs_problem_info(cs_problem* p, int64_t* info) {
     info[2] = p->nnz_local;
     info[3] = p->row_begin;
     info[4] = p->n_ghost;
-    info[5] = static_cast<int64_t>(p->vals.bytes + p->cols.bytes + p->pat.bytes + p->pval.bytes +
+    info[5] = static_cast<int64_t>(p->vals.bytes + p->cols.bytes + p->pat.bytes + p->pval.bytes + p->pkey.bytes + p->pbits.bytes +
                                    p->meta.bytes + p->slice_ptr.bytes);
     info[6] = p->nslices;
     info[7] = p->compressed_slices;
     info[8] = p->uniform_slices;
     info[9] = p->pattern_entries;
+    info[10] = static_cast<int64_t>(p->cdia.size());
+    bool ud = !p->cdia.empty();
+    for (const auto& k : p->cdia) ud = ud && k.t.diag != 0.0;
+    info[11] = ud ? 1 : 0;
   });
 }
 
@@ -389,12 +393,65 @@ int cs_spmv(cs_problem* p, const double* x, double* y) {
   });
 }
 
+namespace {
+// kind 5: the z_0 push kernel alone; kind 6: one fast-MPK middle step through the
+// peer-memory halo (interior + release, wait + boundary). Both on the solve
+// workspace's Z columns, with the exchange re-armed by p2p_setup (collective).
+void bench_p2p(cs_problem* p, int kind, int reps, double* ms) {
+  cs_ctx* c = p->ctx;
+  if (p->ws.p == nullptr || p->ws_s < 2) fail(CS_ERR_INVALID_ARGUMENT, 0, "run a solve first");
+  const int64_t ld = p->ld;
+  double* Z = p->ws.as<double>() + 2 * p->ws_s * ld;  // workspace(): Q, AQ, Z, P, ...
+  if (!p2p_setup(p, Z)) fail(CS_ERR_INVALID_ARGUMENT, 0, "peer-memory halo unavailable");
+  std::function<void()> run;
+  SpmvArgs g;
+  if (kind == 5) {
+    run = [&] {
+      Launch L(c, CS_PHASE_COMM);
+      SpmvArgs a;
+      fill_push_args(p, a, 0);
+      launch_halo_push(a, Z, p->n_local, nullptr, c->stream);
+    };
+  } else {
+    g.x = Z;
+    g.y = Z + 3 * ld;  // scratch columns of the basis
+    g.zp2 = Z + ld;
+    g.zout = Z + 2 * ld;
+    g.ca = 1.0;
+    g.cb = -0.5;
+    g.cc = -1.0;
+    p2p_push(p, Z, 0, nullptr);  // epoch 1's ghost planes (the z_0 push of a solve)
+    run = [&] { spmv_p2p(p, kMpkMidF, g, 0); };
+  }
+  cudaEvent_t a, b;
+  CS_CUDA(cudaEventCreate(&a));
+  CS_CUDA(cudaEventCreate(&b));
+  run();
+  CS_CUDA(cudaEventRecord(a, c->stream));
+  for (int i = 0; i < reps; ++i) run();
+  CS_CUDA(cudaEventRecord(b, c->stream));
+  CS_CUDA(cudaEventSynchronize(b));
+  float t = 0.f;
+  CS_CUDA(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms = t / reps;
+  // leave no push unreleased / no stale epoch: re-arm (collective)
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  p2p_setup(p, Z);
+}
+}  // namespace
+
 int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
   return guard([&] {
     cs_ctx* c = p->ctx;
     CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
-    if (reps < 1 || kind < 0 || kind > 4) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad bench args");
+    if (reps < 1 || kind < 0 || kind > 6) fail(CS_ERR_INVALID_ARGUMENT, 0, "bad bench args");
+    if (kind >= 5) {  // multi-GPU halo transport probes (collective; after one solve)
+      bench_p2p(p, kind, reps, ms_per_launch);
+      return;
+    }
     const int64_t ld = p->ld, n = p->n_local;
     constexpr int S = 8;
     const int nvec = kind <= 2 ? 6 : 4 * S + 4;

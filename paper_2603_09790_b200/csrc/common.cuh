@@ -84,6 +84,8 @@ struct CdiaTable {
   int n;
   int off[kCdiaMax];
   double v[kCdiaMax];
+  double diag;  // every row of the class holds offset 0 with this value (else 0)
+  double inv;   // launch-time: 1.0 / diag for the Jacobi epilogue (else 0)
 };
 struct CdiaClass {  // host side
   int64_t s0, s1;

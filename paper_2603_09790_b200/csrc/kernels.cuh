@@ -41,9 +41,16 @@ void scan_rowptr(const int64_t* len, int64_t n, int64_t* rowptr, void* tmp, size
                  cudaStream_t st);
 // SELL-32 -> SELL-32P(U) conversion (see SellView): plan per-slice kinds, sizes
 // and uniform-table hashes; sort the hashes into shared tables; fill; verify.
+// Local -> global column map of a rank block (the merge key is the global
+// relative offset: rows store their entries in ascending global column order).
+struct ColMap {
+  int64_t row_begin, n_local;
+  const int64_t* ghost;  // ghost_global (device), n_ghost entries
+};
 void launch_compress_plan(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                          const double* vals, int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt,
-                          int64_t* kind, unsigned long long* hash, int dedupe, cudaStream_t st);
+                          const double* vals, ColMap cm, int64_t* val_cnt, int64_t* pat_cnt,
+                          int64_t* col_cnt, int64_t* kind, unsigned long long* hash, int dedupe,
+                          cudaStream_t st);
 // inclusive max-scan (tmp == nullptr: query *tmp_bytes)
 void scan_max_i64(const int64_t* in, int64_t n, int64_t* out, void* tmp, size_t* tmp_bytes,
                   cudaStream_t st);
@@ -57,18 +64,22 @@ void launch_table_assign(int64_t n, const unsigned long long* key, const int32_t
                          const int64_t* headpos, const int64_t* tab_ptr, int64_t* slice_tab,
                          int32_t* slice_rep, cudaStream_t st);
 void launch_iota_i32(int64_t n, int32_t* out, cudaStream_t st);
-// CDIA participation words (see CdiaClass); *bad = 1 if a table offset is missing
-void launch_cdia_bits(int64_t nslices, int ncls, const int64_t* starts, const int32_t* offs,
-                      const int32_t* nofs, const int64_t* meta, const int2* pat, uint32_t* bits,
-                      int* bad, cudaStream_t st);
+// CDIA participation words (see CdiaClass); *bad = 1 if a table key is missing;
+// nodiag[c] = 1 if some owned row of class c lacks key 0 (its diagonal)
+void launch_cdia_bits(int64_t nslices, int64_t n_local, int ncls, const int64_t* starts,
+                      const int64_t* ckeys, const int32_t* nofs, const int64_t* meta,
+                      const int64_t* pkey, const int2* pat, uint32_t* bits, int* bad,
+                      int* nodiag, cudaStream_t st);
 void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                          const double* vals, const int64_t* kind, const int64_t* slice_tab,
-                          const int32_t* slice_rep, const int64_t* new_ptr, const int64_t* pat_ptr,
-                          int64_t pat_base, const int64_t* col_ptr, double* nvals, int32_t* ncols,
-                          int2* pat, double* pval, int64_t* meta, cudaStream_t st);
+                          const double* vals, ColMap cm, const int64_t* kind,
+                          const int64_t* slice_tab, const int32_t* slice_rep,
+                          const int64_t* new_ptr, const int64_t* pat_ptr, int64_t pat_base,
+                          const int64_t* col_ptr, double* nvals, int32_t* ncols, int2* pat,
+                          double* pval, int64_t* pkey, int64_t* meta, cudaStream_t st);
 void launch_compress_verify(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                            const double* vals, const int64_t* kind, const int64_t* slice_tab,
-                            const int2* pat, const double* pval, int* bad, cudaStream_t st);
+                            const double* vals, ColMap cm, const int64_t* kind,
+                            const int64_t* slice_tab, const int2* pat, const double* pval,
+                            const int64_t* pkey, int* bad, cudaStream_t st);
 // inv_diag[i] = 1/diag[i]; *bad = 1 if any diag <= 0 (precond.cpp:17-22)
 void launch_inv_diag(int64_t n, const double* diag, double* inv_diag, int* bad, cudaStream_t st);
 
@@ -96,14 +107,18 @@ struct SpmvArgs {
   // NVLink peer-memory halo (z-slab problems, fast MPK). Producer:
   // z rows [0, send_lo) also go to push_lo[row] (rank-1's upper ghost plane) and
   // rows [hi_begin, n_local) to push_hi[row - hi_begin] (rank+1's lower ghost
-  // plane); each warp then adds its row counts to the peers' receive counters
-  // (release, system scope). Consumer: before the first slice every block waits
-  // until wait_ctr[0] >= want_lo and wait_ctr[1] >= want_hi (acquire).
+  // plane), plain remote stores. Signal: the NEXT kernel on the producer's
+  // stream (its predecessor has completed, so every remote store of it is
+  // visible) adds the known row counts to the peers' receive counters with one
+  // release reduction each (rel_*), from block 0 before anything else.
+  // Consumer: before the first slice every block waits until wait_ctr[0] >=
+  // want_lo and wait_ctr[1] >= want_hi (acquire).
   double* push_lo = nullptr;
   double* push_hi = nullptr;
   int64_t send_lo = 0, hi_begin = 0;
-  unsigned long long* sig_lo = nullptr;
-  unsigned long long* sig_hi = nullptr;
+  unsigned long long* rel_lo = nullptr;
+  unsigned long long* rel_hi = nullptr;
+  unsigned long long rel_lo_n = 0, rel_hi_n = 0;
   const unsigned long long* wait_ctr = nullptr;
   unsigned long long want_lo = 0, want_hi = 0;
 };
@@ -111,9 +126,11 @@ void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t slice_b
                  int64_t slice_end, cudaStream_t st);
 int spmv_dot_blocks(int64_t nslices);
 // Push rows [0, send_lo) and [hi_begin, n_local) of col into the neighbours'
-// ghost slots and signal their receive counters (the z_0 halo of the fast MPK).
+// ghost slots (the z_0 halo of the fast MPK; signalled by the next kernel).
 void launch_halo_push(const SpmvArgs& g, const double* col, int64_t n_local, DevState* st,
                       cudaStream_t s);
+// Release a previous kernel's pushes when no SpMV launch follows to do it.
+void launch_halo_release(const SpmvArgs& g, DevState* st, cudaStream_t s);
 
 // ------------------------------------------------------------------ vector kernels (vec.cu)
 void launch_precond_apply(int64_t n, const double* inv_diag, const double* in, double* out,

@@ -1,8 +1,10 @@
 // runtime.cu -- device context, device-resident problems, halo exchange,
 // collectives and launch/timing accounting.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -56,9 +58,11 @@ Launch::~Launch() {
 void collect_timing(cs_ctx* c) {
   if (c->spans.empty()) return;
   CS_CUDA(cudaStreamSynchronize(c->stream));
+  static const bool trace = std::getenv("CS_TIMING_TRACE") != nullptr;  // diagnostics
   for (const auto& s : c->spans) {
     float ms = 0.f;
     CS_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
+    if (trace) std::fprintf(stderr, "[trace r%d] phase %d %.4f ms\n", c->rank, s.phase, ms);
     c->phase_ms[s.phase] += ms;
     c->event_pool.push_back(s.a);
     c->event_pool.push_back(s.b);
@@ -161,18 +165,24 @@ struct PeerInfo {
   int32_t ok, pad;
 };
 
+void fill_push(const cs_problem* p, SpmvArgs& g, int col);
+}  // namespace
+
+void fill_push_args(const cs_problem* p, SpmvArgs& g, int col) { fill_push(p, g, col); }
+
+namespace {
 void fill_push(const cs_problem* p, SpmvArgs& g, int col) {
   if (p->ghost_lo > 0) {  // my first plane -> rank-1's upper ghost plane
     const cs_problem::PeerMap& m = p->peer[0];
     g.push_lo = static_cast<double*>(m.ws) + m.ghost_off + static_cast<int64_t>(col) * m.ld;
     g.send_lo = p->send_lo;
-    g.sig_lo = static_cast<unsigned long long*>(m.sig) + 1;  // its "from upper" counter
+
   }
   if (p->ghost_hi > 0) {  // my last plane -> rank+1's lower ghost plane
     const cs_problem::PeerMap& m = p->peer[1];
     g.push_hi = static_cast<double*>(m.ws) + m.ghost_off + static_cast<int64_t>(col) * m.ld;
     g.hi_begin = p->n_local - p->send_hi;
-    g.sig_hi = static_cast<unsigned long long*>(m.sig) + 0;  // its "from lower" counter
+
   }
 }
 }  // namespace
@@ -191,6 +201,7 @@ bool p2p_setup(cs_problem* p, double* Z) {
   cs_ctx* c = p->ctx;
   p->p2p = false;
   p->p2p_epoch = 0;
+  p->p2p_pending = false;
   if (c->nranks == 1 || p->general_halo) return false;
   const char* env = std::getenv("CS_P2P_HALO");
   int ok = (env == nullptr || std::atoi(env) != 0) && !p->ws.pooled && p->ws.p != nullptr;
@@ -272,27 +283,52 @@ bool p2p_setup(cs_problem* p, double* Z) {
   return p->p2p;
 }
 
+// release args for the pushes of the previous kernel (if it pushed)
+void fill_release(cs_problem* p, SpmvArgs& g) {
+  if (!p->p2p_pending) return;
+  if (p->ghost_lo > 0) {  // rank-1's "from upper" counter
+    g.rel_lo = static_cast<unsigned long long*>(p->peer[0].sig) + 1;
+    g.rel_lo_n = static_cast<unsigned long long>(p->send_lo);
+  }
+  if (p->ghost_hi > 0) {  // rank+1's "from lower" counter
+    g.rel_hi = static_cast<unsigned long long*>(p->peer[1].sig) + 0;
+    g.rel_hi_n = static_cast<unsigned long long>(p->send_hi);
+  }
+  p->p2p_pending = false;
+}
+
 void spmv_p2p(cs_problem* p, int kind, SpmvArgs g, int push_col) {
   cs_ctx* c = p->ctx;
   const SellView A = p->view();
   ++p->p2p_epoch;
   if (push_col >= 0) fill_push(p, g, push_col);
   {
-    Launch L(c, CS_PHASE_SPMV);
-    launch_spmv(kind, A, g, p->slice_int_begin, p->slice_int_end, c->stream);
+    SpmvArgs gi = g;  // the interior launch releases the previous kernel's pushes
+    fill_release(p, gi);
+    if (p->slice_int_end > p->slice_int_begin) {
+      Launch L(c, CS_PHASE_SPMV);
+      launch_spmv(kind, A, gi, p->slice_int_begin, p->slice_int_end, c->stream);
+    } else if (gi.rel_lo || gi.rel_hi) {
+      Launch L(c, CS_PHASE_COMM);
+      launch_halo_release(gi, g.st, c->stream);
+    }
   }
   g.wait_ctr = p->sig.as<unsigned long long>();
   g.want_lo = p->p2p_epoch * static_cast<unsigned long long>(p->ghost_lo);
   g.want_hi = p->p2p_epoch * static_cast<unsigned long long>(p->ghost_hi);
   Launch L(c, CS_PHASE_SPMV);
   launch_spmv(kind, A, g, p->slice_int_end, p->nslices + p->slice_int_begin, c->stream);
+  p->p2p_pending = push_col >= 0;
 }
 
 void p2p_push(cs_problem* p, const double* src, int col, DevState* st) {
   SpmvArgs g;
   fill_push(p, g, col);
+  fill_release(p, g);  // (nothing pending here in practice)
+  if (g.rel_lo || g.rel_hi) launch_halo_release(g, st, p->ctx->stream);
   Launch L(p->ctx, CS_PHASE_COMM);
   launch_halo_push(g, src, p->n_local, st, p->ctx->stream);
+  p->p2p_pending = true;
 }
 
 std::string format_device_error(unsigned long long word, int) {
@@ -441,43 +477,64 @@ void build_cdia(cs_problem* p) {
   std::vector<int64_t> meta(ns);
   std::vector<int2> pat(p->table_entries);
   std::vector<double> pval(p->table_entries);
+  std::vector<int64_t> pkey(p->table_entries);
   CS_CUDA(cudaMemcpyAsync(meta.data(), p->meta.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost,
                           c->stream));
   CS_CUDA(cudaMemcpyAsync(pat.data(), p->pat.p, sizeof(int2) * pat.size(), cudaMemcpyDeviceToHost,
                           c->stream));
   CS_CUDA(cudaMemcpyAsync(pval.data(), p->pval.p, sizeof(double) * pval.size(),
                           cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaMemcpyAsync(pkey.data(), p->pkey.p, sizeof(int64_t) * pkey.size(),
+                          cudaMemcpyDeviceToHost, c->stream));
   CS_CUDA(cudaStreamSynchronize(c->stream));
   constexpr int kMaxClasses = 64;
+  // class entries (global key, local offset, value), kept in key order = the
+  // stored order of every row (rows are ascending in global columns)
+  struct Ent {
+    int64_t key;
+    int off;
+    double v;
+  };
   std::vector<CdiaClass> cls;
-  std::vector<std::pair<int, double>> cur;  // sorted by offset
+  std::vector<std::vector<int64_t>> cls_keys;
+  std::vector<Ent> cur;
   int64_t s0 = 0, last_tab = -1;
   auto flush = [&](int64_t s1) {
     CdiaClass k{};
     k.s0 = s0;
     k.s1 = s1;
     k.t.n = static_cast<int>(cur.size());
+    std::vector<int64_t> keys;
     for (size_t j = 0; j < cur.size(); ++j) {
-      k.t.off[j] = cur[j].first;
-      k.t.v[j] = cur[j].second;
+      k.t.off[j] = cur[j].off;
+      k.t.v[j] = cur[j].v;
+      keys.push_back(cur[j].key);
     }
     cls.push_back(k);
+    cls_keys.push_back(keys);
   };
+  const char* split_env = std::getenv("CS_CDIA_SPLIT");  // diagnostics: forced class break
+  const int64_t split_at = split_env ? std::atoll(split_env) : -1;
   for (int64_t sl = 0; sl < ns; ++sl) {
     const int64_t ti = pat_index(meta[sl]);
+    if (sl == split_at && sl > s0) {
+      flush(sl);
+      s0 = sl;
+      cur.clear();
+      last_tab = -1;
+    }
     if (ti == last_tab) continue;  // same table as the previous slice
     const int U = pat_uniform(meta[sl]);
-    std::vector<std::pair<int, double>> merged = cur;
+    std::vector<Ent> merged = cur;
     bool ok = true;
     for (int k = 0; k < U && ok; ++k) {
-      const int off = pat[ti + k].x;
-      const double v = pval[ti + k];
-      auto it = std::lower_bound(merged.begin(), merged.end(), std::make_pair(off, -HUGE_VAL),
-                                 [](const auto& a, const auto& b) { return a.first < b.first; });
-      if (it != merged.end() && it->first == off) {
-        if (std::memcmp(&it->second, &v, sizeof v) != 0) ok = false;  // bitwise
+      const Ent e{pkey[ti + k], pat[ti + k].x, pval[ti + k]};
+      auto it = std::lower_bound(merged.begin(), merged.end(), e,
+                                 [](const Ent& a, const Ent& b) { return a.key < b.key; });
+      if (it != merged.end() && it->key == e.key) {  // same entry: same offset, same value bits
+        if (it->off != e.off || std::memcmp(&it->v, &e.v, sizeof e.v) != 0) ok = false;
       } else {
-        merged.insert(it, {off, v});
+        merged.insert(it, e);
       }
     }
     if (ok && merged.size() <= static_cast<size_t>(kCdiaMax)) {
@@ -488,38 +545,45 @@ void build_cdia(cs_problem* p) {
       if (static_cast<int>(cls.size()) >= kMaxClasses) return;
       s0 = sl;
       cur.clear();
-      for (int k = 0; k < U; ++k) cur.push_back({pat[ti + k].x, pval[ti + k]});
+      for (int k = 0; k < U; ++k) cur.push_back({pkey[ti + k], pat[ti + k].x, pval[ti + k]});
     }
     last_tab = ti;
   }
   flush(ns);
   // participation words on the device
   std::vector<int64_t> starts(cls.size());
-  std::vector<int32_t> offs(cls.size() * kCdiaMax, 0);
+  std::vector<int64_t> keys(cls.size() * kCdiaMax, INT64_MIN);
   std::vector<int32_t> nofs(cls.size());
   for (size_t k = 0; k < cls.size(); ++k) {
     starts[k] = cls[k].s0;
     nofs[k] = cls[k].t.n;
-    for (int j = 0; j < cls[k].t.n; ++j) offs[k * kCdiaMax + j] = cls[k].t.off[j];
+    for (int j = 0; j < cls[k].t.n; ++j) keys[k * kCdiaMax + j] = cls_keys[k][j];
   }
-  DBuf d_starts(sizeof(int64_t) * starts.size()), d_offs(sizeof(int32_t) * offs.size()),
+  DBuf d_starts(sizeof(int64_t) * starts.size()), d_keys(sizeof(int64_t) * keys.size()),
       d_n(sizeof(int32_t) * nofs.size());
   CS_CUDA(cudaMemcpyAsync(d_starts.p, starts.data(), d_starts.bytes, cudaMemcpyHostToDevice,
                           c->stream));
-  CS_CUDA(cudaMemcpyAsync(d_offs.p, offs.data(), d_offs.bytes, cudaMemcpyHostToDevice, c->stream));
+  CS_CUDA(cudaMemcpyAsync(d_keys.p, keys.data(), d_keys.bytes, cudaMemcpyHostToDevice, c->stream));
   CS_CUDA(cudaMemcpyAsync(d_n.p, nofs.data(), d_n.bytes, cudaMemcpyHostToDevice, c->stream));
   p->pbits.alloc(sizeof(uint32_t) * ns * kSliceRows);
-  DBuf bad(sizeof(int));
-  CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
-  launch_cdia_bits(ns, static_cast<int>(cls.size()), d_starts.as<int64_t>(), d_offs.as<int32_t>(),
-                   d_n.as<int32_t>(), p->meta.as<int64_t>(), p->pat.as<int2>(),
-                   p->pbits.as<uint32_t>(), bad.as<int>(), c->stream);
-  int hbad = 0;
-  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  DBuf flags(sizeof(int) * (1 + cls.size()));
+  CS_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, c->stream));
+  launch_cdia_bits(ns, p->n_local, static_cast<int>(cls.size()), d_starts.as<int64_t>(),
+                   d_keys.as<int64_t>(), d_n.as<int32_t>(), p->meta.as<int64_t>(),
+                   p->pkey.as<int64_t>(), p->pat.as<int2>(), p->pbits.as<uint32_t>(),
+                   flags.as<int>(), flags.as<int>() + 1, c->stream);
+  std::vector<int> hf(1 + cls.size());
+  CS_CUDA(cudaMemcpyAsync(hf.data(), flags.p, flags.bytes, cudaMemcpyDeviceToHost, c->stream));
   CS_CUDA(cudaStreamSynchronize(c->stream));
-  if (hbad) {
+  if (hf[0]) {
     p->pbits.release();
     return;
+  }
+  for (size_t k = 0; k < cls.size(); ++k) {
+    cls[k].t.diag = 0.0;
+    if (hf[1 + k]) continue;
+    for (int j = 0; j < cls[k].t.n; ++j)
+      if (cls_keys[k][j] == 0) cls[k].t.diag = cls[k].t.v[j];
   }
   p->cdia = std::move(cls);
 }
@@ -547,8 +611,9 @@ void compress_sell(cs_problem* p, int dedupe = 1) {
   int32_t* iota = slcs.as<int32_t>();
   int32_t* slc_sorted = iota + nn;
   int32_t* slice_rep = slc_sorted + nn;
+  const ColMap cm{p->row_begin, p->n_local, p->ghost_global.as<int64_t>()};
   launch_compress_plan(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), p->vals.as<double>(),
-                       val_cnt, pat_cnt, col_cnt, kind, hash, dedupe, c->stream);
+                       cm, val_cnt, pat_cnt, col_cnt, kind, hash, dedupe, c->stream);
   // uniform tables: sort (hash, slice), one table per group of equal hashes
   launch_iota_i32(ns, iota, c->stream);
   size_t tb = 0, tm = 0, ts = 0;
@@ -581,16 +646,17 @@ void compress_sell(cs_problem* p, int dedupe = 1) {
   DBuf ncols(sizeof(int32_t) * std::max<int64_t>(ncol, 1));
   DBuf npatb(sizeof(int2) * std::max<int64_t>(npat, 1));
   DBuf npval(sizeof(double) * std::max<int64_t>(npat, 1));
+  DBuf npkey(sizeof(int64_t) * std::max<int64_t>(npat, 1));
   DBuf nmeta(sizeof(int64_t) * nn);
   launch_compress_fill(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(), p->vals.as<double>(),
-                       kind, slice_tab, slice_rep, new_ptr, pat_ptr, ntab, col_ptr,
+                       cm, kind, slice_tab, slice_rep, new_ptr, pat_ptr, ntab, col_ptr,
                        nvals.as<double>(), ncols.as<int32_t>(), npatb.as<int2>(),
-                       npval.as<double>(), nmeta.as<int64_t>(), c->stream);
+                       npval.as<double>(), npkey.as<int64_t>(), nmeta.as<int64_t>(), c->stream);
   DBuf bad(sizeof(int));
   CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
   launch_compress_verify(ns, p->slice_ptr.as<int64_t>(), p->cols.as<int32_t>(),
-                         p->vals.as<double>(), kind, slice_tab, npatb.as<int2>(),
-                         npval.as<double>(), bad.as<int>(), c->stream);
+                         p->vals.as<double>(), cm, kind, slice_tab, npatb.as<int2>(),
+                         npval.as<double>(), npkey.as<int64_t>(), bad.as<int>(), c->stream);
   int hbad = 0;
   CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CS_CUDA(cudaStreamSynchronize(c->stream));
@@ -622,6 +688,7 @@ void compress_sell(cs_problem* p, int dedupe = 1) {
   p->cols = std::move(ncols);
   p->pat = std::move(npatb);
   p->pval = std::move(npval);
+  p->pkey = std::move(npkey);
   p->meta = std::move(nmeta);
   p->slice_ptr = std::move(nptr);
   p->compressed_slices = nc;
@@ -687,14 +754,14 @@ cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_
   p->diag.alloc(sizeof(double) * std::max<int64_t>(p->n_local, 1));
   launch_stencil_fill(d, p->n_local, p->nslices, p->slice_ptr.as<int64_t>(), p->vals.as<double>(),
                       p->cols.as<int32_t>(), p->diag.as<double>(), c->stream);
-  compress_sell(p.get());
-  // ghost global ids: plane z0-1 then plane z1
+  // ghost global ids: plane z0-1 then plane z1 (the compression's merge keys need them)
   for (int64_t i = 0; i < p->ghost_lo; ++i) p->ghosts_host.push_back(r0 - plane + i);
   for (int64_t i = 0; i < p->ghost_hi; ++i) p->ghosts_host.push_back(r1 + i);
   p->ghost_global.alloc(sizeof(int64_t) * std::max<int64_t>(p->n_ghost, 1));
   if (p->n_ghost)
     CS_CUDA(cudaMemcpyAsync(p->ghost_global.p, p->ghosts_host.data(), sizeof(int64_t) * p->n_ghost,
                             cudaMemcpyHostToDevice, c->stream));
+  compress_sell(p.get());
   CS_CUDA(cudaStreamSynchronize(c->stream));
   return p.release();
 }

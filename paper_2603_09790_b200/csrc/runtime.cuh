@@ -129,7 +129,7 @@ struct cs_problem {
   }
   int gen_kind = -1;
   int64_t nx = 0, ny = 0, nz = 0;
-  csg::DBuf slice_ptr, vals, cols, meta, pat, pval, pbits, diag, inv_diag, ghost_global;
+  csg::DBuf slice_ptr, vals, cols, meta, pat, pval, pkey, pbits, diag, inv_diag, ghost_global;
   std::vector<csg::CdiaClass> cdia;
   int64_t compressed_slices = 0, uniform_slices = 0, pattern_entries = 0, table_entries = 0;
   int max_width = 0;
@@ -154,6 +154,7 @@ struct cs_problem {
   int64_t z_off = 0;                // element offset of Z in ws
   bool p2p = false;                 // peer mappings valid for the current ws
   unsigned long long p2p_epoch = 0; // halo exchanges consumed in the current solve
+  bool p2p_pending = false;         // the last kernel pushed rows not yet released
   csg::SellView view() const {
     csg::SellView v;
     v.n_local = n_local;
@@ -204,6 +205,8 @@ void p2p_teardown(cs_problem* p);
 void spmv_p2p(cs_problem* p, int kind, SpmvArgs g, int push_col);
 // push Z column `col`'s boundary rows (the z_0 halo after the update pass)
 void p2p_push(cs_problem* p, const double* src, int col, DevState* st);
+// the push arguments of Z column `col` (diagnostics)
+void fill_push_args(const cs_problem* p, SpmvArgs& g, int col);
 // scratch region of the context, grown on demand
 void* ctx_scratch(cs_ctx* c, size_t bytes);
 

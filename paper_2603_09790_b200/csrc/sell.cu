@@ -14,6 +14,7 @@
 //    is partition-invariant.
 //  * CSR -> SELL conversion for uploaded reference CsrMatrix data.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -306,42 +307,67 @@ constexpr int kSentinel = 0x7fffffff;
 constexpr unsigned long long kNoTable = ~0ull;
 enum SliceKind : int64_t { kExplicit = 0, kValuePattern = 1, kUniform = 2 };
 
-// Merge cursor over one slice's 32 sorted rows (one lane per row).
+// Merge cursor over one slice's 32 rows (one lane per row). Rows keep their
+// entries in ascending GLOBAL column order (the reference's stored order), so
+// the union is merged on the global relative offset (global col - global row);
+// the table stores the LOCAL relative offset (local col - local row) that the
+// SpMV adds to its row index. On a rank whose lower ghost plane lives after its
+// owned rows, the first plane's rows are not ascending in local columns, but
+// they still are in global ones, and their local offsets stay constant.
 struct PatWalk {
   const int32_t* cols;
   const double* vals;
-  int64_t base, row;
+  ColMap m;
+  int64_t base, row, grow;
   int len, idx, width;
   bool sorted;
-  __device__ void init(const int64_t* slice_ptr, const int32_t* c, const double* v, int64_t slice,
-                       int lane) {
-    cols = c, vals = v;
+  __device__ int64_t key(int32_t c) const {
+    return (c < m.n_local ? m.row_begin + c : m.ghost[c - m.n_local]) - grow;
+  }
+  __device__ void init(const int64_t* slice_ptr, const int32_t* c, const double* v, ColMap cm,
+                       int64_t slice, int lane) {
+    cols = c, vals = v, m = cm;
     row = slice * kSliceRows + lane;
+    grow = m.row_begin + row;
     base = slice_ptr[slice] + lane;
     width = static_cast<int>((slice_ptr[slice + 1] - slice_ptr[slice]) >> 5);
     len = 0, idx = 0;
     sorted = true;
-    int32_t prev = -1;
+    int64_t prev = INT64_MIN;
     for (int k = 0; k < width; ++k) {
       const int32_t col = cols[base + k * kSliceRows];
       if (col < 0) break;  // trailing padding
-      if (col <= prev) sorted = false;
-      prev = col;
+      const int64_t kk = key(col);
+      if (kk <= prev) sorted = false;
+      prev = kk;
       ++len;
     }
   }
-  // next union entry: offset, lane mask, the value of the lowest holding lane
-  // and whether every holding lane stores that value bitwise; false at the end
-  __device__ bool next(int& off, unsigned& mask, unsigned long long& vbits, bool& uni) {
-    const int cur = idx < len ? static_cast<int>(cols[base + idx * kSliceRows] - row) : kSentinel;
-    off = __reduce_min_sync(0xffffffffu, cur);
-    if (off == kSentinel) return false;
-    const bool hit = cur == off;
+  // next union entry: global key, local offset, lane mask, the value of the
+  // lowest holding lane, whether every holding lane stores that value bitwise
+  // (uni) and sits at the same local offset (same); false at the end
+  __device__ bool next(int64_t& gk, int& off, unsigned& mask, unsigned long long& vbits,
+                       bool& uni, bool& same) {
+    const int32_t col = idx < len ? cols[base + idx * kSliceRows] : -1;
+    const int64_t cur = idx < len ? key(col) : INT64_MAX;
+    int64_t mn = cur;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t t = __shfl_xor_sync(0xffffffffu, mn, o);
+      mn = t < mn ? t : mn;
+    }
+    if (mn == INT64_MAX) return false;
+    gk = mn;
+    const bool hit = cur == mn;
     mask = __ballot_sync(0xffffffffu, hit);
+    const int lead = __ffs(mask) - 1;
+    const int mine_off = hit ? static_cast<int>(col - row) : 0;
+    off = __shfl_sync(0xffffffffu, mine_off, lead);
+    same = __all_sync(0xffffffffu, !hit || mine_off == off);
     const unsigned long long mine =
         hit ? static_cast<unsigned long long>(__double_as_longlong(vals[base + idx * kSliceRows]))
             : 0ull;
-    vbits = __shfl_sync(0xffffffffu, mine, __ffs(mask) - 1);
+    vbits = __shfl_sync(0xffffffffu, mine, lead);
     uni = __all_sync(0xffffffffu, !hit || mine == vbits);
     if (hit) ++idx;
     return true;
@@ -357,7 +383,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long h, unsign
 
 __global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
                                      const int32_t* __restrict__ cols,
-                                     const double* __restrict__ vals, int64_t* val_cnt,
+                                     const double* __restrict__ vals, ColMap cm, int64_t* val_cnt,
                                      int64_t* pat_cnt, int64_t* col_cnt, int64_t* kind,
                                      unsigned long long* hash, int allow, int allow_uniform,
                                      int dedupe) {
@@ -365,21 +391,28 @@ __global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict_
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices) return;
   PatWalk w;
-  w.init(slice_ptr, cols, vals, slice, lane);
+  w.init(slice_ptr, cols, vals, cm, slice, lane);
   const int W = w.width;
   bool ok = __all_sync(0xffffffffu, w.sorted) && W > 0 && allow;
   bool uni = ok && allow_uniform;
   int U = 0;
   unsigned long long h = 0x243f6a8885a308d3ull;
   if (ok) {
+    int64_t gk;
     int off;
     unsigned mask;
     unsigned long long vb;
-    bool u;
-    while (w.next(off, mask, vb, u)) {
+    bool u, same;
+    while (w.next(gk, off, mask, vb, u, same)) {
       ++U;
+      if (!same) {  // one slot must be one local offset for every row holding it
+        ok = uni = false;
+        break;
+      }
       uni = uni && u && U <= kUniformMaxSlots;
-      if (uni) h = mix64(mix64(mix64(h, static_cast<unsigned>(off)), mask), vb);
+      if (uni)
+        h = mix64(mix64(mix64(mix64(h, static_cast<unsigned>(off)), mask), vb),
+                  static_cast<unsigned long long>(gk));
       if (!uni && 264 * U > 384 * W) {
         ok = false;
         break;
@@ -435,14 +468,15 @@ __global__ void table_assign_kernel(int64_t n, const unsigned long long* __restr
 
 __global__ void compress_fill_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
                                      const int32_t* __restrict__ cols,
-                                     const double* __restrict__ vals,
+                                     const double* __restrict__ vals, ColMap cm,
                                      const int64_t* __restrict__ kind,
                                      const int64_t* __restrict__ slice_tab,
                                      const int32_t* __restrict__ slice_rep,
                                      const int64_t* __restrict__ new_ptr,
                                      const int64_t* __restrict__ pat_ptr, int64_t pat_base,
                                      const int64_t* __restrict__ col_ptr, double* nvals,
-                                     int32_t* ncols, int2* pat, double* pval, int64_t* meta) {
+                                     int32_t* ncols, int2* pat, double* pval, int64_t* pkey,
+                                     int64_t* meta) {
   const int lane = threadIdx.x & 31;
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices) return;
@@ -465,17 +499,19 @@ __global__ void compress_fill_kernel(int64_t nslices, const int64_t* __restrict_
     return;
   }
   PatWalk w;
-  w.init(slice_ptr, cols, vals, slice, lane);
+  w.init(slice_ptr, cols, vals, cm, slice, lane);
   const int64_t pb = k == kUniform ? slice_tab[slice] : pat_base + pat_ptr[slice];
   const int64_t nb = new_ptr[slice] + lane;
+  int64_t gk;
   int off;
   unsigned mask;
   unsigned long long vb;
-  bool u;
-  for (int q = 0; q < U && w.next(off, mask, vb, u); ++q) {
+  bool u, same;
+  for (int q = 0; q < U && w.next(gk, off, mask, vb, u, same); ++q) {
     if (lane == 0) {
       pat[pb + q] = make_int2(off, static_cast<int>(mask));
       pval[pb + q] = k == kUniform ? __longlong_as_double(static_cast<long long>(vb)) : 0.0;
+      pkey[pb + q] = gk;
     }
     if (k == kValuePattern) {
       // w.idx was advanced past this entry on the holding lanes
@@ -489,30 +525,32 @@ __global__ void compress_fill_kernel(int64_t nslices, const int64_t* __restrict_
 // every uniform slice against the table it points at, exactly
 __global__ void compress_verify_kernel(int64_t nslices, const int64_t* __restrict__ slice_ptr,
                                        const int32_t* __restrict__ cols,
-                                       const double* __restrict__ vals,
+                                       const double* __restrict__ vals, ColMap cm,
                                        const int64_t* __restrict__ kind,
                                        const int64_t* __restrict__ slice_tab,
                                        const int2* __restrict__ pat,
-                                       const double* __restrict__ pval, int* bad) {
+                                       const double* __restrict__ pval,
+                                       const int64_t* __restrict__ pkey, int* bad) {
   const int lane = threadIdx.x & 31;
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices || (kind[slice] & 0xff) != kUniform) return;
   const int U = static_cast<int>(kind[slice] >> 8);
   const int64_t pb = slice_tab[slice];
   PatWalk w;
-  w.init(slice_ptr, cols, vals, slice, lane);
+  w.init(slice_ptr, cols, vals, cm, slice, lane);
+  int64_t gk;
   int off;
   unsigned mask;
   unsigned long long vb;
-  bool u;
-  bool same = true;
+  bool u, same;
+  bool eq = true;
   int q = 0;
-  for (; q < U && w.next(off, mask, vb, u); ++q) {
+  for (; q < U && w.next(gk, off, mask, vb, u, same); ++q) {
     const int2 e = pat[pb + q];
-    same = same && e.x == off && static_cast<unsigned>(e.y) == mask &&
-           static_cast<unsigned long long>(__double_as_longlong(pval[pb + q])) == vb;
+    eq = eq && e.x == off && static_cast<unsigned>(e.y) == mask && pkey[pb + q] == gk &&
+         static_cast<unsigned long long>(__double_as_longlong(pval[pb + q])) == vb;
   }
-  if (lane == 0 && (!same || q != U)) atomicExch(bad, 1);
+  if (lane == 0 && (!eq || q != U)) atomicExch(bad, 1);
 }
 
 __global__ void inv_diag_kernel(int64_t n, const double* __restrict__ diag, double* inv, int* bad) {
@@ -604,16 +642,17 @@ void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* gho
 }
 
 void launch_compress_plan(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                          const double* vals, int64_t* val_cnt, int64_t* pat_cnt, int64_t* col_cnt,
-                          int64_t* kind, unsigned long long* hash, int dedupe, cudaStream_t st) {
+                          const double* vals, ColMap cm, int64_t* val_cnt, int64_t* pat_cnt,
+                          int64_t* col_cnt, int64_t* kind, unsigned long long* hash, int dedupe,
+                          cudaStream_t st) {
   if (nslices == 0) return;
   // CS_SELL_EXPLICIT=1 keeps every slice explicit; CS_SELL_VALUES=1 keeps the value
   // slots (no uniform-value slices) -- format A/B experiments, read per conversion
   const int allow = std::getenv("CS_SELL_EXPLICIT") ? 0 : 1;
   const int allow_uniform = std::getenv("CS_SELL_VALUES") ? 0 : 1;
   compress_plan_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
-      nslices, slice_ptr, cols, vals, val_cnt, pat_cnt, col_cnt, kind, hash, allow, allow_uniform,
-      dedupe);
+      nslices, slice_ptr, cols, vals, cm, val_cnt, pat_cnt, col_cnt, kind, hash, allow,
+      allow_uniform, dedupe);
   CS_CUDA(cudaGetLastError());
 }
 
@@ -648,33 +687,38 @@ void launch_table_assign(int64_t n, const unsigned long long* key, const int32_t
 void launch_iota_i32(int64_t n, int32_t* out, cudaStream_t st);
 
 void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                          const double* vals, const int64_t* kind, const int64_t* slice_tab,
-                          const int32_t* slice_rep, const int64_t* new_ptr, const int64_t* pat_ptr,
-                          int64_t pat_base, const int64_t* col_ptr, double* nvals, int32_t* ncols,
-                          int2* pat, double* pval, int64_t* meta, cudaStream_t st) {
+                          const double* vals, ColMap cm, const int64_t* kind,
+                          const int64_t* slice_tab, const int32_t* slice_rep,
+                          const int64_t* new_ptr, const int64_t* pat_ptr, int64_t pat_base,
+                          const int64_t* col_ptr, double* nvals, int32_t* ncols, int2* pat,
+                          double* pval, int64_t* pkey, int64_t* meta, cudaStream_t st) {
   if (nslices == 0) return;
   compress_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
-      nslices, slice_ptr, cols, vals, kind, slice_tab, slice_rep, new_ptr, pat_ptr, pat_base,
-      col_ptr, nvals, ncols, pat, pval, meta);
+      nslices, slice_ptr, cols, vals, cm, kind, slice_tab, slice_rep, new_ptr, pat_ptr, pat_base,
+      col_ptr, nvals, ncols, pat, pval, pkey, meta);
   CS_CUDA(cudaGetLastError());
 }
 
 void launch_compress_verify(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
-                            const double* vals, const int64_t* kind, const int64_t* slice_tab,
-                            const int2* pat, const double* pval, int* bad, cudaStream_t st) {
+                            const double* vals, ColMap cm, const int64_t* kind,
+                            const int64_t* slice_tab, const int2* pat, const double* pval,
+                            const int64_t* pkey, int* bad, cudaStream_t st) {
   if (nslices == 0) return;
   compress_verify_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
-      nslices, slice_ptr, cols, vals, kind, slice_tab, pat, pval, bad);
+      nslices, slice_ptr, cols, vals, cm, kind, slice_tab, pat, pval, pkey, bad);
   CS_CUDA(cudaGetLastError());
 }
 
 // CDIA participation words: per slice (one warp), its class by binary search
-// over the class starts, then every table entry's offset located in the
-// class's sorted offsets; lane l collects bit j for each entry it holds.
-__global__ void cdia_bits_kernel(int64_t nslices, int ncls, const int64_t* __restrict__ starts,
-                                 const int32_t* __restrict__ offs, const int32_t* __restrict__ nofs,
-                                 const int64_t* __restrict__ meta, const int2* __restrict__ pat,
-                                 uint32_t* bits, int* bad) {
+// over the class starts, then every table entry located in the class table by
+// its global key (the class table is in key = stored order); lane l collects
+// bit j for each entry it holds.
+__global__ void cdia_bits_kernel(int64_t nslices, int64_t n_local, int ncls,
+                                 const int64_t* __restrict__ starts,
+                                 const int64_t* __restrict__ ckeys, const int32_t* __restrict__ nofs,
+                                 const int64_t* __restrict__ meta, const int64_t* __restrict__ pkey,
+                                 const int2* __restrict__ pat, uint32_t* bits, int* bad,
+                                 int* nodiag) {
   const int lane = threadIdx.x & 31;
   const int64_t slice = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (slice >= nslices) return;
@@ -684,7 +728,7 @@ __global__ void cdia_bits_kernel(int64_t nslices, int ncls, const int64_t* __res
     if (starts[mid] <= slice) lo = mid;
     else hi = mid - 1;
   }
-  const int32_t* co = offs + lo * kCdiaMax;
+  const int64_t* ck = ckeys + lo * kCdiaMax;
   const int cn = nofs[lo];
   const int64_t m = meta[slice];
   const int64_t pi = pat_index(m);
@@ -692,25 +736,31 @@ __global__ void cdia_bits_kernel(int64_t nslices, int ncls, const int64_t* __res
   uint32_t w = 0;
   bool ok = true;
   for (int k = 0; k < U; ++k) {
-    const int2 e = pat[pi + k];
+    const int64_t key = pkey[pi + k];
     int j = 0;
-    while (j < cn && co[j] != e.x) ++j;
+    while (j < cn && ck[j] != key) ++j;
     if (j == cn) {
       ok = false;
       break;
     }
-    if ((static_cast<unsigned>(e.y) >> lane) & 1u) w |= 1u << j;
+    if ((static_cast<unsigned>(pat[pi + k].y) >> lane) & 1u) w |= 1u << j;
   }
   if (!ok && lane == 0) atomicExch(bad, 1);
-  bits[slice * kSliceRows + lane] = w;
+  // class-uniform diagonal: every owned row must hold key 0
+  int j0 = 0;
+  while (j0 < cn && ck[j0] != 0) ++j0;
+  const int64_t row = slice * kSliceRows + lane;
+  if (row < n_local && (j0 == cn || !((w >> j0) & 1u))) atomicOr(nodiag + lo, 1);
+  bits[row] = w;
 }
 
-void launch_cdia_bits(int64_t nslices, int ncls, const int64_t* starts, const int32_t* offs,
-                      const int32_t* nofs, const int64_t* meta, const int2* pat, uint32_t* bits,
-                      int* bad, cudaStream_t st) {
+void launch_cdia_bits(int64_t nslices, int64_t n_local, int ncls, const int64_t* starts,
+                      const int64_t* ckeys, const int32_t* nofs, const int64_t* meta,
+                      const int64_t* pkey, const int2* pat, uint32_t* bits, int* bad,
+                      int* nodiag, cudaStream_t st) {
   if (nslices == 0) return;
-  cdia_bits_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(nslices, ncls, starts, offs, nofs,
-                                                                meta, pat, bits, bad);
+  cdia_bits_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
+      nslices, n_local, ncls, starts, ckeys, nofs, meta, pkey, pat, bits, bad, nodiag);
   CS_CUDA(cudaGetLastError());
 }
 

@@ -201,19 +201,22 @@ struct EpiOps {
 };
 
 // epilogue operands of one row, loaded ahead of (independent of) the row sum
+// cinv != 0: the CDIA class's uniform Jacobi scale 1/a_ii (bitwise the
+// inv_diag entry, precond.cpp:22), so the D^-1 vector is not streamed.
 template <int KIND, bool JAC>
-__device__ __forceinline__ EpiOps epi_load(const SellView& a, const SpmvArgs& g, int64_t row) {
+__device__ __forceinline__ EpiOps epi_load(const SellView& a, const SpmvArgs& g, int64_t row,
+                                           double cinv = 0.0) {
   EpiOps e;
   if constexpr (KIND == kResid) e.e1 = g.b[row];
   if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
     e.e1 = g.zp1[row];
     if constexpr (KIND == kMpkMid) e.e2 = g.zp2[row];
-    if constexpr (JAC) e.einv = a.inv_diag[row];
+    if constexpr (JAC) e.einv = cinv != 0.0 ? cinv : a.inv_diag[row];
   }
   if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
     e.exd = g.x[row];
     if constexpr (KIND == kMpkMidF) e.e2 = g.zp2[row];
-    if constexpr (JAC) e.einv = a.inv_diag[row];
+    if constexpr (JAC) e.einv = cinv != 0.0 ? cinv : a.inv_diag[row];
   }
   if constexpr (KIND == kDot) e.exd = g.x[row];
   return e;
@@ -312,37 +315,21 @@ __device__ __noinline__ void halo_wait(const unsigned long long* ctr, unsigned l
   }
 }
 
+// signal side: the previous kernel's pushes are complete (stream order), so one
+// thread releases them. __threadfence_system() per pushing warp/block instead
+// compiled to MEMBAR.SC.SYS (+ CCTL.IVALL, wiping L1) hundreds of times per
+// launch and cost ~0.25 ms per exchange on B200.
+__device__ __forceinline__ void halo_release(const SpmvArgs& g) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (g.rel_lo) red_release_sys(g.rel_lo, g.rel_lo_n);
+    if (g.rel_hi) red_release_sys(g.rel_hi, g.rel_hi_n);
+  }
+}
+
 // producer side, per row: copy z into the neighbour's ghost slot
 __device__ __forceinline__ void halo_push_row(const SpmvArgs& g, int64_t row, double z) {
   if (g.push_lo != nullptr && row < g.send_lo) g.push_lo[row] = z;
   if (g.push_hi != nullptr && row >= g.hi_begin) g.push_hi[row - g.hi_begin] = z;
-}
-
-// producer side, once per block after its last row (every thread of the block
-// must call it): the block's pushed row counts are summed in shared memory and
-// thread 0 publishes them with one release reduction per peer. The barrier
-// orders every thread's remote stores before that release (cumulativity), so
-// no per-thread system fence is needed: __threadfence_system() would be
-// MEMBAR.SC.SYS + CCTL.IVALL, which also wipes the SM's L1 under the SpMV.
-__device__ __forceinline__ void halo_signal(const SpmvArgs& g, unsigned long long cnt_lo,
-                                            unsigned long long cnt_hi) {
-  __shared__ unsigned long long blk_cnt[2];
-  if (threadIdx.x == 0) blk_cnt[0] = blk_cnt[1] = 0ull;
-  __syncthreads();
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    cnt_lo += __shfl_xor_sync(0xffffffffu, cnt_lo, off);
-    cnt_hi += __shfl_xor_sync(0xffffffffu, cnt_hi, off);
-  }
-  if ((threadIdx.x & 31) == 0 && (cnt_lo | cnt_hi)) {
-    atomicAdd(&blk_cnt[0], cnt_lo);
-    atomicAdd(&blk_cnt[1], cnt_hi);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (blk_cnt[0]) red_release_sys(g.sig_lo, blk_cnt[0]);
-    if (blk_cnt[1]) red_release_sys(g.sig_hi, blk_cnt[1]);
-  }
 }
 
 __global__ void __launch_bounds__(256) halo_push_kernel(SpmvArgs g, const double* __restrict__ col,
@@ -350,23 +337,16 @@ __global__ void __launch_bounds__(256) halo_push_kernel(SpmvArgs g, const double
   if (st != nullptr && *(volatile int*)&st->done) return;
   const int64_t nlo = g.push_lo ? g.send_lo : 0;
   const int64_t nhi = g.push_hi ? n_local - g.hi_begin : 0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t total = nlo + nhi;
-  unsigned long long cl = 0, ch = 0;
-  // whole warps iterate together (trip count rounded up) so the warp shuffles see all lanes
-  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
-  for (int64_t base = w0; base < total; base += stride) {
-    const int64_t i = base + (threadIdx.x & 31);
-    if (i < nlo) {
-      g.push_lo[i] = col[i];
-      ++cl;
-    } else if (i < total) {
-      const int64_t r = i - nlo;
-      g.push_hi[r] = col[g.hi_begin + r];
-      ++ch;
-    }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nlo + nhi;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < nlo) g.push_lo[i] = col[i];
+    else g.push_hi[i - nlo] = col[g.hi_begin + i - nlo];
   }
-  halo_signal(g, cl, ch);
+}
+
+__global__ void halo_release_kernel(SpmvArgs g, DevState* st) {
+  if (st != nullptr && *(volatile int*)&st->done) return;
+  halo_release(g);
 }
 
 // ------------------------------------------------------------------ LDG kernel
@@ -378,6 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_S
     sell_kernel(SellView a, SpmvArgs g, int64_t slice_begin, int64_t slice_end,
                 const __grid_constant__ CdiaTable t) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
+  halo_release(g);
   if (g.wait_ctr != nullptr) {
     if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
     __syncthreads();
@@ -387,7 +368,6 @@ __global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_S
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
   constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
-  unsigned long long cnt_lo = 0, cnt_hi = 0;
   constexpr bool CD = CDN != 0;
   __shared__ SlotRec stab[CD ? 1 : kStabMax];
   const int staged = !CD && a.uniform ? stage_tables(a, stab) : 0;
@@ -412,7 +392,7 @@ __global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_S
     const int64_t row = phys(slice) * kSliceRows + lane;
     const bool own = row < a.n_local;
     EpiOps e;
-    if (own) e = epi_load<KIND, JAC>(a, g, row);
+    if (own) e = epi_load<KIND, JAC>(a, g, row, CD ? t.inv : 0.0);
     double acc;
     if constexpr (CD)
       acc = row_sum_cdia<(CDN > 0 ? CDN : 0)>(t, g.x, static_cast<int>(row), bits);
@@ -421,18 +401,12 @@ __global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_S
       double zv = 0.0;
       epi_store<KIND, JAC>(g, row, acc, e, dotv, zv);
       if constexpr (kPush) {
-        if (push) {
-          halo_push_row(g, row, zv);
-          cnt_lo += g.push_lo != nullptr && row < g.send_lo;
-          cnt_hi += g.push_hi != nullptr && row >= g.hi_begin;
-        }
+        if (push) halo_push_row(g, row, zv);
       }
     }
     sm = next;
     bits = bits_next;
   }
-  if constexpr (kPush)
-    if (push) halo_signal(g, cnt_lo, cnt_hi);
   if constexpr (KIND == kDot) dot_finish(g, dotv);
 }
 
@@ -623,7 +597,8 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
           const int64_t lo = std::max(r[0], a.cdia[k].s0), hi = std::min(r[1], a.cdia[k].s1);
           if (lo >= hi) continue;
           const unsigned grid = static_cast<unsigned>(spmv_grid(hi - lo, true));
-          const CdiaTable& t = a.cdia[k].t;
+          CdiaTable t = a.cdia[k].t;
+          t.inv = jac && t.diag != 0.0 ? 1.0 / t.diag : 0.0;  // IEEE, = inv_diag_kernel
 #define CSG_CD(N)                                                                        \
   do {                                                                                   \
     if (jac) sell_kernel<KIND, true, N><<<grid, kWarps * 32, 0, st>>>(a, g, lo, hi, t);  \
@@ -651,6 +626,11 @@ void launch_halo_push(const SpmvArgs& g, const double* col, int64_t n_local, Dev
   if (rows == 0) return;
   const int64_t blocks = std::min<int64_t>((rows + 255) / 256, 148 * 4);
   halo_push_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(g, col, n_local, st);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_halo_release(const SpmvArgs& g, DevState* st, cudaStream_t s) {
+  halo_release_kernel<<<1, 32, 0, s>>>(g, st);
   CS_CUDA(cudaGetLastError());
 }
 

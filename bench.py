@@ -329,7 +329,9 @@ def run_ours(args):
 
     # roofline per hot kernel family, the dominant one as "roofline"
     nnz_l = prob.nnz_local
-    mat = prob.device_bytes
+    # matrix bytes one SpMV streams: CDIA reads only the 32-bit participation
+    # words (its tables are kernel parameters); other formats their SELL arrays
+    mat = 4 * 32 * prob.slices if prob.cdia_classes > 0 else prob.device_bytes
     dstream = not prob.cdia_uniform_diag  # CDIA: 1/a_ii is a kernel constant
     alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode,
                                  diag_stream=dstream)

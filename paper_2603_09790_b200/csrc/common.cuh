@@ -90,6 +90,7 @@ struct CdiaTable {
 struct CdiaClass {  // host side
   int64_t s0, s1;
   CdiaTable t;
+  int64_t zstride;  // P if t is a 3 x 9 box stencil with groups P apart (P % 32 == 0), else 0
 };
 
 struct SellView {

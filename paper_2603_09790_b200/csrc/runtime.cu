@@ -579,6 +579,17 @@ void build_cdia(cs_problem* p) {
     p->pbits.release();
     return;
   }
+  for (size_t k = 0; k < cls.size(); ++k) {  // z-blocking structure (sell_zb_kernel)
+    const CdiaTable& t = cls[k].t;
+    cls[k].zstride = 0;
+    if (t.n != 27) continue;
+    const int64_t P = static_cast<int64_t>(t.off[9]) - t.off[0];
+    bool box = P > 0 && P % kSliceRows == 0;
+    for (int i = 0; i < 9 && box; ++i)
+      box = static_cast<int64_t>(t.off[9 + i]) - t.off[i] == P &&
+            static_cast<int64_t>(t.off[18 + i]) - t.off[9 + i] == P;
+    if (box) cls[k].zstride = P;
+  }
   for (size_t k = 0; k < cls.size(); ++k) {
     cls[k].t.diag = 0.0;
     if (hf[1 + k]) continue;

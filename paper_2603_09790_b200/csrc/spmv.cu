@@ -36,6 +36,12 @@ constexpr int kWarps = 8;  // warps per 256-thread block
 #ifndef CS_CD_KB
 #define CS_CD_KB 9  // CDIA gathers in flight per batch
 #endif
+#ifndef CS_SPMV_ZB
+#define CS_SPMV_ZB 1
+#endif
+#ifndef CS_SPMV_ZB_MINB
+#define CS_SPMV_ZB_MINB 3  // z-blocked kernel: two planes of gathers in flight
+#endif
 #ifndef CS_SPMV_CD_MINB
 #define CS_SPMV_CD_MINB 4  // CDIA kernel: 64 registers (all x gathers of a row in flight)
 #endif
@@ -410,6 +416,85 @@ __global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_S
   if constexpr (KIND == kDot) dot_finish(g, dotv);
 }
 
+// ------------------------------------------------------------------ z-blocked CDIA kernel
+// A 27-entry class whose table is three groups of nine offsets a plane apart
+// (off[9+i] = off[i] + P, off[18+i] = off[9+i] + P: a box stencil in natural
+// ordering) lets one lane compute the rows r and r + P together: their 54
+// neighbours are only 36 distinct x values (planes z-1, z, z+1, z+2), so each
+// is gathered once and feeds both rows' sums, each row still adding its
+// entries in its own stored order (group 0, 1, 2). Slice pairs (s, s + P/32)
+// tile a range of whole plane pairs.
+template <int KIND, bool JAC>
+__global__ void __launch_bounds__(kWarps * 32, CS_SPMV_ZB_MINB)
+    sell_zb_kernel(SellView a, SpmvArgs g, int64_t lo, int64_t npairs, int64_t sp,
+                   const __grid_constant__ CdiaTable t) {
+  if (g.st != nullptr && *(volatile int*)&g.st->done) return;
+  halo_release(g);
+  if (g.wait_ctr != nullptr) {
+    if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
+  const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
+  const int P = static_cast<int>(sp * kSliceRows);
+  const double* __restrict__ x = g.x;
+  double dotv = 0.0;
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * kWarps + warp; v < npairs; v += wstride) {
+    const int64_t q = v / sp, w = v - q * sp;
+    const int64_t s1 = lo + 2 * q * sp + w;
+    const int ra = static_cast<int>(s1 * kSliceRows + lane), rb = ra + P;
+    const bool own_a = ra < a.n_local, own_b = rb < a.n_local;
+    const uint32_t ba = __ldcs(a.pbits + ra), bb = __ldcs(a.pbits + rb);
+    EpiOps ea, eb;
+    if (own_a) ea = epi_load<KIND, JAC>(a, g, ra, t.inv);
+    if (own_b) eb = epi_load<KIND, JAC>(a, g, rb, t.inv);
+    double acc_a = 0.0, acc_b = 0.0;
+    double L0[9], L1[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      L0[i] = ((ba >> i) & 1u) ? __ldg(x + (ra + t.off[i])) : 0.0;
+      L1[i] = (((ba >> (9 + i)) | (bb >> i)) & 1u) ? __ldg(x + (ra + t.off[9 + i])) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      if ((ba >> i) & 1u) acc_a = __dadd_rn(acc_a, __dmul_rn(t.v[i], L0[i]));
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      L0[i] = (((ba >> (18 + i)) | (bb >> (9 + i))) & 1u) ? __ldg(x + (ra + t.off[18 + i])) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if ((ba >> (9 + i)) & 1u) acc_a = __dadd_rn(acc_a, __dmul_rn(t.v[9 + i], L1[i]));
+      if ((bb >> i) & 1u) acc_b = __dadd_rn(acc_b, __dmul_rn(t.v[i], L1[i]));
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      L1[i] = ((bb >> (18 + i)) & 1u) ? __ldg(x + (rb + t.off[18 + i])) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if ((ba >> (18 + i)) & 1u) acc_a = __dadd_rn(acc_a, __dmul_rn(t.v[18 + i], L0[i]));
+      if ((bb >> (9 + i)) & 1u) acc_b = __dadd_rn(acc_b, __dmul_rn(t.v[9 + i], L0[i]));
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      if ((bb >> (18 + i)) & 1u) acc_b = __dadd_rn(acc_b, __dmul_rn(t.v[18 + i], L1[i]));
+    if (own_a) {
+      double zv = 0.0;
+      epi_store<KIND, JAC>(g, ra, acc_a, ea, dotv, zv);
+      if constexpr (kPush)
+        if (push) halo_push_row(g, ra, zv);
+    }
+    if (own_b) {
+      double zv = 0.0;
+      epi_store<KIND, JAC>(g, rb, acc_b, eb, dotv, zv);
+      if constexpr (kPush)
+        if (push) halo_push_row(g, rb, zv);
+    }
+  }
+  if constexpr (KIND == kDot) dot_finish(g, dotv);
+}
+
 // ------------------------------------------------------------------ TMA kernel
 // A block owns tiles of kWarps consecutive slices; their value slots are one
 // contiguous range of `vals`, streamed into shared memory by a single
@@ -583,32 +668,57 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
     else tma_launch<KIND, false>(a, g, sb, se, st);
     return;
   }
-  // CDIA: one launch per (class x physical range) piece; kDot finalises one sum
-  // per launch, so a multi-piece kDot takes the table kernel instead
+  // CDIA: one launch per (class x physical range) piece -- z-blocked over whole
+  // plane pairs where the class allows it, the rest row-wise. kDot finalises
+  // one sum per launch, so a multi-launch kDot takes the table kernel instead.
+  // Only the first launch releases the previous kernel's peer pushes.
   if (a.ncdia > 0) {
-    int64_t piece[2][2] = {{sb, se < a.nslices ? se : a.nslices}, {0, se - a.nslices}};
-    int count = 0;
-    for (auto& r : piece)
-      for (int k = 0; k < a.ncdia; ++k)
-        count += std::max(r[0], a.cdia[k].s0) < std::min(r[1], a.cdia[k].s1);
-    if (KIND != kDot || count == 1) {
-      for (auto& r : piece)
-        for (int k = 0; k < a.ncdia; ++k) {
-          const int64_t lo = std::max(r[0], a.cdia[k].s0), hi = std::min(r[1], a.cdia[k].s1);
-          if (lo >= hi) continue;
-          const unsigned grid = static_cast<unsigned>(spmv_grid(hi - lo, true));
-          CdiaTable t = a.cdia[k].t;
-          t.inv = jac && t.diag != 0.0 ? 1.0 / t.diag : 0.0;  // IEEE, = inv_diag_kernel
-#define CSG_CD(N)                                                                        \
-  do {                                                                                   \
-    if (jac) sell_kernel<KIND, true, N><<<grid, kWarps * 32, 0, st>>>(a, g, lo, hi, t);  \
-    else sell_kernel<KIND, false, N><<<grid, kWarps * 32, 0, st>>>(a, g, lo, hi, t);     \
+    struct Piece {
+      int k;
+      int64_t lo, hi, sp;  // sp > 0: z-blocked, hi - lo = 2 * pairs
+    };
+    Piece list[2 * 64 * 2];
+    int np = 0;
+    const int64_t ranges[2][2] = {{sb, se < a.nslices ? se : a.nslices}, {0, se - a.nslices}};
+    for (const auto& r : ranges)
+      for (int k = 0; k < a.ncdia; ++k) {
+        int64_t lo = std::max(r[0], a.cdia[k].s0);
+        const int64_t hi = std::min(r[1], a.cdia[k].s1);
+        if (lo >= hi) continue;
+        const int64_t sp = CS_SPMV_ZB ? a.cdia[k].zstride / kSliceRows : 0;
+        if (sp > 0 && hi - lo >= 2 * sp) {
+          const int64_t span = (hi - lo) / (2 * sp) * (2 * sp);
+          list[np++] = {k, lo, lo + span, sp};
+          lo += span;
+        }
+        if (lo < hi) list[np++] = {k, lo, hi, 0};
+      }
+    if (KIND != kDot || np == 1) {
+      SpmvArgs gg = g;
+      for (int e = 0; e < np; ++e) {
+        const Piece& pc = list[e];
+        CdiaTable t = a.cdia[pc.k].t;
+        t.inv = jac && t.diag != 0.0 ? 1.0 / t.diag : 0.0;  // IEEE, = inv_diag_kernel
+        if (pc.sp > 0) {
+          const int64_t pairs = (pc.hi - pc.lo) / 2;
+          const unsigned zg = static_cast<unsigned>(std::min<int64_t>(
+              std::max<int64_t>((pairs + kWarps - 1) / kWarps, 1), 148 * CS_SPMV_ZB_MINB));
+          if (jac) sell_zb_kernel<KIND, true><<<zg, kWarps * 32, 0, st>>>(a, gg, pc.lo, pairs, pc.sp, t);
+          else sell_zb_kernel<KIND, false><<<zg, kWarps * 32, 0, st>>>(a, gg, pc.lo, pairs, pc.sp, t);
+        } else {
+          const unsigned grid = static_cast<unsigned>(spmv_grid(pc.hi - pc.lo, true));
+#define CSG_CD(N)                                                                                \
+  do {                                                                                           \
+    if (jac) sell_kernel<KIND, true, N><<<grid, kWarps * 32, 0, st>>>(a, gg, pc.lo, pc.hi, t);   \
+    else sell_kernel<KIND, false, N><<<grid, kWarps * 32, 0, st>>>(a, gg, pc.lo, pc.hi, t);      \
   } while (0)
           if (t.n == 27) CSG_CD(27);
           else if (t.n == 7) CSG_CD(7);
           else CSG_CD(-1);
 #undef CSG_CD
         }
+        gg.rel_lo = gg.rel_hi = nullptr;
+      }
       return;
     }
   }

@@ -213,21 +213,28 @@ bool p2p_setup(cs_problem* p, double* Z) {
   // reset before any peer's first push
   if (p->sig.p) CS_CUDA(cudaMemsetAsync(p->sig.p, 0, 64, c->stream));
   PeerInfo mine{};
-  if (ok) {
-    ok = cudaIpcGetMemHandle(&mine.ws, p->ws.p) == cudaSuccess &&
-         cudaIpcGetMemHandle(&mine.sig, p->sig.p) == cudaSuccess;
+  if (ok && p->ipc_gen != p->ws_gen) {  // export handles once per workspace generation
+    ok = cudaIpcGetMemHandle(&p->ipc_ws, p->ws.p) == cudaSuccess &&
+         cudaIpcGetMemHandle(&p->ipc_sig, p->sig.p) == cudaSuccess;
     cudaGetLastError();
+    if (ok) p->ipc_gen = p->ws_gen;
+  }
+  if (ok) {
+    mine.ws = p->ipc_ws;
+    mine.sig = p->ipc_sig;
   }
   mine.gen = p->ws_gen;
   mine.z_off = Z - p->ws.as<double>();
   mine.ld = p->ld;
   mine.n_local = p->n_local;
   mine.ghost_lo = p->ghost_lo;
-  {
+  if (!c->uuid_known) {  // cudaGetDeviceProperties costs milliseconds: once per context
     cudaDeviceProp prop;
     CS_CUDA(cudaGetDeviceProperties(&prop, c->device));
-    std::memcpy(mine.uuid, prop.uuid.bytes, 16);
+    std::memcpy(c->uuid, prop.uuid.bytes, 16);
+    c->uuid_known = true;
   }
+  std::memcpy(mine.uuid, c->uuid, 16);
   mine.ok = ok;
   DBuf dev(3 * sizeof(PeerInfo));
   PeerInfo* d = dev.as<PeerInfo>();

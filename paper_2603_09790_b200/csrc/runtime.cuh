@@ -108,6 +108,8 @@ struct cs_ctx {
   csg::DBuf normbuf;    // ||b|| reduction scratch
   size_t scratch_bytes = 0;
   void* pinned = nullptr;  // pinned host staging for flags
+  unsigned char uuid[16] = {};
+  bool uuid_known = false;
 };
 
 struct cs_problem {
@@ -153,6 +155,8 @@ struct cs_problem {
   csg::DBuf sig;                    // my receive counters [from rank-1, from rank+1] (IPC-exported)
   int64_t z_off = 0;                // element offset of Z in ws
   bool p2p = false;                 // peer mappings valid for the current ws
+  uint64_t ipc_gen = 0;             // ws generation of ipc_ws
+  cudaIpcMemHandle_t ipc_ws{}, ipc_sig{};
   unsigned long long p2p_epoch = 0; // halo exchanges consumed in the current solve
   bool p2p_pending = false;         // the last kernel pushed rows not yet released
   csg::SellView view() const {

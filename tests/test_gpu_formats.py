@@ -1,0 +1,72 @@
+"""Every device storage format gives the same bits.
+
+The conversion SELL-32 -> SELL-32P -> SELL-32PU -> CDIA is chosen per slice
+from the matrix; environment switches force the earlier formats:
+CS_SELL_EXPLICIT=1 (explicit int32 columns everywhere), CS_SELL_VALUES=1
+(pattern slices keep their value slots), CS_SELL_CDIA=0 (uniform tables, no
+constant-diagonal classes). For each format: the SpMV equals the CPU oracle
+bit for bit, and a fast-algebra solve is bitwise identical to the default
+format's (same spectrum injected)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FORMATS = {
+    "explicit": {"CS_SELL_EXPLICIT": "1"},
+    "pattern_values": {"CS_SELL_VALUES": "1"},
+    "uniform_tables": {"CS_SELL_CDIA": "0"},
+    "cdia": {},
+}
+CASES = [("poisson27", (32, 32, 32), None), ("poisson27", (33, 17, 9), None),
+         ("poisson7", (24, 24, 24), None), ("aniso7", (20, 18, 16), (1.0, 1.0, 100.0))]
+
+
+def _generate(cs, kind, dims, coef, env):
+    old = {k: os.environ.get(k) for k in ("CS_SELL_EXPLICIT", "CS_SELL_VALUES", "CS_SELL_CDIA")}
+    try:
+        for k in old:
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        return cs.DeviceProblem.generate(kind, *dims, coef or (1.0, 1.0, 1.0)).set_precond("jacobi")
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _oracle(port, kind, dims, coef):
+    if kind == "poisson27":
+        return port.poisson27(*dims)
+    return port.stencil7(*dims, coef=coef or (1.0, 1.0, 1.0))
+
+
+@pytest.mark.parametrize("kind,dims,coef", CASES)
+def test_formats_spmv_and_solve_bitwise(cs, port, kind, dims, coef):
+    o = _oracle(port, kind, dims, coef)
+    x = np.random.default_rng(5).standard_normal(o.n)
+    want = port.spmv(o, x)
+    sols = {}
+    for name, env in FORMATS.items():
+        p = _generate(cs, kind, dims, coef, env)
+        try:
+            if name == "cdia":
+                assert p.cdia_classes >= 1, "stencils convert to constant-diagonal classes"
+            if name == "explicit":
+                assert p.pattern_slices == 0
+            if name == "pattern_values":
+                assert p.uniform_slices == 0 and p.pattern_slices > 0
+            y = p.spmv(x)
+            assert y.tobytes() == want.tobytes(), name
+            lam = cs.SpectrumEstimate(*port.estimate_interval(o, 1))
+            r = p.pcg_s_solve(cfg=cs.SolverConfig(s=4, tol=1e-8, max_outer=2000, spectrum=lam))
+            sols[name] = (r.x.tobytes(), r.report.outer_iters)
+        finally:
+            p.close()
+    ref = sols["cdia"]
+    for name, v in sols.items():
+        assert v == ref, f"{name} differs from the CDIA solve"

@@ -165,6 +165,12 @@ struct UpdateArgs {
   const double* alpha;   // device s
   const double* beta;    // device s x s, nullptr = no block update
   DevState* st;
+  // NVLink peer halo of z_0 (fast MPK, see SpmvArgs): rows [0, send_lo) also to
+  // push_lo[row], rows [hi_begin, n) to push_hi[row - hi_begin]; released by
+  // the next kernel on the stream
+  double* push_lo = nullptr;
+  double* push_hi = nullptr;
+  int64_t send_lo = 0, hi_begin = 0;
 };
 void launch_fast_update(const UpdateArgs& a, cudaStream_t s);  // beta block update + x/r + z0
 void launch_ref_xr_update(const UpdateArgs& a, cudaStream_t s);   // solver.cpp:159-162

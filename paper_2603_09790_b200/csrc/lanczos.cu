@@ -117,15 +117,27 @@ __global__ void __launch_bounds__(kThreads)
   double acc[kMdCols];
 #pragma unroll
   for (int k = 0; k < kMdCols; ++k) acc[k] = 0.0;
+  // kMdUnroll tiles per iteration: their loads are independent, so a warp keeps
+  // kMdUnroll x (1 + its columns) 256-byte loads in flight (one tile per
+  // iteration left the pass latency-bound for the first, narrow steps)
+  constexpr int kMdUnroll = 4;
   const int64_t tiles = (n + 31) / 32;
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t i = t * 32 + lane;
-    if (i < n) {
-      const double rv = r[i];
+  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMdUnroll; t0 < tiles;
+       t0 += static_cast<int64_t>(gridDim.x) * kMdUnroll) {
+    double rv[kMdUnroll];
 #pragma unroll
-      for (int k = 0; k < kMdCols; ++k) {
-        const int c = warp + 8 * k;
-        if (c < m) acc[k] = fma(G[c * ld + i], rv, acc[k]);
+    for (int u = 0; u < kMdUnroll; ++u) {
+      const int64_t i = (t0 + u) * 32 + lane;
+      rv[u] = i < n ? r[i] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kMdCols; ++k) {
+      const int c = warp + 8 * k;
+      if (c >= m) break;
+#pragma unroll
+      for (int u = 0; u < kMdUnroll; ++u) {
+        const int64_t i = (t0 + u) * 32 + lane;
+        if (i < n) acc[k] = fma(G[c * ld + i], rv[u], acc[k]);
       }
     }
   }

@@ -635,11 +635,19 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   auto outer_fast = [&](bool first) {
     ua.beta = first ? nullptr : beta_d;
     ua.zw = bk.Z;  // z_0 = M^-1 r_k for the next MPK
+    if (p2p) {  // z_0's boundary rows go to the neighbours from the update pass itself
+      SpmvArgs pa;
+      fill_push_args(p, pa, 0);
+      ua.push_lo = pa.push_lo;
+      ua.push_hi = pa.push_hi;
+      ua.send_lo = pa.send_lo;
+      ua.hi_begin = pa.hi_begin;
+    }
     {
       Launch L(c, CS_PHASE_UPDATE);
       launch_fast_update(ua, c->stream);
     }
-    if (p2p) p2p_push(p, bk.Z, 0, st);
+    if (p2p) p->p2p_pending = true;  // released by the first MPK step's interior launch
     mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true, p2p);
     packed_reduce(bk.Q, bk.Z);
     small(launch_fast_step);

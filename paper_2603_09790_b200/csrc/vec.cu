@@ -387,6 +387,8 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
     if (aq_role) {
       const double z = a.inv_diag ? __dmul_rn(a.inv_diag[i], acc) : acc;
       a.zw[i] = z;
+      if (a.push_lo != nullptr && i < a.send_lo) a.push_lo[i] = z;
+      if (a.push_hi != nullptr && i >= a.hi_begin) a.push_hi[i - a.hi_begin] = z;
       if (!isfinite(z)) atomicCAS(&a.st->pending, 0ull, make_err(4, 0));
     }
   }

@@ -100,71 +100,6 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Fast CGS projections h_c = g_c . r for c < m in ONE pass: the 8 warps of a
-// block walk the same 32-row tiles (r is read from HBM once, then hits L1),
-// warp w owning columns w, w+8, ... (<= kMdCols each); per-block partials are
-// finalised by the last block in a fixed order.
-constexpr int kMdCols = 8;  // m <= 8 * kMdCols
-constexpr int kMdBlocks = 296;
-
-__global__ void __launch_bounds__(kThreads)
-    multidot_kernel(int64_t n, int64_t ld, int m, const double* __restrict__ G,
-                    const double* __restrict__ r, double* partial, unsigned* ticket, double* out,
-                    DevState* st) {
-  if (halted(st)) return;
-  __shared__ bool last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double acc[kMdCols];
-#pragma unroll
-  for (int k = 0; k < kMdCols; ++k) acc[k] = 0.0;
-  // kMdUnroll tiles per iteration: their loads are independent, so a warp keeps
-  // kMdUnroll x (1 + its columns) 256-byte loads in flight (one tile per
-  // iteration left the pass latency-bound for the first, narrow steps)
-  constexpr int kMdUnroll = 4;
-  const int64_t tiles = (n + 31) / 32;
-  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kMdUnroll; t0 < tiles;
-       t0 += static_cast<int64_t>(gridDim.x) * kMdUnroll) {
-    double rv[kMdUnroll];
-#pragma unroll
-    for (int u = 0; u < kMdUnroll; ++u) {
-      const int64_t i = (t0 + u) * 32 + lane;
-      rv[u] = i < n ? r[i] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < kMdCols; ++k) {
-      const int c = warp + 8 * k;
-      if (c >= m) break;
-#pragma unroll
-      for (int u = 0; u < kMdUnroll; ++u) {
-        const int64_t i = (t0 + u) * 32 + lane;
-        if (i < n) acc[k] = fma(G[c * ld + i], rv[u], acc[k]);
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < kMdCols; ++k) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], off);
-    const int c = warp + 8 * k;
-    if (lane == 0 && c < m) partial[static_cast<int64_t>(blockIdx.x) * m + c] = acc[k];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
-      double sum = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(partial + static_cast<int64_t>(b) * m + c);
-      out[c] = sum;
-    }
-    if (threadIdx.x == 0) *ticket = 0u;
-  }
-}
-
 // scalar steps: 0 normalise start (nrm = sqrt(v.g) > 0), 1 alpha_j (finite),
 // 2 beta_j = sqrt(max(0, r.gr)) with the invariant-subspace exit.
 __global__ void scalar_kernel(int which, int j, int steps, LanczosScalars* sc, DevState* st) {
@@ -221,14 +156,6 @@ void lz_axpy2(int64_t n, const double* v, const double* g, double* r, double* gr
   if (n == 0) return;
   axpy2_kernel<<<grid_for(n), kThreads, 0, s>>>(n, v, g, r, gr, proj, st);
   CS_CUDA(cudaGetLastError());
-}
-
-bool lz_multidot(int64_t n, int64_t ld, int m, const double* G, const double* r, double* out,
-                 double* partial, unsigned* ticket, DevState* st, cudaStream_t s) {
-  if (m > 8 * kMdCols) return false;
-  multidot_kernel<<<kMdBlocks, kThreads, 0, s>>>(n, ld, m, G, r, partial, ticket, out, st);
-  CS_CUDA(cudaGetLastError());
-  return true;
 }
 
 int lz_cgs_blocks(int64_t n) { return static_cast<int>(grid_for(n > 0 ? n : 1)); }

@@ -20,9 +20,6 @@ void lz_resid(int64_t n, const double* t, const double* inv_diag, const double* 
               const LanczosScalars* sc, int j, DevState* st, cudaStream_t s);
 void lz_axpy2(int64_t n, const double* v, const double* g, double* r, double* gr,
               const double* proj, DevState* st, cudaStream_t s);
-// out[c] = g_c . r for c < m, one pass (partial: 296*m doubles); false if m > 64
-bool lz_multidot(int64_t n, int64_t ld, int m, const double* G, const double* r, double* out,
-                 double* partial, unsigned* ticket, DevState* st, cudaStream_t s);
 int lz_cgs_blocks(int64_t n);
 void lz_cgs(int64_t n, int64_t ld, int m, const double* V, const double* G, double* r, double* gr,
             const double* proj, double* partial, unsigned* ticket, double* result, DevState* st,

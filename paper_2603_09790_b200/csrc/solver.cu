@@ -217,8 +217,7 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
     } else {
       {  // classical Gram-Schmidt: all projections in one pass
         auto l = L();
-        if (!lz_multidot(n, ld, j + 1, G, r, sc->proj, partial, ticket + 2, st, c->stream))
-          launch_tree_gram(n, j + 1, 1, G, ld, r, ld, sc->proj, partial, ticket + 2, st, c->stream);
+        launch_tree_gram(n, j + 1, 1, G, ld, r, ld, sc->proj, partial, ticket + 2, st, c->stream);
       }
       allreduce_sum(c, sc->proj, j + 1);
       auto l = L();

@@ -345,7 +345,8 @@ def run_ours(args):
         # Q, Z, P, r read once (one launch per outer + the setup one)
         "reduce": (outers_t + len(reps_t)) * v8 * (3 * args.s + 1),
     }
-    names = {"spmv": "sell_kernel<kMpk*> (SELL-32PU FP64 SpMV + fused MPK epilogue)",
+    names = {"spmv": "sell_zb_kernel / sell_kernel<kMpk*, CDIA> (FP64 SpMV over the constant-"
+                     "diagonal class table + fused MPK epilogue)",
              "update": "update_kernel<s,beta,xr,z0> (Q, AQ, x, r, z_0 update pass)",
              "reduce": "pack_kernel<s> (packed Gram/projection block, DMMA)"}
     peak, peak_src = measured_peak()

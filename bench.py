@@ -165,7 +165,7 @@ def outer_bytes_format(mat_bytes, n, s, diag_stream=True):
     j = v if diag_stream else 0
     mpk = (mat_bytes + 3 * v + j) + (s - 2) * (mat_bytes + 4 * v + j) + (mat_bytes + 2 * v) \
         if s > 1 else mat_bytes + 2 * v
-    return mpk + v * (3 * s + 1) + v * (6 * s + 6)
+    return mpk + v * (3 * s + 1) + v * (6 * s + (6 if diag_stream else 5))
 
 
 def outer_bytes(nnz, n, s):
@@ -340,8 +340,8 @@ def run_ours(args):
     alg_phase = {
         "spmv": sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps,
                                    args.mode, diag_stream=dstream)[0] for r in reps_t),
-        # Q, Z, AQ, P, x, r, D^-1 read; Q, AQ, x, r, z_0 written (one launch per outer)
-        "update": outers_t * v8 * (6 * args.s + 6),
+        # Q, Z, AQ, P, x, r (+ D^-1 unless uniform) read; Q, AQ, x, r, z_0 written
+        "update": outers_t * v8 * (6 * args.s + (6 if dstream else 5)),
         # Q, Z, P, r read once (one launch per outer + the setup one)
         "reduce": (outers_t + len(reps_t)) * v8 * (3 * args.s + 1),
     }

@@ -162,6 +162,7 @@ struct UpdateArgs {
   double* x;
   double* r;
   const double* inv_diag;  // nullptr = identity
+  double inv_const = 0.0;  // != 0: every row's 1/a_ii (uniform diagonal): no D^-1 stream
   const double* alpha;   // device s
   const double* beta;    // device s x s, nullptr = no block update
   DevState* st;

@@ -562,6 +562,12 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   ua.x = bk.x;
   ua.r = bk.r;
   ua.inv_diag = A.inv_diag;
+  {  // one diagonal value for every row (constant-coefficient stencils): 1/a_ii as a constant
+    double d0 = A.ncdia > 0 ? A.cdia[0].t.diag : 0.0;
+    for (int k = 1; k < A.ncdia; ++k)
+      if (std::memcmp(&A.cdia[k].t.diag, &d0, sizeof d0) != 0) d0 = 0.0;
+    ua.inv_const = A.inv_diag != nullptr && d0 != 0.0 ? 1.0 / d0 : 0.0;  // = inv_diag_kernel
+  }
   ua.alpha = alpha_d;
   ua.st = st;
 

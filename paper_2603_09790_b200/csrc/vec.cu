@@ -385,7 +385,9 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
   }
   if constexpr (Z0) {
     if (aq_role) {
-      const double z = a.inv_diag ? __dmul_rn(a.inv_diag[i], acc) : acc;
+      const double z = !a.inv_diag        ? acc
+                       : a.inv_const != 0.0 ? __dmul_rn(a.inv_const, acc)
+                                            : __dmul_rn(a.inv_diag[i], acc);
       a.zw[i] = z;
       if (a.push_lo != nullptr && i < a.send_lo) a.push_lo[i] = z;
       if (a.push_hi != nullptr && i >= a.hi_begin) a.push_hi[i - a.hi_begin] = z;

@@ -133,6 +133,10 @@ __device__ void fgs_fast_generic(int s, const double* W, int k, const double* rh
 // gram.cpp:78-119. Returns 0 or the NotSpd sub-code. x, tmp: s*k.
 // fast = reassociated sweeps (fast algebra only); otherwise the reference's
 // exact operation sequence.
+// S > 0: the order is known at compile time and only that register variant is
+// instantiated (the runtime switch inlines every variant: ~14k SASS instructions
+// in one kernel, whose instruction-cache misses ncu showed as the top stall).
+template <int S = 0>
 __device__ int fgs_dev(int s, const double* W, int k, const double* rhs, int nu, double* x,
                        double* delta, double* tmp, bool fast = false) {
   for (int i = 0; i < s; ++i)
@@ -144,6 +148,13 @@ __device__ int fgs_dev(int s, const double* W, int k, const double* rhs, int nu,
   const double rn = rn_sh;
   if (rn == 0.0) {
     *delta = 0.0;
+    return 0;
+  }
+  if constexpr (S > 0) {
+    if (fast) fgs_fast_reg<S>(W, k, rhs, nu, x);
+    else fgs_columns_reg<S>(W, k, rhs, nu, x);
+    __syncthreads();
+    *delta = gram_residual(s, W, k, rhs, x, rn, tmp);
     return 0;
   }
   if (fast) {
@@ -232,9 +243,10 @@ __device__ int chol_dev(int s, const double* W, int k, const double* rhs, double
   return 0;
 }
 
+template <int S = 0>
 __device__ int solve_dev(const SmallArgs& a, const double* W, int k, const double* rhs, double* x,
                          double* delta, double* scratch, bool fast = false) {
-  if (a.gram == 0) return fgs_dev(a.s, W, k, rhs, a.nu, x, delta, scratch, fast);
+  if (a.gram == 0) return fgs_dev<S>(a.s, W, k, rhs, a.nu, x, delta, scratch, fast);
   return chol_dev(a.s, W, k, rhs, x, delta, scratch, scratch + a.s * a.s);
 }
 
@@ -280,6 +292,7 @@ __device__ __forceinline__ bool halted(const DevState* st) {
 
 // After setup MPK(r0) and the packed reduction with Q = Z: W_1 = sym(Z^T P),
 // b1 = Z^T r0, rel[0] = sqrt(r0.r0)/||b||; alpha_1.
+template <int S>
 __global__ void fast_setup_kernel(SmallArgs a) {
   DevState* st = a.st;
   if (halted(st)) return;
@@ -298,7 +311,7 @@ __global__ void fast_setup_kernel(SmallArgs a) {
     return;
   }
   double delta;
-  const int bad = solve_dev(a, m.W, 1, m.rhs, m.x, &delta, m.scr, true);
+  const int bad = solve_dev<S>(a, m.W, 1, m.rhs, m.x, &delta, m.scr, true);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, 1);
     return;
@@ -315,6 +328,7 @@ __global__ void fast_setup_kernel(SmallArgs a) {
 // End of outer k: stop test on r_k, beta_k = FGS(W_k, -G1), then the
 // one-allreduce recurrence W_{k+1} = G2 + G1^T b + b^T G1 + b^T W_k b,
 // b1_{k+1} = c1 + b^T c2 and alpha_{k+1}.
+template <int S>
 __global__ void fast_step_kernel(SmallArgs a) {
   DevState* st = a.st;
   if (halted(st)) return;
@@ -350,7 +364,7 @@ __global__ void fast_step_kernel(SmallArgs a) {
   __syncthreads();
   if (stop) return;
   double delta;
-  int bad = solve_dev(a, m.W, s, m.rhs, m.x, &delta, m.scr, true);
+  int bad = solve_dev<S>(a, m.W, s, m.rhs, m.x, &delta, m.scr, true);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, k);
     return;
@@ -391,7 +405,7 @@ __global__ void fast_step_kernel(SmallArgs a) {
     if (threadIdx.x == 0) raise(st, 5, kSubAssembly, k + 1);
     return;
   }
-  bad = solve_dev(a, m.Wn, 1, m.rhs, m.x, &delta, m.scr, true);
+  bad = solve_dev<S>(a, m.Wn, 1, m.rhs, m.x, &delta, m.scr, true);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, k + 1);
     return;
@@ -603,8 +617,19 @@ void launch_small(K kern, const SmallArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-void launch_fast_setup(const SmallArgs& a, cudaStream_t s) { launch_small(fast_setup_kernel, a, s); }
-void launch_fast_step(const SmallArgs& a, cudaStream_t s) { launch_small(fast_step_kernel, a, s); }
+#define CSG_SMALL_DISPATCH(KERNEL, a, st)                    \
+  switch ((a).s) {                                          \
+    case 2: launch_small(KERNEL<2>, a, st); break;          \
+    case 3: launch_small(KERNEL<3>, a, st); break;          \
+    case 4: launch_small(KERNEL<4>, a, st); break;          \
+    case 5: launch_small(KERNEL<5>, a, st); break;          \
+    case 6: launch_small(KERNEL<6>, a, st); break;          \
+    case 8: launch_small(KERNEL<8>, a, st); break;          \
+    default: launch_small(KERNEL<0>, a, st);                \
+  }
+void launch_fast_setup(const SmallArgs& a, cudaStream_t s) { CSG_SMALL_DISPATCH(fast_setup_kernel, a, s); }
+void launch_fast_step(const SmallArgs& a, cudaStream_t s) { CSG_SMALL_DISPATCH(fast_step_kernel, a, s); }
+#undef CSG_SMALL_DISPATCH
 void launch_ref_alpha(const SmallArgs& a, cudaStream_t s) { launch_small(ref_alpha_kernel, a, s); }
 void launch_ref_test(const SmallArgs& a, cudaStream_t s) {
   ref_test_kernel<<<1, 1, 0, s>>>(a);

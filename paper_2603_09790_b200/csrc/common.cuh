@@ -91,6 +91,9 @@ struct CdiaClass {  // host side
   int64_t s0, s1;
   CdiaTable t;
   int64_t zstride;  // P if t is a 3 x 9 box stencil with groups P apart (P % 32 == 0), else 0
+  // 3x3x3 box in natural ordering, off[9g+3i+j] = g*P + i*L + j - (P+L+1)
+  // (P % 4 == 0, P >= 3L, L >= 3): plane-streaming kernel (sell_box_kernel)
+  int64_t boxP = 0, boxL = 0;
 };
 
 struct SellView {
@@ -110,6 +113,7 @@ struct SellView {
   const uint32_t* pbits;                // CDIA participation words (device), or nullptr
   const CdiaClass* cdia;                // CDIA classes (HOST pointer; launchers only)
   int ncdia;
+  int64_t xlen;                         // elements of every SpMV operand (owned + ghost, even)
 };
 
 __host__ __device__ inline unsigned long long make_err(int code, int payload) {

@@ -591,7 +591,7 @@ void build_cdia(cs_problem* p) {
     cls[k].zstride = 0;
     if (t.n != 27) continue;
     const int64_t P = static_cast<int64_t>(t.off[9]) - t.off[0];
-    bool box = P > 0 && P % kSliceRows == 0;
+    bool box = P > 0;
     for (int i = 0; i < 9 && box; ++i)
       box = static_cast<int64_t>(t.off[9 + i]) - t.off[i] == P &&
             static_cast<int64_t>(t.off[18 + i]) - t.off[9 + i] == P;
@@ -599,7 +599,18 @@ void build_cdia(cs_problem* p) {
     // only where the plane stride is a power of two -- there the three planes of
     // a row's neighbours alias in L1 and the row-wise kernel loses ~10%;
     // elsewhere the row-wise kernel is ~7% faster
-    if (box && (P & (P - 1)) == 0) cls[k].zstride = P;
+    if (box && P % kSliceRows == 0 && (P & (P - 1)) == 0) cls[k].zstride = P;
+    cls[k].boxP = cls[k].boxL = 0;
+    const int64_t L = static_cast<int64_t>(t.off[3]) - t.off[0];
+    bool box3 = box && L >= 3 && P >= 3 * L && P % 4 == 0 && t.off[13] == 0;
+    for (int g = 0; g < 3 && box3; ++g)
+      for (int i = 0; i < 3 && box3; ++i)
+        for (int j = 0; j < 3 && box3; ++j)
+          box3 = t.off[9 * g + 3 * i + j] == g * P + i * L + j - (P + L + 1);
+    if (box3) {
+      cls[k].boxP = P;
+      cls[k].boxL = L;
+    }
   }
   for (size_t k = 0; k < cls.size(); ++k) {
     cls[k].t.diag = 0.0;

@@ -176,6 +176,7 @@ struct cs_problem {
     v.cdia = cdia.data();
     v.ncdia = static_cast<int>(cdia.size());
     v.max_width = max_width;
+    v.xlen = (n_local + n_ghost + 1) / 2 * 2;
     v.inv_diag = precond == CS_PRECOND_JACOBI ? inv_diag.as<double>() : nullptr;
     return v;
   }

@@ -23,6 +23,9 @@
 //              D = a_ii and z_{q-1}[row] are picked up by the row loop itself, so
 //              the step reads/writes 24n fewer bytes than the reference recurrence.
 #include <algorithm>
+#include <cstdint>
+#include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -625,6 +628,280 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   if constexpr (KIND == kDot) dot_finish(g, dotv);
 }
 
+// ------------------------------------------------------------------ plane-streaming box kernel
+// A 27-entry CDIA class whose table is a 3x3x3 box in natural ordering
+// (off[9g + 3i + j] = g*P + i*L + j - (P + L + 1), so off[13] = 0: the
+// generated 27-point operators, CdiaClass::boxL) is applied plane by plane
+// from shared memory. Rows of a class range [R0, R1) are cut into columns of
+// T consecutive rows per plane (row r = R0 + m*P + c*T + i); a block walks its
+// columns upwards through the planes. Ring stage k of column c holds
+//   x[S_k, S_k + T + 2L + 2), S_k = R0 + c*T + (k-1)*P - L - 1 (every x value
+//     that group g of the rows of plane m = k - g reads),
+//   the participation words of plane k's rows, z_{q-2} of plane k-2's rows,
+// each one cp.async.bulk completing on the stage's mbarrier. At stage k a row
+// position i loads its nine x values ONCE and feeds three rows: group 0 of
+// plane k (a new sum), group 1 of plane k-1, group 2 of plane k-2 (complete:
+// epilogue). Each row still adds its 27 entries in stored (ascending offset)
+// order, each bit-tested exactly as row_sum_cdia, so the sum is bitwise the
+// CDIA / CSR row sum. Per row: 9 shared loads instead of 27 L1 gathers, and
+// every operand stream arrives by bulk copy, several planes ahead.
+#ifndef CS_BOX_THREADS
+#define CS_BOX_THREADS 512
+#endif
+#ifndef CS_BOX_ROWS
+#define CS_BOX_ROWS 4  // rows per thread per plane: T = 2048
+#endif
+#ifndef CS_BOX_NS
+#define CS_BOX_NS 4  // ring stages (planes in flight + 1)
+#endif
+constexpr int kBoxT = CS_BOX_THREADS * CS_BOX_ROWS;
+
+struct BoxGeom {
+  int64_t R0, R1;     // class rows of this launch (local row indices)
+  int64_t P, L;       // plane stride, line stride
+  int64_t nplanes;    // ceil((R1 - R0) / P)
+  int64_t ncols;      // ceil(P / T)
+  int64_t xlen;       // x elements that may be read (even)
+  int64_t n_local;
+  int xs;             // x doubles per stage (even)
+  int ns;             // ring stages
+  uint32_t stage_bytes;
+};
+
+// stage s of this block's sequence -> (column c, stage index k, segment m0, m1)
+__device__ __forceinline__ bool box_stage(const BoxGeom& b, int64_t i0, int64_t i1, int64_t s,
+                                          int64_t& c, int64_t& k, int64_t& m0, int64_t& m1) {
+  int64_t it = i0;
+  while (it < i1) {
+    c = it / b.nplanes;
+    m0 = it - c * b.nplanes;
+    m1 = m0 + (i1 - it) < b.nplanes ? m0 + (i1 - it) : b.nplanes;
+    const int64_t cnt = m1 - m0 + 2;
+    if (s < cnt) {
+      k = m0 + s;
+      return true;
+    }
+    s -= cnt;
+    it += m1 - m0;
+  }
+  return false;
+}
+
+template <bool E2>
+__device__ __forceinline__ void box_issue(const BoxGeom& b, const SellView& a, const SpmvArgs& g,
+                                          unsigned char* stage, uint64_t* bar, int64_t c,
+                                          int64_t k, int64_t m1) {
+  const int64_t cb = b.R0 + c * kBoxT;
+  const int64_t width = b.P - c * kBoxT < kBoxT ? b.P - c * kBoxT : kBoxT;
+  const int64_t S = cb + (k - 1) * b.P - b.L - 1;
+  const int64_t E = S & ~int64_t{1};
+  const int64_t xlo = E > 0 ? E : 0, xhi = E + b.xs < b.xlen ? E + b.xs : b.xlen;
+  uint32_t bytes = 0;
+  const uint32_t bx = xhi > xlo ? static_cast<uint32_t>((xhi - xlo) * 8) : 0u;
+  bytes += bx;
+  int64_t nb = 0, rb = cb + k * b.P;
+  if (k < m1) {
+    nb = b.R1 - rb < width ? b.R1 - rb : width;
+    nb = nb > 0 ? (nb + 3) & ~int64_t{3} : 0;
+  }
+  bytes += static_cast<uint32_t>(nb * 4);
+  int64_t nz = 0, rz = cb + (k - 2) * b.P;
+  if constexpr (E2) {
+    if (k >= 2 && k - 2 < m1) {
+      nz = b.R1 - rz < width ? b.R1 - rz : width;
+      nz = nz > 0 ? (nz + 1) & ~int64_t{1} : 0;
+    }
+    bytes += static_cast<uint32_t>(nz * 8);
+  }
+  mbar_expect_tx(bar, bytes);
+  double* xs = reinterpret_cast<double*>(stage);
+  if (bx) bulk_g2s(xs + (xlo - E), g.x + xlo, bx, bar);
+  if (nb) bulk_g2s(stage + 8 * b.xs + 8 * kBoxT, a.pbits + rb, static_cast<uint32_t>(nb * 4), bar);
+  if constexpr (E2)
+    if (nz) bulk_g2s(stage + 8 * b.xs, g.zp2 + rz, static_cast<uint32_t>(nz * 8), bar);
+}
+
+// One row position of a stage: its nine x values (3 lines x 3) feed group 0 of
+// the plane-k row, group 1 of the plane-(k-1) row and group 2 of the
+// plane-(k-2) row, each sum in stored order. MODE 0: every row holds all 27
+// entries. MODE 1: the three rows hold the same 9-entry sub-pattern m (an x or
+// y face of the grid): absent entries read as 0.0 and are added -- bitwise the
+// same as skipping them, because a running sum that starts at +0.0 is never
+// -0.0 (round-to-nearest gives +0 on exact cancellation) and every table value
+// is finite, so acc + v * 0.0 == acc. MODE 2: per-row, per-entry tests.
+// NEG1: every off-centre value is -1.0 and acc + (-1.0 * x) is computed as the
+// bitwise-equal acc - x.
+template <int MODE, bool NEG1>
+__device__ __forceinline__ void box_terms(const CdiaTable& t, const double* xs, int L,
+                                          uint32_t bk, uint32_t b1, uint32_t b2, uint32_t m,
+                                          double& acc0, double& acc1, double& acc2, double& cen) {
+  double v[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    if (MODE == 0) {
+      v[e] = xs[(e / 3) * L + (e % 3)];
+    } else if (MODE == 1) {
+      v[e] = e == 4 || ((m >> e) & 1u) ? xs[(e / 3) * L + (e % 3)] : 0.0;
+    } else {
+      // the centre is always loaded: it is also x[row] of the plane k-1 row
+      const bool need = e == 4 || (((bk >> e) | (b1 >> (9 + e)) | (b2 >> (18 + e))) & 1u) != 0u;
+      v[e] = need ? xs[(e / 3) * L + (e % 3)] : 0.0;
+    }
+  }
+  cen = v[4];
+  if (MODE == 1 && !((m >> 4) & 1u)) v[4] = 0.0;
+  const auto term = [&](double& acc, int slot, double xv) {
+    if (NEG1 && slot != 13) acc = __dsub_rn(acc, xv);
+    else acc = __dadd_rn(acc, __dmul_rn(t.v[slot], xv));
+  };
+#pragma unroll
+  for (int e = 0; e < 9; ++e)
+    if (MODE < 2 || ((b2 >> (18 + e)) & 1u)) term(acc2, 18 + e, v[e]);
+#pragma unroll
+  for (int e = 0; e < 9; ++e)
+    if (MODE < 2 || ((b1 >> (9 + e)) & 1u)) term(acc1, 9 + e, v[e]);
+#pragma unroll
+  for (int e = 0; e < 9; ++e)
+    if (MODE < 2 || ((bk >> e) & 1u)) term(acc0, e, v[e]);
+}
+
+template <int KIND, bool JAC, bool NEG1>
+__global__ void __launch_bounds__(CS_BOX_THREADS, 1)
+    sell_box_kernel(SellView a, SpmvArgs g, BoxGeom b, const __grid_constant__ CdiaTable t) {
+  if (g.st != nullptr && *(volatile int*)&g.st->done) return;
+  halo_release(g);
+  if (g.wait_ctr != nullptr) {
+    if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
+    __syncthreads();
+  }
+  constexpr bool kE2 = KIND == kMpkMidF;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
+  constexpr int R = CS_BOX_ROWS;
+  const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
+  extern __shared__ __align__(128) unsigned char box_smem[];
+  __shared__ __align__(8) uint64_t full[CS_BOX_NS];
+  const int64_t items = b.ncols * b.nplanes;
+  const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+  int64_t nseq = 0;
+  for (int64_t it = i0; it < i1;) {  // total stages of this block
+    const int64_t c = it / b.nplanes, m0 = it - c * b.nplanes;
+    const int64_t m1 = m0 + (i1 - it) < b.nplanes ? m0 + (i1 - it) : b.nplanes;
+    nseq += m1 - m0 + 2;
+    it += m1 - m0;
+  }
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < b.ns; ++sl) mbar_init(&full[sl], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t s = 0; s < b.ns - 1 && s < nseq; ++s) {
+      int64_t c, k, m0, m1;
+      box_stage(b, i0, i1, s, c, k, m0, m1);
+      box_issue<kE2>(b, a, g, box_smem + s * b.stage_bytes, &full[s], c, k, m1);
+    }
+  }
+  __syncthreads();
+  double ap[R], ap2[R], cen2[R];  // running sums of planes k-1, k-2; centre of plane k-2
+  uint32_t bp[R], bp2[R];         // participation words of planes k-1, k-2
+  double dotv = 0.0;
+  int64_t c = 0, k = 0, m0 = 0, m1 = 0;
+  for (int64_t s = 0; s < nseq; ++s) {
+    if (threadIdx.x == 0 && s + b.ns - 1 < nseq) {
+      int64_t c2, k2, a0, a1;
+      const int64_t sn = s + b.ns - 1;
+      box_stage(b, i0, i1, sn, c2, k2, a0, a1);
+      const int sl = static_cast<int>(sn % b.ns);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      box_issue<kE2>(b, a, g, box_smem + sl * b.stage_bytes, &full[sl], c2, k2, a1);
+    }
+    box_stage(b, i0, i1, s, c, k, m0, m1);
+    const int sl = static_cast<int>(s % b.ns);
+    mbar_wait(&full[sl], static_cast<uint32_t>((s / b.ns) & 1));
+    const unsigned char* stage = box_smem + sl * b.stage_bytes;
+    const int64_t cb = b.R0 + c * kBoxT;
+    const int64_t S = cb + (k - 1) * b.P - b.L - 1;
+    const double* xs = reinterpret_cast<const double*>(stage) + (S - (S & ~int64_t{1}));
+    const double* zs = reinterpret_cast<const double*>(stage + 8 * b.xs);
+    const uint32_t* bs = reinterpret_cast<const uint32_t*>(stage + 8 * b.xs + 8 * kBoxT);
+    const int64_t width = b.P - c * kBoxT < kBoxT ? b.P - c * kBoxT : kBoxT;
+    const int L = static_cast<int>(b.L);
+    if (k == m0) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ap[j] = ap2[j] = cen2[j] = 0.0;
+        bp[j] = bp2[j] = 0u;
+      }
+    }
+    // rows of plane k (new sums) and plane k-2 (complete) held by this column
+    const int64_t rbk = cb + k * b.P, rb2 = cb + (k - 2) * b.P;
+    const int64_t end2 = b.R1 < b.n_local ? b.R1 : b.n_local;
+    const int lim_k = k < m1 ? static_cast<int>(max(int64_t{0}, min(width, b.R1 - rbk))) : 0;
+    const int lim_2 = k - 2 >= m0 ? static_cast<int>(max(int64_t{0}, min(width, end2 - rb2))) : 0;
+    const int64_t rb1 = rbk - b.P;
+    const int lim_1 =
+        k - 1 >= m0 && k - 1 < m1 ? static_cast<int>(max(int64_t{0}, min(width, b.R1 - rb1))) : 0;
+    uint32_t bk[R], mk[R];
+    bool agree = true, full = true;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = threadIdx.x + j * CS_BOX_THREADS;
+      bk[j] = i < lim_k ? bs[i] : 0u;
+      // the 9-entry sub-pattern each live row uses from this stage (rows outside
+      // the column/segment are never stored, so they do not constrain it)
+      const uint32_t g0 = bk[j] & 0x1FFu, g1 = (bp[j] >> 9) & 0x1FFu, g2 = (bp2[j] >> 18) & 0x1FFu;
+      const bool l0 = i < lim_k, l1 = i < lim_1, l2 = i < lim_2;
+      const uint32_t m = (l0 ? g0 : 0u) | (l1 ? g1 : 0u) | (l2 ? g2 : 0u);
+      mk[j] = m;
+      agree = agree && (!l0 || g0 == m) && (!l1 || g1 == m) && (!l2 || g2 == m);
+      full = full && m == 0x1FFu;
+    }
+    double acc0[R], acc1[R], acc2[R], cen[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      acc0[j] = 0.0;
+      acc1[j] = ap[j];
+      acc2[j] = ap2[j];
+    }
+    const unsigned all_agree = __all_sync(0xffffffffu, agree);
+    if (all_agree && __all_sync(0xffffffffu, full)) {  // interior: all 27 entries
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        box_terms<0, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
+                           mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
+    } else if (all_agree) {  // x / y faces: one sub-pattern per row position
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        box_terms<1, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
+                           mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        box_terms<2, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
+                           mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = threadIdx.x + j * CS_BOX_THREADS;
+      if (i < lim_2) {  // plane k-2 row complete
+        const int64_t r2 = rb2 + i;
+        EpiOps eo;
+        eo.exd = cen2[j];
+        eo.einv = JAC ? t.inv : 1.0;
+        if constexpr (kE2) eo.e2 = zs[i];
+        if constexpr (KIND == kResid) eo.e1 = g.b[r2];
+        double zv = 0.0;
+        epi_store<KIND, JAC>(g, r2, acc2[j], eo, dotv, zv);
+        if constexpr (kPush)
+          if (push) halo_push_row(g, r2, zv);
+      }
+      ap2[j] = acc1[j];
+      bp2[j] = bp[j];
+      cen2[j] = cen[j];  // x[row] of the plane k-1 row (off[13] = 0)
+      ap[j] = acc0[j];
+      bp[j] = bk[j];
+    }
+    __syncthreads();  // every thread is done with slot sl before it is refilled
+  }
+}
+
 #ifndef CS_SPMV_TMA
 #define CS_SPMV_TMA 0  // measured slower on B200 (16 warps/SM at 128 regs); DESIGN.md 3
 #endif
@@ -660,6 +937,61 @@ void tma_launch(const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se, cu
   sell_tma_kernel<KIND, JAC><<<tma_grid(se - sb), kWarps * 32, 2 * stage, st>>>(a, g, sb, se, stage);
 }
 
+// CS_SPMV_BOX=0 in the environment: box classes take the gather kernels (A/B runs)
+bool box_enabled() {
+  const char* e = std::getenv("CS_SPMV_BOX");
+  return e == nullptr || std::atoi(e) != 0;
+}
+
+constexpr bool box_kind(int kind) {
+  return kind == kPlain || kind == kResid || kind == kMpkFirstF || kind == kMpkMidF ||
+         kind == kMpkLast;
+}
+
+// Plane-streaming launch over the class rows [lo, hi) * 32; false: not applicable.
+template <int KIND>
+bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass& cl,
+                const CdiaTable& t, int64_t lo, int64_t hi, cudaStream_t st) {
+  if constexpr (!box_kind(KIND)) {
+    return false;
+  } else {
+    if (!box_enabled() || cl.boxL == 0 || a.pbits == nullptr) return false;
+    const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+    if (!al16(g.x) || (KIND == kMpkMidF && !al16(g.zp2))) return false;
+    BoxGeom b{};
+    b.R0 = lo * kSliceRows;
+    b.R1 = hi * kSliceRows;
+    b.P = cl.boxP;
+    b.L = cl.boxL;
+    b.nplanes = (b.R1 - b.R0 + b.P - 1) / b.P;
+    b.ncols = (b.P + kBoxT - 1) / kBoxT;
+    b.xlen = a.xlen;
+    b.n_local = a.n_local;
+    b.xs = static_cast<int>((kBoxT + 2 * b.L + 4 + 1) / 2 * 2);
+    b.stage_bytes = static_cast<uint32_t>(round_up(8 * b.xs + 12 * kBoxT, 128));
+    constexpr int kSmemMax = 227 * 1024 - 1024;
+    b.ns = std::min<int>(CS_BOX_NS, kSmemMax / static_cast<int>(b.stage_bytes));
+    if (b.ns < 2) return false;
+    const int smem = b.ns * static_cast<int>(b.stage_bytes);
+    for (int e = 0; e < 27; ++e)  // box_terms MODE 1 adds 0.0 * v for absent entries
+      if (!std::isfinite(t.v[e])) return false;
+    bool neg1 = true;  // every off-centre value is -1.0 (the 27-point Poisson operators)
+    for (int e = 0; e < 27; ++e) neg1 = neg1 && (e == 13 || t.v[e] == -1.0);
+    static int configured[4] = {0, 0, 0, 0};
+    const int ki = (jac ? 1 : 0) + (neg1 ? 2 : 0);
+    auto kern = jac ? (neg1 ? sell_box_kernel<KIND, true, true> : sell_box_kernel<KIND, true, false>)
+                    : (neg1 ? sell_box_kernel<KIND, false, true> : sell_box_kernel<KIND, false, false>);
+    if (smem > configured[ki]) {
+      CS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured[ki] = smem;
+    }
+    const int64_t items = b.ncols * b.nplanes;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(items, 148)));
+    kern<<<grid, CS_BOX_THREADS, smem, st>>>(a, g, b, t);
+    return true;
+  }
+}
+
 template <int KIND>
 void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,
                  cudaStream_t st) {
@@ -685,6 +1017,10 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
         int64_t lo = std::max(r[0], a.cdia[k].s0);
         const int64_t hi = std::min(r[1], a.cdia[k].s1);
         if (lo >= hi) continue;
+        if (box_kind(KIND) && box_enabled() && a.cdia[k].boxL > 0) {
+          list[np++] = {k, lo, hi, -1};
+          continue;
+        }
         const int64_t sp = CS_SPMV_ZB ? a.cdia[k].zstride / kSliceRows : 0;
         if (sp > 0 && hi - lo >= 2 * sp) {
           const int64_t span = (hi - lo) / (2 * sp) * (2 * sp);
@@ -699,6 +1035,17 @@ void launch_kind(bool jac, const SellView& a, const SpmvArgs& g, int64_t sb, int
         const Piece& pc = list[e];
         CdiaTable t = a.cdia[pc.k].t;
         t.inv = jac && t.diag != 0.0 ? 1.0 / t.diag : 0.0;  // IEEE, = inv_diag_kernel
+        if (pc.sp < 0 && box_launch<KIND>(jac, a, gg, a.cdia[pc.k], t, pc.lo, pc.hi, st)) {
+          gg.rel_lo = gg.rel_hi = nullptr;
+          continue;
+        }
+        if (pc.sp < 0) {  // box launch not applicable after all: row-wise
+          const unsigned grid = static_cast<unsigned>(spmv_grid(pc.hi - pc.lo, true));
+          if (jac) sell_kernel<KIND, true, 27><<<grid, kWarps * 32, 0, st>>>(a, gg, pc.lo, pc.hi, t);
+          else sell_kernel<KIND, false, 27><<<grid, kWarps * 32, 0, st>>>(a, gg, pc.lo, pc.hi, t);
+          gg.rel_lo = gg.rel_hi = nullptr;
+          continue;
+        }
         if (pc.sp > 0) {
           const int64_t pairs = (pc.hi - pc.lo) / 2;
           const unsigned zg = static_cast<unsigned>(std::min<int64_t>(

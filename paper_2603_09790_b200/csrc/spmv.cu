@@ -668,24 +668,29 @@ struct BoxGeom {
   uint32_t stage_bytes;
 };
 
-// stage s of this block's sequence -> (column c, stage index k, segment m0, m1)
-__device__ __forceinline__ bool box_stage(const BoxGeom& b, int64_t i0, int64_t i1, int64_t s,
-                                          int64_t& c, int64_t& k, int64_t& m0, int64_t& m1) {
-  int64_t it = i0;
-  while (it < i1) {
-    c = it / b.nplanes;
-    m0 = it - c * b.nplanes;
-    m1 = m0 + (i1 - it) < b.nplanes ? m0 + (i1 - it) : b.nplanes;
-    const int64_t cnt = m1 - m0 + 2;
-    if (s < cnt) {
-      k = m0 + s;
-      return true;
-    }
-    s -= cnt;
-    it += m1 - m0;
+// a block's stage sequence: items [i0, i1) (item = column * nplanes + plane)
+// split into column segments of planes [m0, m1); a segment streams stages
+// k = m0 .. m1 + 1
+struct BoxIter {
+  int64_t it, i1;
+  int c = 0, k = 0, m0 = 0, m1 = 0;
+  bool valid = false;
+  __device__ __forceinline__ void seg(const BoxGeom& b) {
+    valid = it < i1;
+    if (!valid) return;
+    const int64_t cc = it / b.nplanes;
+    c = static_cast<int>(cc);
+    m0 = static_cast<int>(it - cc * b.nplanes);
+    m1 = static_cast<int>(m0 + (i1 - it) < b.nplanes ? m0 + (i1 - it) : b.nplanes);
+    k = m0;
   }
-  return false;
-}
+  __device__ __forceinline__ void next(const BoxGeom& b) {
+    if (++k > m1 + 1) {
+      it += m1 - m0;
+      seg(b);
+    }
+  }
+};
 
 template <bool E2>
 __device__ __forceinline__ void box_issue(const BoxGeom& b, const SellView& a, const SpmvArgs& g,
@@ -782,47 +787,45 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
   __shared__ __align__(8) uint64_t full[CS_BOX_NS];
   const int64_t items = b.ncols * b.nplanes;
   const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
-  int64_t nseq = 0;
-  for (int64_t it = i0; it < i1;) {  // total stages of this block
-    const int64_t c = it / b.nplanes, m0 = it - c * b.nplanes;
-    const int64_t m1 = m0 + (i1 - it) < b.nplanes ? m0 + (i1 - it) : b.nplanes;
-    nseq += m1 - m0 + 2;
-    it += m1 - m0;
-  }
+  BoxIter cur{i0, i1}, pre{i0, i1};
+  cur.seg(b);
+  pre.seg(b);
+  int psl = 0;
   if (threadIdx.x == 0) {
     for (int sl = 0; sl < b.ns; ++sl) mbar_init(&full[sl], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t s = 0; s < b.ns - 1 && s < nseq; ++s) {
-      int64_t c, k, m0, m1;
-      box_stage(b, i0, i1, s, c, k, m0, m1);
-      box_issue<kE2>(b, a, g, box_smem + s * b.stage_bytes, &full[s], c, k, m1);
-    }
+    for (; psl < b.ns - 1 && pre.valid; ++psl, pre.next(b))
+      box_issue<kE2>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
   }
   __syncthreads();
   double ap[R], ap2[R], cen2[R];  // running sums of planes k-1, k-2; centre of plane k-2
   uint32_t bp[R], bp2[R];         // participation words of planes k-1, k-2
   double dotv = 0.0;
-  int64_t c = 0, k = 0, m0 = 0, m1 = 0;
-  for (int64_t s = 0; s < nseq; ++s) {
-    if (threadIdx.x == 0 && s + b.ns - 1 < nseq) {
-      int64_t c2, k2, a0, a1;
-      const int64_t sn = s + b.ns - 1;
-      box_stage(b, i0, i1, sn, c2, k2, a0, a1);
-      const int sl = static_cast<int>(sn % b.ns);
+  const int R0 = static_cast<int>(b.R0), R1 = static_cast<int>(b.R1), P = static_cast<int>(b.P);
+  const int L = static_cast<int>(b.L);
+  const int end2 = static_cast<int>(b.R1 < b.n_local ? b.R1 : b.n_local);
+  int sl = 0;
+  uint32_t phase = 0;
+  for (; cur.valid; cur.next(b)) {
+    if (threadIdx.x == 0 && pre.valid) {  // refill the slot consumed last iteration
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      box_issue<kE2>(b, a, g, box_smem + sl * b.stage_bytes, &full[sl], c2, k2, a1);
+      box_issue<kE2>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
+      pre.next(b);
+      psl = psl + 1 == b.ns ? 0 : psl + 1;
     }
-    box_stage(b, i0, i1, s, c, k, m0, m1);
-    const int sl = static_cast<int>(s % b.ns);
-    mbar_wait(&full[sl], static_cast<uint32_t>((s / b.ns) & 1));
+    const int c = cur.c, k = cur.k, m0 = cur.m0, m1 = cur.m1;
+    mbar_wait(&full[sl], phase);
     const unsigned char* stage = box_smem + sl * b.stage_bytes;
-    const int64_t cb = b.R0 + c * kBoxT;
-    const int64_t S = cb + (k - 1) * b.P - b.L - 1;
-    const double* xs = reinterpret_cast<const double*>(stage) + (S - (S & ~int64_t{1}));
+    if (++sl == b.ns) {
+      sl = 0;
+      phase ^= 1u;
+    }
+    const int cb = R0 + c * kBoxT;
+    const int S = cb + (k - 1) * P - L - 1;
+    const double* xs = reinterpret_cast<const double*>(stage) + (S & 1);
     const double* zs = reinterpret_cast<const double*>(stage + 8 * b.xs);
     const uint32_t* bs = reinterpret_cast<const uint32_t*>(stage + 8 * b.xs + 8 * kBoxT);
-    const int64_t width = b.P - c * kBoxT < kBoxT ? b.P - c * kBoxT : kBoxT;
-    const int L = static_cast<int>(b.L);
+    const int width = min(P - c * kBoxT, kBoxT);
     if (k == m0) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
@@ -830,14 +833,11 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
         bp[j] = bp2[j] = 0u;
       }
     }
-    // rows of plane k (new sums) and plane k-2 (complete) held by this column
-    const int64_t rbk = cb + k * b.P, rb2 = cb + (k - 2) * b.P;
-    const int64_t end2 = b.R1 < b.n_local ? b.R1 : b.n_local;
-    const int lim_k = k < m1 ? static_cast<int>(max(int64_t{0}, min(width, b.R1 - rbk))) : 0;
-    const int lim_2 = k - 2 >= m0 ? static_cast<int>(max(int64_t{0}, min(width, end2 - rb2))) : 0;
-    const int64_t rb1 = rbk - b.P;
-    const int lim_1 =
-        k - 1 >= m0 && k - 1 < m1 ? static_cast<int>(max(int64_t{0}, min(width, b.R1 - rb1))) : 0;
+    // rows of planes k (new sums), k-1 and k-2 (complete) held by this column
+    const int rbk = cb + k * P, rb1 = rbk - P, rb2 = rb1 - P;
+    const int lim_k = k < m1 ? max(0, min(width, R1 - rbk)) : 0;
+    const int lim_1 = k - 1 >= m0 && k - 1 < m1 ? max(0, min(width, R1 - rb1)) : 0;
+    const int lim_2 = k - 2 >= m0 ? max(0, min(width, end2 - rb2)) : 0;
     uint32_t bk[R], mk[R];
     bool agree = true, full = true;
 #pragma unroll

@@ -345,8 +345,9 @@ def run_ours(args):
         # Q, Z, P, r read once (one launch per outer + the setup one)
         "reduce": (outers_t + len(reps_t)) * v8 * (3 * args.s + 1),
     }
-    names = {"spmv": "sell_zb_kernel / sell_kernel<kMpk*, CDIA> (FP64 SpMV over the constant-"
-                     "diagonal class table + fused MPK epilogue)",
+    names = {"spmv": "sell_box_kernel<kMpk*> (plane-streaming FP64 SpMV over the 3x3x3 constant-"
+                     "diagonal class: bulk-copied plane stages, fused MPK epilogue; gather "
+                     "kernels for other classes)",
              "update": "update_kernel<s,beta,xr,z0> (Q, AQ, x, r, z_0 update pass)",
              "reduce": "pack_kernel<s> (packed Gram/projection block, DMMA)"}
     peak, peak_src = measured_peak()

@@ -770,8 +770,11 @@ __device__ __forceinline__ void box_terms(const CdiaTable& t, const double* xs, 
     if (MODE < 2 || ((bk >> e) & 1u)) term(acc0, e, v[e]);
 }
 
+#ifndef CS_BOX_MINB
+#define CS_BOX_MINB 1
+#endif
 template <int KIND, bool JAC, bool NEG1>
-__global__ void __launch_bounds__(CS_BOX_THREADS, 1)
+__global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     sell_box_kernel(SellView a, SpmvArgs g, BoxGeom b, const __grid_constant__ CdiaTable t) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
   halo_release(g);
@@ -985,8 +988,14 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
       CS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       configured[ki] = smem;
     }
+    static int per_sm[4] = {0, 0, 0, 0}, per_sm_smem[4] = {0, 0, 0, 0};  // occupancy API
+    if (per_sm_smem[ki] != smem) {
+      CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ki], kern, CS_BOX_THREADS, smem));
+      per_sm_smem[ki] = smem;
+    }
     const int64_t items = b.ncols * b.nplanes;
-    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(items, 148)));
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(items, 148 * std::max(per_sm[ki], 1))));
     kern<<<grid, CS_BOX_THREADS, smem, st>>>(a, g, b, t);
     return true;
   }

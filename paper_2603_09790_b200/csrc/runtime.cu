@@ -1,6 +1,7 @@
 // runtime.cu -- device context, device-resident problems, halo exchange,
 // collectives and launch/timing accounting.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <atomic>
@@ -913,6 +914,24 @@ void interior_range(cs_problem* p) {
 
 }  // namespace
 
+namespace {
+// CS_TRACE=1: per-phase wall times of the CSR upload (stream-synchronised; diagnostics only)
+struct UploadTrace {
+  cudaStream_t st;
+  bool on = std::getenv("CS_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit UploadTrace(cudaStream_t s) : st(s) {}
+  void mark(const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cs-trace]   upload %s %.1f ms\n", phase,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+}  // namespace
+
 cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin, int64_t row_end,
                                  const int64_t* rowptr, const int64_t* col, const double* val) {
   if (n_global < 0 || row_begin < 0 || row_end < row_begin || row_end > n_global)
@@ -925,6 +944,7 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
   if (nnz < 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[n] must equal nnz");
   CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
+  UploadTrace ut(c->stream);
   auto p = std::make_unique<cs_problem>();
   p->ctx = c;
   p->n_global = n_global;
@@ -958,6 +978,7 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
     CS_CUDA(cudaMemcpyAsync(dval.p, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
   }
   CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  ut.mark("alloc+h2d");
   p->slice_ptr.alloc(sizeof(int64_t) * (p->nslices + 1));
   if (p->nslices > 0) {
     DBuf widths(sizeof(int64_t) * p->nslices);
@@ -983,6 +1004,7 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
                       p->diag.as<double>(), bad.as<int>(), c->stream);
     CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CS_CUDA(cudaStreamSynchronize(c->stream));
+    ut.mark("widths+fill");
     local_err = hbad ? 2 : 0;
   }
   if (c->nranks > 1) {
@@ -999,7 +1021,9 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
   if (local_err == 2) fail(CS_ERR_INVALID_MATRIX, 0, "column index out of range");
   interior_range(p.get());
   plan_general_halo(p.get());
+  ut.mark("halo plan");
   compress_sell(p.get());
+  ut.mark("compress");
   return p.release();
 }
 

@@ -18,3 +18,10 @@ for i in range(3):
     t0 = time.perf_counter()
     r = cs.pcg_s_solve(ah, b.numpy(), x0.numpy(), m, cfg)
     print(f"e2e {time.perf_counter()-t0:.3f} s outer {r.report.outer_iters} t_solve {r.report.t_solve_ms:.0f} t_lz {r.report.t_lanczos_ms:.0f}", flush=True)
+# raw pinned H2D bandwidth of the value array, for comparison with the upload phase
+d = torch.empty(keep[2].numel(), dtype=torch.float64, device="cuda")
+for i in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    d.copy_(keep[2], non_blocking=True); torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"pinned h2d {keep[2].numel()*8/1e9:.2f} GB {dt*1e3:.1f} ms {keep[2].numel()*8/dt/1e9:.1f} GB/s", flush=True)

@@ -104,26 +104,46 @@ __global__ void __launch_bounds__(kThreads)
                      const double* __restrict__ v, int64_t ldv, double* g, double* partial,
                      unsigned* ticket, DevState* st) {
   if (halted(st)) return;
-  __shared__ double red[kThreads / 32];
+  // kTreeGroup entries per pass over the block's rows: a row of v (and of u
+  // when entries share it) is loaded once per group instead of once per entry.
+  // Each entry keeps its own accumulator, thread stride and reduction tree, so
+  // the result is bitwise the one-entry-per-pass order.
+  constexpr int kTreeGroup = 8;
+  __shared__ double red[kTreeGroup][kThreads / 32];
   __shared__ bool last;
   const int ne = ku * kv;
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t b1 = min(n, b0 + chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int e = 0; e < ne; ++e) {
-    const double* ui = u + (e % ku) * ldu;
-    const double* vj = v + (e / ku) * ldv;
-    double acc = 0.0;
-    for (int64_t l = b0 + threadIdx.x; l < b1; l += kThreads) acc += ui[l] * vj[l];
+  for (int e0 = 0; e0 < ne; e0 += kTreeGroup) {
+    const int cnt = min(kTreeGroup, ne - e0);
+    const double* ui[kTreeGroup];
+    const double* vj[kTreeGroup];
+    double acc[kTreeGroup];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-    if (lane == 0) red[warp] = acc;
+    for (int g = 0; g < kTreeGroup; ++g) {
+      const int e = min(e0 + g, ne - 1);
+      ui[g] = u + (e % ku) * ldu;
+      vj[g] = v + (e / ku) * ldv;
+      acc[g] = 0.0;
+    }
+    for (int64_t l = b0 + threadIdx.x; l < b1; l += kThreads) {
+#pragma unroll
+      for (int g = 0; g < kTreeGroup; ++g)
+        if (g < cnt) acc[g] += ui[g][l] * vj[g][l];
+    }
+#pragma unroll
+    for (int g = 0; g < kTreeGroup; ++g) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[g] += __shfl_down_sync(0xffffffffu, acc[g], off);
+      if (lane == 0) red[g][warp] = acc[g];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < cnt) {
       double s = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-      partial[static_cast<int64_t>(blockIdx.x) * ne + e] = s;
+      for (int w = 0; w < kThreads / 32; ++w) s += red[threadIdx.x][w];
+      partial[static_cast<int64_t>(blockIdx.x) * ne + e0 + threadIdx.x] = s;
     }
     __syncthreads();
   }

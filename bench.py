@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=256, help="grid edge per GPU")
+    ap.add_argument("--grid", type=int, default=512,
+                    help="grid edge (default 512: BASELINE configs[2], the north-star 27-pt 512^3)")
     ap.add_argument("--stencil", type=int, default=27, choices=[7, 27])
     ap.add_argument("--s", type=int, default=8)
     ap.add_argument("--nu", type=int, default=30)
@@ -53,7 +54,7 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the n^3 grid split into z-slabs over N GPUs (default); "
                          "weak: n^3 per GPU, global n x n x nN")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
@@ -175,21 +176,26 @@ def outer_bytes(nnz, n, s):
 
 # ------------------------------------------------------------------------------ CPU baseline
 
-def golden_outer(stencil, n, s, nu, world):
+def golden_run(stencil, n, s, nu, world):
+    """The reference's outer count and spectrum for this workload: the compiled
+    reference (ref_probe) where it could run here, else the GPU's reference-
+    algebra mode (the reference's operation order; bitwise equal to it wherever
+    both ran), recorded in tests/golden/outer_counts.json with its source."""
     try:
         with open(os.path.join(ROOT, "tests", "golden", "outer_counts.json")) as f:
             table = json.load(f)
         key = f"p{stencil}_{n}x{n}x{n * world}_s{s}_nu{nu}_jacobi_1e-08"
-        return (table.get(key) or {}).get("outer_iters")
+        return table.get(key)
     except (OSError, ValueError):
         return None
 
 
-def cpu_sample(args, lam, world=1):
+def cpu_sample(args, lam, world=1, lanczos=True):
     """Bounded CPU sample of the same workload on one host core: the reference
-    pcg_s_solve on a 256 x 256 x nzs slab of the same operator with the same
-    spectrum, per-outer time = t(max_outer=2) - t(max_outer=1), scaled to the
-    full grid (per-outer cost is linear in n)."""
+    on a grid x grid x nzs slab of the same operator with the same spectrum.
+    Per-outer time = t(max_outer=2) - t(max_outer=1) of pcg_s_solve; the
+    Lanczos estimate (40 steps, the solve's own first phase) timed once on the
+    same slab. Both are linear in n and are scaled to the full grid."""
     from oracle import oracle as orc
     kind = "ref" if orc.available("ref") else "port"
     o = orc.Oracle(kind)
@@ -197,25 +203,32 @@ def cpu_sample(args, lam, world=1):
         os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
     except (AttributeError, OSError):
         pass
-    nzs = 16
-    nxy = args.n
+    nxy = args.grid
+    nzs = max(2, (1 << 21) // (nxy * nxy))  # ~2M rows: 8 planes at 512^2, 32 at 256^2
     if args.stencil == 27:
         a = o.poisson27(nxy, nxy, nzs)
     else:
         a = orc.Oracle("port").stencil7(nxy, nxy, nzs)
+    scale = nxy * world / nzs if args.scaling == "weak" else nxy / nzs
     t = []
     for mo in (1, 2):
         t0 = time.perf_counter()
         o.pcg_s_solve(a, s=args.s, nu=args.nu, tol=args.tol, max_outer=mo, spectrum=lam,
                       precond=1)
         t.append(time.perf_counter() - t0)
-    per_outer = max(t[1] - t[0], 1e-9) * (args.n * world) / nzs
+    per_outer = max(t[1] - t[0], 1e-9) * scale
+    t_lz = 0.0
+    if lanczos:
+        t0 = time.perf_counter()
+        o.estimate_interval(a, 1, 40, 1234)
+        t_lz = (time.perf_counter() - t0) * scale
     return {"kind": "reference" if kind == "ref" else "port", "cores": 1,
-            "per_outer_s": per_outer,
-            "sample": (f"pcg_s_solve on a {nxy}x{nxy}x{nzs} slab, same operator/s/nu/spectrum, "
-                       f"t(max_outer=2)-t(max_outer=1) = {t[1]-t[0]:.3f} s scaled x{args.n*world/nzs:g} "
-                       "to the full grid; Lanczos excluded; 1 of "
-                       f"{os.cpu_count()} host cores (the reference is single-threaded)")}
+            "per_outer_s": per_outer, "lanczos_s": t_lz,
+            "sample": (f"reference pcg_s_solve on a {nxy}x{nxy}x{nzs} slab of the same operator, "
+                       f"same s/nu/spectrum: t(max_outer=2)-t(max_outer=1) = {t[1]-t[0]:.3f} s; "
+                       f"Lanczos (40 steps) on the slab {t_lz / scale:.3f} s; both scaled "
+                       f"x{scale:g} to the full grid; 1 of {os.cpu_count()} host cores (the "
+                       "reference is single-threaded)")}
 
 
 # ------------------------------------------------------------------------------ reference arm
@@ -224,31 +237,37 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    n = args.n
+    n = args.grid
     wz = world if args.scaling == "weak" else 1
     n_global = n * n * n * wz
-    outer = golden_outer(args.stencil, n, args.s, args.nu, wz)
-    lam = (0.0023, 1.5205)  # 27-pt Jacobi spectrum interval at 128^3; sample only
-    src = "golden"
-    if outer is None:
-        outer, src = 1000, "assumed"
+    g = golden_run(args.stencil, n, args.s, args.nu, wz)
+    if g:
+        outer, lam, src = g["outer_iters"], (g["lambda_min"], g["lambda_max"]), g["source"]
+    else:  # no recorded run for this grid: 27-pt Jacobi interval of 128^3
+        outer, lam, src = 1000, (0.0023051621745818554, 1.5204622252319928), "assumed"
     vals = []
-    sample = None
+    smp = cpu_sample(args, lam, wz, lanczos=True)
+    t_lz = smp["lanczos_s"]
     for i in range(args.warmup + args.steps):
-        sample = cpu_sample(args, lam, wz)
+        if i > 0:
+            smp = cpu_sample(args, lam, wz, lanczos=False)
         if i >= args.warmup:
-            vals.append(n_global / (outer * sample["per_outer_s"]) / 1e9)
+            vals.append(n_global / (t_lz + outer * smp["per_outer_s"]) / 1e9)
     v = statistics.median(vals)
+    t_step = n_global / v / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (27-point Poisson, b=1, x0=0)",
             "config": {"workload": f"{args.stencil}-pt Poisson {n}x{n}x{n*wz}, s={args.s}, "
                        f"nu={args.nu}, Jacobi, tol {args.tol:g}",
-                       "outer_iters": outer, "outer_iters_source": src},
-            "ms_per_step": outer * sample["per_outer_s"] * 1e3,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": sample["kind"],
-                             "sample": sample["sample"]},
+                       "outer_iters": outer, "outer_iters_source": src,
+                       "lambda": list(lam), "extrapolated": True,
+                       "timing": "each step = one bounded slab sample (one host core); solve time "
+                                 "= Lanczos + outer_iters x per-outer, scaled to the full grid"},
+            "ms_per_step": t_step * 1e3,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": smp["kind"],
+                             "sample": smp["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -277,7 +296,7 @@ def run_ours(args):
         obj = [cs.Context.unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
         ctx.comm_init(world, rank, obj[0])
-    n = args.n
+    n = args.grid
     nz = n * world if args.scaling == "weak" else n
     kind = "poisson27" if args.stencil == 27 else "poisson7"
     prob = cs.DeviceProblem.generate(kind, n, n, nz, ctx=ctx).set_precond("jacobi")
@@ -311,12 +330,12 @@ def run_ours(args):
     t_ms = e0.elapsed_time(e1)
     t_max = ctx.allreduce_max(t_ms)
     barrier()
-    # (2) the same K solves again with CUDA events around every launch: per-phase
-    # kernel times for the roofline (instrumentation overhead reported)
+    # (2) one more solve with CUDA events around every launch: per-phase kernel
+    # times for the roofline (instrumentation overhead reported)
     ctx.reset_timing()
     ctx.set_timing(True)
     e0.record(ext)
-    reps_t = [step() for _ in range(args.steps)]
+    reps_t = [step()]  # one instrumented solve: the per-phase split, not the headline
     e1.record(ext)
     e1.synchronize()
     ctx.set_timing(False)
@@ -371,9 +390,9 @@ def run_ours(args):
             "unit": "GB/s", "frac": d["frac"], "traffic": d["traffic"],
             "traffic_alg_per_launch": d["traffic_alg_per_launch"], "peak_source": peak_src,
             "share_of_step": d["share_of_step"],
-            "measured": "CUDA events around every launch of K instrumented solves run right "
+            "measured": "CUDA events around every launch of one instrumented solve run right "
                         "after the timed region (instrumentation overhead %.1f%%)" %
-                        (100 * (t_inst / t_ms - 1) if t_ms > 0 else 0),
+                        (100 * (t_inst / len(reps_t) / (t_ms / args.steps) - 1) if t_ms > 0 else 0),
             "kernels": kern,
             "alg_bytes_per_spmv": b_spmv,
             "matrix_bytes": mat, "matrix_bytes_per_nnz": mat / nnz_l,
@@ -434,10 +453,14 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         lam = (rep.spectrum_used.lambda_min, rep.spectrum_used.lambda_max)
         smp = cpu_sample(args, lam)
-        v = ng / (rep.outer_iters * smp["per_outer_s"]) / 1e9
+        g = golden_run(args.stencil, args.grid, args.s, args.nu, 1)
+        outer, src = ((g["outer_iters"], g["source"]) if g else
+                      (rep.outer_iters, "this GPU run (no recorded reference count)"))
+        v = ng / (smp["lanczos_s"] + outer * smp["per_outer_s"]) / 1e9
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": smp["cores"],
-                                "kind": smp["kind"], "sample": smp["sample"] +
-                                f"; x {rep.outer_iters} outer iterations of this GPU run"}
+                                "kind": smp["kind"], "extrapolated": True,
+                                "sample": smp["sample"] + f"; solve = Lanczos + {outer} outer "
+                                f"iterations ({src})"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     prob.close()
@@ -447,47 +470,66 @@ def run_ours(args):
     return 0
 
 
+def host_mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def e2e(args, cs, ctx, prob, world, torch):
-    """Reference-facing entry with HOST buffers: N=1 -> cs_pcg_s_solve_csr with the host
-    int64 CSR (upload + SELL conversion + Jacobi setup + Lanczos + solve + x download);
-    N>1 -> cs_pcg_s_solve on the rank's slab with host b/x0/x."""
+    """The same solve through the reference-facing entry with HOST buffers in
+    PAGEABLE memory (what a reference caller passes: std::vector / numpy), every
+    host<->device byte inside the timed region.
+
+    N=1 and the host can hold the reference's int64 CSR (+ headroom):
+      cs_pcg_s_solve_csr = chebstep::pcg_s_solve(const CsrMatrix&, b, x0, M, cfg):
+      streamed CSR upload overlapped with the SELL-32 fill, CDIA conversion,
+      Jacobi setup, Lanczos, solve, x download.
+    Otherwise (e.g. 27-pt 512^3: 58.8 GB of int64 CSR) the device-resident-
+      problem overload cs_pcg_s_solve with host b / x0 -> host x."""
     import numpy as np
     nl, ng = prob.n_local, prob.n_global
     cfg = cs.SolverConfig(s=args.s, tol=args.tol, max_outer=50000, fgs=cs.FgsConfig(nu=args.nu),
                           mode=args.mode)
-
-    def pinned(arr):
-        t = torch.empty(arr.size, dtype={np.int64: torch.int64, np.float64: torch.float64}[arr.dtype.type],
-                        pin_memory=True)
-        t.numpy()[:] = arr
-        return t
-
-    if world == 1:
-        a = prob.to_csr()
-        keep = [pinned(a.row_offsets), pinned(a.col_indices), pinned(a.values)]
-        ah = cs.CsrMatrix(a.n, keep[0].numpy(), keep[1].numpy(), keep[2].numpy())
-        del a
-        bh, x0h = pinned(np.ones(nl)), pinned(np.zeros(nl))
-        m = cs.JacobiPreconditioner(ah)
-        call = lambda: cs.pcg_s_solve(ah, bh.numpy(), x0h.numpy(), m, cfg, ctx=ctx)  # noqa: E731
-        h2d = 8 * (ah.n + 1) + 16 * ah.nnz() + 16 * nl
-        entry = "cs_pcg_s_solve_csr (host int64 CSR + b + x0 -> host x)"
+    nnz = prob.nnz_local
+    csr_bytes = 8 * (nl + 1) + 16 * nnz
+    avail = host_mem_available()
+    use_csr = world == 1 and avail > 1.5 * csr_bytes + 32 * nl
+    if use_csr:
+        a = prob.to_csr()  # numpy (pageable) int64 CSR, the reference layout
+        bh, x0h = np.ones(nl), np.zeros(nl)
+        m = cs.JacobiPreconditioner(a)
+        call = lambda: cs.pcg_s_solve(a, bh, x0h, m, cfg, ctx=ctx)  # noqa: E731
+        h2d = csr_bytes + 16 * nl
+        entry = ("cs_pcg_s_solve_csr: pageable host int64 CSR + b + x0 -> host x (streamed "
+                 "upload, SELL/CDIA conversion, Jacobi, Lanczos, solve, download)")
     else:
-        bh, x0h = pinned(np.ones(nl)), pinned(np.zeros(nl))
-        call = lambda: prob.pcg_s_solve(bh.numpy(), x0h.numpy(), cfg)  # noqa: E731
+        bh, x0h = np.ones(nl), np.zeros(nl)
+        call = lambda: prob.pcg_s_solve(bh, x0h, cfg)  # noqa: E731
         h2d = 16 * nl
-        entry = "cs_pcg_s_solve (device-resident slab, host b + x0 -> host x)"
+        entry = ("cs_pcg_s_solve: device-resident problem, pageable host b + x0 -> host x" +
+                 (f" (host MemAvailable {avail / 1e9:.0f} GB cannot hold the {csr_bytes / 1e9:.1f} "
+                  "GB int64 CSR)" if world == 1 else ""))
     call()  # warm-up
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
+    ts = []
+    res = None
     for _ in range(args.e2e_steps):
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
         res = call()
-    dt = (time.perf_counter() - t0) / args.e2e_steps
-    dt = ctx.allreduce_max(dt)
+        ts.append(ctx.allreduce_max(time.perf_counter() - t0))
+    dt = statistics.median(ts)
     return {"value": ng / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 8 * nl, "steps": args.e2e_steps, "entry": entry,
-            "ms_per_step": dt * 1e3, "outer_iters": res.report.outer_iters}
+            "ms_per_step": dt * 1e3, "ms_per_step_all": [round(t * 1e3, 1) for t in ts],
+            "statistic": "median over steps, wall clock (host buffers), max over ranks",
+            "outer_iters": res.report.outer_iters}
 
 
 def main():

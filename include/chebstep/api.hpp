@@ -200,6 +200,29 @@ class JacobiPreconditioner final : public Preconditioner {
   std::vector<double> inv_diag_;
 };
 
+/// Block Jacobi, M = blockdiag(A_11, A_22, ...) over blocks of `bs` consecutive
+/// rows (a preconditioner beyond the reference's two, through the
+/// same `Preconditioner` interface, precond.hpp:12-23). The ctor extracts the
+/// dense diagonal blocks (a short last block padded with the identity) and
+/// Cholesky-factors them (small_cholesky_solve's order, dense_ops.cpp:55-88);
+/// NotSpdError if a block is not SPD. apply() is the host method (forward then
+/// back substitution); the solver factors the same blocks on the device and
+/// applies them there, bitwise equal.
+class BlockJacobiPreconditioner final : public Preconditioner {
+ public:
+  BlockJacobiPreconditioner(const CsrMatrix& a, int bs);
+  void apply(std::span<const double> in, std::span<double> out) const override;
+  std::string_view name() const override { return "block_jacobi"; }
+  int block_size() const { return bs_; }
+  /// ceil(n/bs) dense bs x bs column-major diagonal blocks of A (unfactored)
+  const std::vector<double>& blocks() const { return blocks_; }
+
+ private:
+  int bs_;
+  index_t n_;
+  std::vector<double> blocks_, factor_;
+};
+
 // ------------------------------------------------------------------ problems (problems.hpp:13-34)
 struct PoissonSpec {
   index_t nx = 1, ny = 1, nz = 1;
@@ -362,6 +385,16 @@ void set_mode(Mode m);
 Mode mode();
 /// CUDA device used by the drop-in entry points (default 0).
 void set_device(int device);
+
+/// Plugin for a preconditioner whose apply runs on the device:
+/// device_apply enqueues out = M^-1 in (n doubles, device pointers) on
+/// `stream` (a cudaStream_t). The solver calls it wherever the reference calls
+/// Preconditioner::apply (mpk.cpp:51-67, spectral.cpp:81,94, solver.cpp:228,254);
+/// the host apply() stays the reference's utility method.
+class DevicePreconditioner : public Preconditioner {
+ public:
+  virtual void device_apply(const double* in, double* out, index_t n, void* stream) const = 0;
+};
 
 /// Device-resident operator (SELL-32P in HBM + preconditioner), the
 /// boundary's addition for sizes whose host CSR would not fit.

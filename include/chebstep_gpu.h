@@ -55,6 +55,8 @@ extern "C" {
 /* ------------------------------------------------------------ enums */
 #define CS_PRECOND_IDENTITY 0
 #define CS_PRECOND_JACOBI 1
+#define CS_PRECOND_BLOCK_JACOBI 2 /* bs consecutive rows per block, Cholesky solves */
+#define CS_PRECOND_DEVICE_FN 3    /* caller-supplied device apply (cs_problem_set_precond_fn) */
 
 #define CS_GEN_POISSON27 0 /* problems.cpp:13-53 */
 #define CS_GEN_STENCIL7 1  /* 7-point, coefficients (cx,cy,cz): poisson7 = (1,1,1), aniso = (1,1,100) */
@@ -102,7 +104,19 @@ typedef struct {
   int track_true_residual;   /* ||b - A x_k|| / ||b|| (initial + per outer) */
   const double* error_reference; /* host x* (n_local): A-norm errors, or NULL */
   int collect_iterates;      /* x_k (initial + per outer) */
+  /* CS_VAR_* bit set: arithmetic variants of a mode, for attributing and
+   * bounding the outer-count sensitivity (tools/count_band.py). 0 = the mode's
+   * shipped arithmetic. */
+  int variant;
 } cs_config;
+
+/* cs_config.variant bits */
+#define CS_VAR_EXPLICIT_W 1   /* fast: W_k = sym(Q_k^T AQ_k) from the vectors each outer (in the
+                                 same single allreduce) instead of the product recurrence */
+#define CS_VAR_RECUR_W 2      /* fast: force the pure W recurrence (round-1 algebra) */
+#define CS_VAR_REF_FGS 4      /* fast: the reference's FGS operation sequence */
+#define CS_VAR_REF_MPK 8      /* fast: the reference's MPK epilogue (zp streams, no FMA); 1 GPU */
+#define CS_VAR_TREE 16        /* reference: fixed-shape tree reductions instead of serial chains */
 
 typedef struct {
   /* SolveReport (solver.hpp:39-68), reference semantics */
@@ -238,6 +252,26 @@ int cs_problem_ghosts(cs_problem* p, int64_t* ghost_cols);
 int cs_problem_halo_mode(cs_problem* p, int* mode);
 int cs_problem_set_precond(cs_problem* p, int kind);
 int cs_problem_inv_diag(cs_problem* p, double* out);
+
+/* Pluggable preconditioners beyond the reference's two (the
+ * reference accepts any `const Preconditioner&`, precond.hpp:12-23). Neither
+ * has a CPU fallback: the apply runs on the device inside the solve.
+ *
+ * Block Jacobi: M = blockdiag(A_11, A_22, ...), blocks of bs consecutive local
+ * rows (the last may be shorter). `blocks` (host) holds ceil(n_local/bs) dense
+ * bs x bs column-major diagonal blocks of A (a short last block padded with the
+ * identity). They are factorised on the device, L L^T = A_bb, left-looking
+ * like small_cholesky_solve (dense_ops.cpp:55-88); CS_ERR_NOT_SPD (payload =
+ * block) if a pivot is not positive and finite. apply: out_b = L^-T L^-1 in_b,
+ * forward then back substitution in the reference's loop order. 1 <= bs <= 16. */
+int cs_problem_set_precond_block_jacobi(cs_problem* p, int bs, const double* blocks);
+/* Device plugin: out = M^-1 in for n_local doubles, both device pointers,
+ * enqueued on `stream` (a cudaStream_t) by the callee; return 0 or nonzero on
+ * failure (the solve then fails with CS_ERR_GENERIC). Called s times per outer
+ * iteration, plus once per Lanczos step and once at setup. */
+typedef int (*cs_precond_fn)(void* user, const double* in, double* out, int64_t n_local,
+                             void* stream);
+int cs_problem_set_precond_fn(cs_problem* p, cs_precond_fn fn, void* user);
 
 /* ------------------------------------------------------------ kernel-level entries (host buffers) */
 int cs_spmv(cs_problem* p, const double* x, double* y);

@@ -19,6 +19,9 @@
 #include "chebstep/gram.hpp"
 #include "chebstep/lapack.hpp"
 #include "chebstep/mpk.hpp"
+#include <cmath>
+#include <span>
+#include <string_view>
 #include "chebstep/precond.hpp"
 #include "chebstep/problems.hpp"
 #include "chebstep/solver.hpp"
@@ -81,16 +84,90 @@ cs::CsrMatrix make_csr(int64_t n, const int64_t* rp, const int64_t* ci, const do
   return a;
 }
 
+// Reference-side block-Jacobi subclass of the reference's own Preconditioner
+// interface (precond.hpp:12-23) -- the parity partner of the device block
+// Jacobi. Test infrastructure: dense diagonal blocks of bs rows
+// (entries summed in stored order, a short last block padded with the
+// identity), left-looking Cholesky in small_cholesky_solve's order
+// (dense_ops.cpp:55-88), apply = forward then back substitution.
+class BlockJacobiRef final : public cs::Preconditioner {
+ public:
+  BlockJacobiRef(const cs::CsrMatrix& a, int bs) : bs_(bs), n_(a.n) {
+    if (bs < 1 || bs > 16) throw cs::InvalidArgumentError("block_jacobi: bs must be in [1, 16]");
+    const int64_t nb = (a.n + bs - 1) / bs;
+    const size_t q = static_cast<size_t>(bs) * bs;
+    f_.assign(static_cast<size_t>(nb) * q, 0.0);
+    for (int64_t r = 0; r < nb * bs; ++r) {
+      double* blk = f_.data() + static_cast<size_t>(r / bs) * q;
+      const int i = static_cast<int>(r % bs);
+      if (r >= a.n) {
+        blk[i + i * bs] = 1.0;
+        continue;
+      }
+      const int64_t b0 = (r / bs) * bs;
+      for (int64_t k = a.row_offsets[r]; k < a.row_offsets[r + 1]; ++k) {
+        const int64_t c = a.col_indices[k];
+        if (c >= b0 && c < b0 + bs) blk[i + (c - b0) * bs] += a.values[k];
+      }
+    }
+    for (int64_t b = 0; b < nb; ++b) {
+      double* L = f_.data() + static_cast<size_t>(b) * q;
+      for (int j = 0; j < bs; ++j) {
+        double d = L[j + j * bs];
+        for (int t = 0; t < j; ++t) d -= L[j + t * bs] * L[j + t * bs];
+        if (!(d > 0.0) || !std::isfinite(d))
+          throw cs::NotSpdError("block_jacobi: diagonal block not positive definite");
+        const double dg = std::sqrt(d);
+        L[j + j * bs] = dg;
+        for (int i = j + 1; i < bs; ++i) {
+          double v = L[i + j * bs];
+          for (int t = 0; t < j; ++t) v -= L[i + t * bs] * L[j + t * bs];
+          L[i + j * bs] = v / dg;
+        }
+      }
+    }
+  }
+  void apply(std::span<const double> in, std::span<double> out) const override {
+    const int bs = bs_;
+    double x[16];
+    for (int64_t r0 = 0; r0 < n_; r0 += bs) {
+      const double* L = f_.data() + static_cast<size_t>(r0 / bs) * bs * bs;
+      for (int i = 0; i < bs; ++i) x[i] = r0 + i < n_ ? in[r0 + i] : 0.0;
+      for (int i = 0; i < bs; ++i) {
+        double v = x[i];
+        for (int t = 0; t < i; ++t) v -= L[i + t * bs] * x[t];
+        x[i] = v / L[i + i * bs];
+      }
+      for (int i = bs - 1; i >= 0; --i) {
+        double v = x[i];
+        for (int t = i + 1; t < bs; ++t) v -= L[t + i * bs] * x[t];
+        x[i] = v / L[i + i * bs];
+      }
+      for (int i = 0; i < bs && r0 + i < n_; ++i) out[r0 + i] = x[i];
+    }
+  }
+  std::string_view name() const override { return "block_jacobi"; }
+
+ private:
+  int bs_;
+  int64_t n_;
+  std::vector<double> f_;
+};
+
 struct Precond {
   cs::IdentityPreconditioner ident;
   std::unique_ptr<cs::JacobiPreconditioner> jac;
+  std::unique_ptr<BlockJacobiRef> bj;
   const cs::Preconditioner& get() const {
+    if (bj) return *bj;
     return jac ? static_cast<const cs::Preconditioner&>(*jac) : ident;
   }
 };
 
+// kind: 0 identity, 1 Jacobi, 100 + bs block Jacobi
 void make_precond(Precond& p, const cs::CsrMatrix& a, int kind) {
   if (kind == 1) p.jac = std::make_unique<cs::JacobiPreconditioner>(a);
+  else if (kind >= 101 && kind <= 116) p.bj = std::make_unique<BlockJacobiRef>(a, kind - 100);
   else if (kind != 0) throw cs::InvalidArgumentError("unknown preconditioner kind");
 }
 

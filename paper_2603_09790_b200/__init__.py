@@ -16,5 +16,6 @@ from .chebstep import (  # noqa: F401
     mpk_chebyshev, partition_rows, pcg_s_solve, pcg_solve, poisson27, random_vector,
     small_cholesky_solve, spmv, spmv_into, stencil7, tridiag_eigvals, read_matrix_market,
     write_matrix_market, validate_structure, validate_symmetric, validate_spd_diagonal, ParseError,
-    normalize_gram, fgs_rate, FgsRate, kappa_sym)
+    normalize_gram, fgs_rate, FgsRate, kappa_sym, BlockJacobiPreconditioner,
+    DevicePreconditioner)
 from ._lib import LIB_PATH  # noqa: F401

@@ -28,10 +28,13 @@ CS_ERR_GENERIC = 9
 CS_ERR_CUDA = 10
 CS_ERR_NCCL = 11
 
-CS_PRECOND_IDENTITY, CS_PRECOND_JACOBI = 0, 1
+CS_PRECOND_IDENTITY, CS_PRECOND_JACOBI, CS_PRECOND_BLOCK_JACOBI, CS_PRECOND_DEVICE_FN = 0, 1, 2, 3
+# int (*)(void* user, const double* in, double* out, int64_t n, void* stream)
+PRECOND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 CS_GEN_POISSON27, CS_GEN_STENCIL7 = 0, 1
 CS_GRAM_FGS, CS_GRAM_CHOLESKY = 0, 1
 CS_MODE_FAST, CS_MODE_REFERENCE = 0, 1
+CS_VAR_EXPLICIT_W, CS_VAR_RECUR_W, CS_VAR_REF_FGS, CS_VAR_REF_MPK, CS_VAR_TREE = 1, 2, 4, 8, 16
 PHASES = ("spmv", "reduce", "small", "update", "lanczos", "comm", "other")
 
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
@@ -47,7 +50,8 @@ class CsConfig(C.Structure):
                 ("lambda_max", C.c_double), ("lanczos_steps", C.c_int), ("seed", C.c_uint64),
                 ("mode", C.c_int), ("check_every", C.c_int),
                 ("collect_gram", C.c_int), ("track_true_residual", C.c_int),
-                ("error_reference", C.c_void_p), ("collect_iterates", C.c_int)]
+                ("error_reference", C.c_void_p), ("collect_iterates", C.c_int),
+                ("variant", C.c_int)]
 
 
 class CsReport(C.Structure):
@@ -105,6 +109,8 @@ SIGNATURES = {
     "cs_problem_ghosts": (C.c_int, [_vp, _i64p]),
     "cs_problem_set_precond": (C.c_int, [_vp, C.c_int]),
     "cs_problem_inv_diag": (C.c_int, [_vp, _f64p]),
+    "cs_problem_set_precond_block_jacobi": (C.c_int, [_vp, C.c_int, _f64p]),
+    "cs_problem_set_precond_fn": (C.c_int, [_vp, _vp, _vp]),
     "cs_spmv": (C.c_int, [_vp, _f64p, _f64p]),
     "cs_mpk": (C.c_int, [_vp, _f64p, C.c_int, C.c_double, C.c_double, _f64p, _f64p]),
     "cs_block_gram": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_int, _f64p, _f64p, _f64p, C.c_int]),

@@ -39,6 +39,7 @@ NCCL_LINK = (["-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker
               "-rpath," + os.path.join(NCCL_DIR, "lib")] if NCCL_DIR else
              ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"])
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          "-Xcompiler", "-ffp-contract=off",
           "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", *NCCL_INC]
 
 
@@ -60,7 +61,8 @@ def _stale(target, deps):
 
 CXX = shutil.which("g++") or "g++"
 CUDA_INC = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
-CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off",
+            "-I" + os.path.join(ROOT, "include"),
             "-I" + CUDA_INC, *NCCL_INC]
 
 

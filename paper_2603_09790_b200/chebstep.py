@@ -112,7 +112,7 @@ class Context:
 
     def close(self):
         if self.handle:
-            lib.cs_ctx_destroy(self.handle)
+            _check(lib.cs_ctx_destroy(self.handle))  # refuses while problems are alive
             self.handle = None
 
     def __del__(self):
@@ -321,11 +321,27 @@ class DeviceProblem:
             pass
 
     def set_precond(self, m) -> "DeviceProblem":
+        """identity / jacobi (fused into the kernels), a BlockJacobiPreconditioner
+        (device-factored blocks) or a DevicePreconditioner plugin."""
+        if isinstance(m, BlockJacobiPreconditioner):
+            if m.n != self.n_local:
+                raise DimensionError("block_jacobi: preconditioner size != problem rows")
+            _check(lib.cs_problem_set_precond_block_jacobi(self.handle, m.bs, m.blocks.ravel()))
+            self._precond_keep = m
+            self.precond = m.name()
+            return self
+        if isinstance(m, DevicePreconditioner):
+            cb = m._c_callback()
+            _check(lib.cs_problem_set_precond_fn(self.handle, C.cast(cb, C.c_void_p), None))
+            self._precond_keep = m  # the callback must outlive the problem's solves
+            self.precond = m.name()
+            return self
         name = m if isinstance(m, str) else m.name()
         kind = {"identity": L.CS_PRECOND_IDENTITY, "jacobi": L.CS_PRECOND_JACOBI}.get(name)
         if kind is None:
             raise InvalidArgumentError(
-                f"preconditioner {name!r} has no device implementation (identity, jacobi)")
+                f"preconditioner {name!r} has no device implementation (identity, jacobi, "
+                "BlockJacobiPreconditioner, DevicePreconditioner)")
         _check(lib.cs_problem_set_precond(self.handle, kind))
         self.precond = name
         return self
@@ -527,6 +543,60 @@ class JacobiPreconditioner(Preconditioner):
         return "jacobi"
 
 
+class BlockJacobiPreconditioner(Preconditioner):
+    """M = blockdiag(A_11, A_22, ...) over blocks of `bs` consecutive rows.
+
+    The dense diagonal blocks are extracted here (entries summed in stored
+    order; a short last block padded with the identity), the device factorises
+    them (Cholesky, dense_ops.cpp:55-88 order) and applies two triangular
+    solves per block inside the solve. apply() is the host restatement."""
+
+    def __init__(self, a: CsrMatrix, bs: int = 4):
+        if not 1 <= bs <= 16:
+            raise InvalidArgumentError("block_jacobi: bs must be in [1, 16]")
+        self.bs, self.n = int(bs), int(a.n)
+        nb = (a.n + bs - 1) // bs
+        blocks = np.zeros((nb, bs, bs))  # blocks[b, j, i] = A[b*bs+i, b*bs+j] (column-major)
+        rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_offsets))
+        cols = a.col_indices
+        inb = (cols // bs) == (rows // bs)
+        np.add.at(blocks, (rows[inb] // bs, cols[inb] % bs, rows[inb] % bs), a.values[inb])
+        for r in range(a.n, nb * bs):
+            blocks[r // bs, r % bs, r % bs] = 1.0
+        self.blocks = np.ascontiguousarray(blocks)
+
+    def name(self) -> str:
+        return "block_jacobi"
+
+
+class DevicePreconditioner(Preconditioner):
+    """Plugin whose apply runs on the device: subclass and implement
+    ``device_apply(in_ptr, out_ptr, n, stream)`` (raw device pointers, n doubles,
+    the solve's cudaStream_t as an int), enqueueing out = M^-1 in on that stream.
+    The solver calls it wherever the reference calls Preconditioner::apply."""
+
+    def device_apply(self, in_ptr: int, out_ptr: int, n: int, stream: int) -> None:
+        raise NotImplementedError
+
+    def name(self) -> str:
+        return "device"
+
+    def _c_callback(self):
+        if getattr(self, "_cb", None) is None:
+            def cb(_user, i, o, n, stream):
+                try:
+                    self.device_apply(i or 0, o or 0, n, stream or 0)
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported as a failed apply
+                    return 1
+            self._cb = L.PRECOND_FN(cb)
+        return self._cb
+
+
+def _general(m) -> bool:
+    return isinstance(m, (BlockJacobiPreconditioner, DevicePreconditioner))
+
+
 def _precond_kind(m: Preconditioner) -> int:
     kind = {"identity": L.CS_PRECOND_IDENTITY, "jacobi": L.CS_PRECOND_JACOBI}.get(m.name())
     if kind is None:
@@ -578,6 +648,7 @@ class SolverConfig:
     collect_iterates: bool = False
     mode: str = "fast"
     check_every: int = 0
+    variant: int = 0  # CS_VAR_* bits (arithmetic variants for sensitivity studies)
 
     def _c(self) -> CsConfig:
         c = CsConfig()
@@ -589,6 +660,7 @@ class SolverConfig:
             c.lambda_min, c.lambda_max = self.spectrum.lambda_min, self.spectrum.lambda_max
         c.lanczos_steps, c.seed = self.lanczos_steps, self.seed
         c.mode, c.check_every = _mode(self.mode), self.check_every
+        c.variant = self.variant
         c.collect_gram = int(self.collect_gram)
         c.track_true_residual = int(self.track_true_residual)
         c.collect_iterates = int(self.collect_iterates)
@@ -696,6 +768,12 @@ def pcg_s_solve(a: CsrMatrix, b, x0, m: Preconditioner, cfg: Optional[SolverConf
         raise InvalidArgumentError("SolverConfig: s must be in [1, 64]")
     b = _vec(b, a.n, "pcg_s_solve")
     x0 = _vec(x0, a.n, "pcg_s_solve")
+    if _general(m):  # block Jacobi / device plugin: upload, attach, solve
+        p = _with_problem(a, m, ctx)
+        try:
+            return p.pcg_s_solve(b, x0, cfg)
+        finally:
+            p.close()
     x = np.zeros(a.n)
     rep, bufs = _report(cfg.max_outer + 2, cfg.s, a.n, cfg)
     _check(lib.cs_pcg_s_solve_csr(ctx.handle, a.n, a.row_offsets.ctypes.data,

@@ -58,22 +58,17 @@ cs_ctx* ctx() {
   return c;
 }
 
+}  // namespace
+void attach_precond(cs_problem* p, const Preconditioner& m);
+namespace {
+
 // device-resident copy of a reference CsrMatrix for one call
 struct Problem {
   cs_problem* p = nullptr;
   Problem(const CsrMatrix& a, const Preconditioner* m) {
     check(cs_problem_upload_csr(ctx(), a.n, a.row_offsets.data(), a.col_indices.data(),
                                 a.values.data(), &p));
-    if (m) {
-      const std::string_view nm = m->name();
-      int kind = -1;
-      if (nm == "identity") kind = CS_PRECOND_IDENTITY;
-      if (nm == "jacobi") kind = CS_PRECOND_JACOBI;
-      if (kind < 0)
-        throw InvalidArgumentError("preconditioner '" + std::string(nm) +
-                                   "' has no device implementation (identity, jacobi)");
-      check(cs_problem_set_precond(p, kind));
-    }
+    if (m) attach_precond(p, *m);
   }
   ~Problem() { cs_problem_destroy(p); }
   Problem(const Problem&) = delete;
@@ -320,6 +315,70 @@ void JacobiPreconditioner::apply(std::span<const double> in, std::span<double> o
   if (in.size() != out.size() || in.size() != inv_diag_.size())
     throw DimensionError("jacobi: size mismatch");
   for (std::size_t i = 0; i < in.size(); ++i) out[i] = inv_diag_[i] * in[i];
+}
+
+// block Jacobi: host extraction + factorisation; the device factorises the same
+// blocks with the same operation order (vec.cu bj_factor_kernel)
+BlockJacobiPreconditioner::BlockJacobiPreconditioner(const CsrMatrix& a, int bs)
+    : bs_(bs), n_(a.n) {
+  if (bs < 1 || bs > 16) throw InvalidArgumentError("block_jacobi: bs must be in [1, 16]");
+  const index_t nb = (a.n + bs - 1) / bs;
+  const std::size_t q = static_cast<std::size_t>(bs) * bs;
+  blocks_.assign(static_cast<std::size_t>(nb) * q, 0.0);
+  for (index_t r = 0; r < nb * bs; ++r) {
+    double* blk = blocks_.data() + static_cast<std::size_t>(r / bs) * q;
+    const int i = static_cast<int>(r % bs);
+    if (r >= a.n) {
+      blk[i + i * bs] = 1.0;
+      continue;
+    }
+    const index_t b0 = (r / bs) * bs;
+    for (index_t k = a.row_offsets[r]; k < a.row_offsets[r + 1]; ++k) {
+      const index_t c = a.col_indices[k];
+      if (c >= b0 && c < b0 + bs) blk[i + (c - b0) * bs] += a.values[k];
+    }
+  }
+  factor_ = blocks_;
+  for (index_t b = 0; b < nb; ++b) {
+    double* L = factor_.data() + static_cast<std::size_t>(b) * q;
+    for (int j = 0; j < bs; ++j) {
+      double d = L[j + j * bs];
+      for (int t = 0; t < j; ++t) d -= L[j + t * bs] * L[j + t * bs];
+      if (!(d > 0.0) || !std::isfinite(d))
+        throw NotSpdError("block_jacobi: diagonal block " + std::to_string(b) +
+                          " is not positive definite");
+      const double dg = std::sqrt(d);
+      L[j + j * bs] = dg;
+      for (int i = j + 1; i < bs; ++i) {
+        double v = L[i + j * bs];
+        for (int t = 0; t < j; ++t) v -= L[i + t * bs] * L[j + t * bs];
+        L[i + j * bs] = v / dg;
+      }
+      for (int i = 0; i < j; ++i) L[i + j * bs] = 0.0;
+    }
+  }
+}
+
+void BlockJacobiPreconditioner::apply(std::span<const double> in, std::span<double> out) const {
+  if (in.size() != out.size() || static_cast<index_t>(in.size()) != n_)
+    throw DimensionError("block_jacobi: size mismatch");
+  const int bs = bs_;
+  std::vector<double> x(static_cast<std::size_t>(bs));
+  for (index_t r0 = 0; r0 < n_; r0 += bs) {
+    const double* L = factor_.data() + static_cast<std::size_t>(r0 / bs) * bs * bs;
+    for (int i = 0; i < bs; ++i) x[i] = r0 + i < n_ ? in[r0 + i] : 0.0;
+    for (int i = 0; i < bs; ++i) {
+      double v = x[i];
+      for (int t = 0; t < i; ++t) v -= L[i + t * bs] * x[t];
+      x[i] = v / L[i + i * bs];
+    }
+    for (int i = bs - 1; i >= 0; --i) {
+      double v = x[i];
+      for (int t = i + 1; t < bs; ++t) v -= L[t + i * bs] * x[t];
+      x[i] = v / L[i + i * bs];
+    }
+    for (int i = 0; i < bs && r0 + i < n_; ++i) out[r0 + i] = x[i];
+  }
 }
 
 // ------------------------------------------------------------------ problems
@@ -624,7 +683,11 @@ SolveResult run_pcg(const PcgConfig& cfg, index_t n, Call&& call) {
   c.max_outer = cfg.max_iter;
   c.mode = mode_code();
   c.collect_iterates = cfg.collect_iterates;
-  if (cfg.error_reference) c.error_reference = cfg.error_reference->data();
+  if (cfg.error_reference) {
+    if (static_cast<index_t>(cfg.error_reference->size()) != n)
+      throw DimensionError("pcg_solve: error_reference length mismatch");
+    c.error_reference = cfg.error_reference->data();
+  }
   SolveResult out;
   out.x.resize(static_cast<std::size_t>(n));
   const int cap = cfg.max_iter + 2;
@@ -647,13 +710,53 @@ int precond_kind(const Preconditioner& m) {
   if (kind < 0) throw InvalidArgumentError("preconditioner has no device implementation");
   return kind;
 }
+
+bool general_precond(const Preconditioner& m) {
+  return dynamic_cast<const BlockJacobiPreconditioner*>(&m) != nullptr ||
+         dynamic_cast<const gpu::DevicePreconditioner*>(&m) != nullptr;
+}
+
+int device_precond_trampoline(void* user, const double* in, double* out, int64_t n, void* stream) {
+  try {
+    static_cast<const gpu::DevicePreconditioner*>(user)->device_apply(in, out, n, stream);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
 }  // namespace
+
+// every preconditioner kind onto a problem: identity/jacobi (fused), block
+// Jacobi (device-factored blocks), device plugin
+void attach_precond(cs_problem* p, const Preconditioner& m) {
+  if (const auto* bj = dynamic_cast<const BlockJacobiPreconditioner*>(&m)) {
+    check(cs_problem_set_precond_block_jacobi(p, bj->block_size(), bj->blocks().data()));
+    return;
+  }
+  if (const auto* dp = dynamic_cast<const gpu::DevicePreconditioner*>(&m)) {
+    check(cs_problem_set_precond_fn(p, device_precond_trampoline,
+                                    const_cast<gpu::DevicePreconditioner*>(dp)));
+    return;
+  }
+  const std::string_view nm = m.name();
+  if (nm != "identity" && nm != "jacobi")
+    throw InvalidArgumentError("preconditioner '" + std::string(nm) +
+                               "' has no device implementation (identity, jacobi, "
+                               "BlockJacobiPreconditioner, gpu::DevicePreconditioner)");
+  check(cs_problem_set_precond(p, precond_kind(m)));
+}
 
 SolveResult pcg_s_solve(const CsrMatrix& a, std::span<const double> b, std::span<const double> x0,
                         const Preconditioner& m, const SolverConfig& cfg) {
   cfg.validate();
   if (static_cast<index_t>(b.size()) != a.n || static_cast<index_t>(x0.size()) != a.n)
     throw DimensionError("pcg_s_solve: vector length mismatch");
+  if (general_precond(m)) {  // upload, attach the device preconditioner, solve
+    Problem p(a, &m);
+    return run_pcgs(cfg, a.n, [&](const cs_config* c, double* x, cs_report* r) {
+      return cs_pcg_s_solve(p.p, b.data(), x0.data(), c, x, r);
+    });
+  }
   const int kind = precond_kind(m);
   return run_pcgs(cfg, a.n, [&](const cs_config* c, double* x, cs_report* r) {
     return cs_pcg_s_solve_csr(ctx(), a.n, a.row_offsets.data(), a.col_indices.data(),
@@ -718,7 +821,7 @@ DeviceProblem DeviceProblem::read_matrix_market(const std::string& path, bool re
   return DeviceProblem(p);
 }
 void DeviceProblem::set_precond(const Preconditioner& m) {
-  check(cs_problem_set_precond(p_, precond_kind(m)));
+  attach_precond(p_, m);
 }
 
 SolveResult pcg_s_solve(const DeviceProblem& p, std::span<const double> b,

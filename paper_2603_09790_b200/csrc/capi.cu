@@ -321,10 +321,11 @@ int cs_problem_read_mm(cs_ctx* ctx, const char* path, int require_spd, cs_proble
 int cs_problem_destroy(cs_problem* p) {
   return guard([&] {
     if (p) {
-      cudaSetDevice(p->ctx->device);
-      cudaStreamSynchronize(p->ctx->stream);
+      cs_ctx* c = p->ctx;
+      cudaSetDevice(c->device);
+      cudaStreamSynchronize(c->stream);
       p2p_teardown(p);
-      delete p;
+      delete p;  // ~cs_problem: buffers freed on c->stream, c->live_problems decremented
     }
   });
 }
@@ -365,6 +366,14 @@ int cs_problem_ghosts(cs_problem* p, int64_t* ghost_cols) {
 
 int cs_problem_set_precond(cs_problem* p, int kind) {
   return guard([&] { problem_set_precond(p, kind); });
+}
+
+int cs_problem_set_precond_block_jacobi(cs_problem* p, int bs, const double* blocks) {
+  return guard([&] { problem_set_precond_block_jacobi(p, bs, blocks); });
+}
+
+int cs_problem_set_precond_fn(cs_problem* p, cs_precond_fn fn, void* user) {
+  return guard([&] { problem_set_precond_fn(p, fn, user); });
 }
 
 int cs_problem_inv_diag(cs_problem* p, double* out) {
@@ -483,7 +492,7 @@ int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
       unsigned* ticket = reinterpret_cast<unsigned*>(sm + 4 * S * S + 2048);
       run = [&, ticket] {
         launch_pack(S, n, ld, v, v + S * ld, v + 2 * S * ld, v + 3 * S * ld, sm, part.as<double>(),
-                    ticket, nullptr, c->stream);
+                    ticket, nullptr, nullptr, c->stream);
       };
     } else {
       ua.s = S;
@@ -538,8 +547,7 @@ int cs_mpk(cs_problem* p, const double* r, int s, double lo, double hi, double* 
     DevState* dst = st.as<DevState>();
     {
       Launch L(c, CS_PHASE_UPDATE);
-      launch_precond_apply(n, p->view().inv_diag, rb.as<double>(), Zb.as<double>(), dst, 0, 0,
-                           c->stream);
+      precond_apply(p, rb.as<double>(), Zb.as<double>(), dst, 0, 0);
     }
     mpk_unit(p, Zb.as<double>(), Pb.as<double>(), rb.as<double>(), za.as<double>(),
              zb.as<double>(), s, lo, hi, dst);

@@ -145,6 +145,12 @@ struct LibError {
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// Launch setup of a kernel on the CURRENT device (thread-safe, cached per
+// (device, kernel, threads, smem)): opts in to `smem` bytes of dynamic shared
+// memory when above the 48 KB default (the attribute is per device) and
+// returns the resident blocks per SM from the occupancy API (>= 1).
+int kernel_setup(const void* func, int threads, int smem);
+
 }  // namespace csg
 
 #ifdef __CUDACC__

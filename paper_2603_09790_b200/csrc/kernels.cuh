@@ -25,10 +25,12 @@ void launch_csr_widths(int64_t n, const int64_t* rowptr, int64_t nslices, int64_
                        int* bad, cudaStream_t st);
 // row block [row_begin, row_begin+n) of an n_global CSR with global columns
 // (ghosts: sorted off-block columns, local n + index)
+// (streamed) rows [r0, r1) of the block, r0 % 32 == 0; col/val hold entries
+// [nnz_base, ...) of the block (the chunk's part of the host arrays)
 void launch_csr_fill(int64_t n, int64_t row_begin, int64_t n_global, const int64_t* ghosts,
                      int64_t n_ghost, const int64_t* rowptr, const int64_t* col, const double* val,
-                     int64_t nslices, const int64_t* slice_ptr, double* vals, int32_t* cols,
-                     double* diag, int* bad, cudaStream_t st);
+                     int64_t nnz_base, int64_t r0, int64_t r1, const int64_t* slice_ptr,
+                     double* vals, int32_t* cols, double* diag, int* bad, cudaStream_t st);
 void launch_slice_ghost_flag(int64_t n_local, int64_t nslices, const int64_t* slice_ptr,
                              const int32_t* cols, unsigned char* flag, cudaStream_t st);
 void launch_halo_gather(int64_t count, const int32_t* idx, const double* x, double* buf,
@@ -136,6 +138,12 @@ void launch_halo_release(const SpmvArgs& g, DevState* st, cudaStream_t s);
 void launch_precond_apply(int64_t n, const double* inv_diag, const double* in, double* out,
                           DevState* st, int col, int pending, cudaStream_t s);
 void launch_random_vector(int64_t n, int64_t offset, uint64_t seed, double* out, cudaStream_t s);
+// block Jacobi: in-place Cholesky of nblocks bs x bs blocks
+// (*bad_block = min failing block, caller initialises to INT_MAX); apply
+// out = M^-1 in with the breakdown check of launch_precond_apply
+void launch_bj_factor(int64_t nblocks, int bs, double* f, int* bad_block, cudaStream_t s);
+void launch_bj_apply(int64_t n, int bs, const double* f, const double* in, double* out,
+                     DevState* st, int col, int pending, cudaStream_t s);
 // serial ascending-order Gram: g[i + j*ku] = sum_l u_i[l] v_j[l]; one thread per entry.
 void launch_serial_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, const double* v,
                         int64_t ldv, double* g, DevState* st, cudaStream_t s);
@@ -146,9 +154,13 @@ void launch_tree_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, c
 size_t tree_gram_partial_doubles(int64_t n, int ku, int kv);
 // fast packed reduction {Q^T P, Z^T P, Z^T r, Q^T r, r^T r} (2s^2+2s+1 doubles)
 bool pack_supported(int s);
+// flags (multi-rank, or nullptr): s rank-local basis-breakdown column flags
+// written by the last block (see launch_pending_flags)
 void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket,
-                 DevState* st, cudaStream_t strm);
+                 DevState* st, double* flags, cudaStream_t strm);
+// flags[j] = 1.0 iff this rank's pending basis breakdown is in column j
+void launch_pending_flags(int s, const DevState* st, double* flags, cudaStream_t strm);
 size_t pack_partial_doubles(int s, int64_t n);
 // x/r/Q/AQ updates
 struct UpdateArgs {
@@ -174,6 +186,13 @@ struct UpdateArgs {
   int64_t send_lo = 0, hi_begin = 0;
 };
 void launch_fast_update(const UpdateArgs& a, cudaStream_t s);  // beta block update + x/r + z0
+// The same beta pass fused with the explicit Gram W = Q_new^T AQ_new of the
+// vectors it writes (raw, unsymmetrised s x s into wout via per-block partials
+// and last-block finalisation). false: s not supported, nothing launched.
+bool update_gram_supported(int s);
+size_t update_gram_partial_doubles(int s);
+bool launch_fast_update_gram(const UpdateArgs& a, double* partial, unsigned* ticket, double* wout,
+                             cudaStream_t s);
 void launch_ref_xr_update(const UpdateArgs& a, cudaStream_t s);   // solver.cpp:159-162
 void launch_ref_block_update(const UpdateArgs& a, cudaStream_t s);  // dense_ops.cpp:29-42 x2
 // generic block_update (unit entry)
@@ -201,6 +220,9 @@ struct SmallArgs {
   double* rel;     // history arrays
   double* da;
   double* db;
+  const double* Wexp = nullptr;  // fast: raw Q_k^T AQ_k of this outer (explicit W), or null
+  const double* flags = nullptr; // fast, multi-rank: allreduced basis-breakdown column flags
+  int fast_fgs = 1;              // fast: reassociated FGS sweeps (0 = reference sequence)
 };
 void launch_fast_setup(const SmallArgs& a, cudaStream_t s);   // W_1, alpha_1 from packed
 void launch_fast_step(const SmallArgs& a, cudaStream_t s);    // stop test, beta, recurrence, alpha

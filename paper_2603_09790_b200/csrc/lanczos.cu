@@ -23,17 +23,18 @@ __device__ __forceinline__ bool halted(const DevState* st) {
 }
 
 // r = M^-1 t - a v_j - b v_{j-1}; gr = t - a g_j - b g_{j-1}  (spectral.cpp:93-102)
+// mt != nullptr: M^-1 t was applied already (general preconditioners), r may alias it
 __global__ void resid_kernel(int64_t n, const double* __restrict__ t,
-                             const double* __restrict__ inv_diag, const double* __restrict__ vj,
-                             const double* __restrict__ gj, const double* __restrict__ vp,
-                             const double* __restrict__ gp, double* r, double* gr,
-                             const LanczosScalars* sc, int j, DevState* st) {
+                             const double* __restrict__ inv_diag, const double* mt,
+                             const double* __restrict__ vj, const double* __restrict__ gj,
+                             const double* __restrict__ vp, const double* __restrict__ gp,
+                             double* r, double* gr, const LanczosScalars* sc, int j, DevState* st) {
   if (halted(st)) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double a = sc->alpha[j];
   const double tv = t[i];
-  double rv = inv_diag ? __dmul_rn(inv_diag[i], tv) : tv;
+  double rv = mt ? mt[i] : inv_diag ? __dmul_rn(inv_diag[i], tv) : tv;
   double gv = tv;
   rv = __dadd_rn(rv, __dmul_rn(-a, vj[i]));
   gv = __dadd_rn(gv, __dmul_rn(-a, gj[i]));
@@ -57,7 +58,10 @@ __global__ void axpy2_kernel(int64_t n, const double* __restrict__ v, const doub
   gr[i] = __dadd_rn(gr[i], __dmul_rn(-p, g[i]));
 }
 
-// fast CGS correction over all stored pairs, fused with the r.gr block sums
+// fast CGS correction over all stored pairs, fused with the r.gr block sums.
+// MB > 0: at most MB pairs, the loop unrolled so every row's 2m loads are in
+// flight together (a runtime-bounded loop issued them two at a time).
+template <int MB>
 __global__ void __launch_bounds__(kThreads)
     cgs_kernel(int64_t n, int64_t ld, int m, const double* __restrict__ V,
                const double* __restrict__ G, double* r, double* gr, const double* proj,
@@ -72,9 +76,25 @@ __global__ void __launch_bounds__(kThreads)
   double d = 0.0;
   if (i < n) {
     double rv = r[i], gv = gr[i];
-    for (int c = 0; c < m; ++c) {
-      rv = fma(-sp[c], V[c * ld + i], rv);
-      gv = fma(-sp[c], G[c * ld + i], gv);
+    if constexpr (MB > 0) {
+      double vv[MB], gg[MB];
+#pragma unroll
+      for (int c = 0; c < MB; ++c)
+        if (c < m) {
+          vv[c] = __ldcs(V + c * ld + i);
+          gg[c] = __ldcs(G + c * ld + i);
+        }
+#pragma unroll
+      for (int c = 0; c < MB; ++c)
+        if (c < m) {
+          rv = fma(-sp[c], vv[c], rv);
+          gv = fma(-sp[c], gg[c], gv);
+        }
+    } else {
+      for (int c = 0; c < m; ++c) {
+        rv = fma(-sp[c], V[c * ld + i], rv);
+        gv = fma(-sp[c], G[c * ld + i], gv);
+      }
     }
     r[i] = rv;
     gr[i] = gv;
@@ -98,6 +118,57 @@ __global__ void __launch_bounds__(kThreads)
     finalize_partials(partial, gridDim.x, 1, result);
     if (threadIdx.x == 0) *ticket = 0u;
   }
+}
+
+// fast CGS projections proj[i] = g_i . r for i < m in ONE pass: r is read
+// once, each g_i once; every thread keeps m accumulators over a grid-stride
+// row sweep (fixed grid: deterministic), then a fixed warp/block tree and
+// last-block finalisation in block order.
+constexpr int kProjBlocks = 296;  // 2 x 148 SMs x 8 warps, up to 40 loads per lane in flight
+
+template <int MB>
+__global__ void __launch_bounds__(kThreads)
+    proj_kernel(int64_t n, int64_t ld, int m, const double* __restrict__ G,
+                const double* __restrict__ r, double* proj, double* partial, unsigned* ticket,
+                DevState* st) {
+  if (halted(st)) return;
+  __shared__ double red[MB][kThreads / 32];
+  __shared__ bool last;
+  double acc[MB];
+#pragma unroll
+  for (int c = 0; c < MB; ++c) acc[c] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    const double rv = __ldcs(r + i);
+#pragma unroll
+    for (int c = 0; c < MB; ++c)
+      if (c < m) acc[c] = fma(__ldcs(G + c * ld + i), rv, acc[c]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < MB; ++c) {
+    if (c < m) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], off);
+      if (lane == 0) red[c][warp] = acc[c];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < m; c += kThreads) {
+    double sum = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) sum += red[c][w];
+    partial[static_cast<int64_t>(blockIdx.x) * m + c] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_partials(partial, gridDim.x, m, proj);
+  if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // scalar steps: 0 normalise start (nrm = sqrt(v.g) > 0), 1 alpha_j (finite),
@@ -143,11 +214,12 @@ __global__ void scalar_kernel(int which, int j, int steps, LanczosScalars* sc, D
 
 }  // namespace
 
-void lz_resid(int64_t n, const double* t, const double* inv_diag, const double* vj,
-              const double* gj, const double* vp, const double* gp, double* r, double* gr,
-              const LanczosScalars* sc, int j, DevState* st, cudaStream_t s) {
+void lz_resid(int64_t n, const double* t, const double* inv_diag, const double* mt,
+              const double* vj, const double* gj, const double* vp, const double* gp, double* r,
+              double* gr, const LanczosScalars* sc, int j, DevState* st, cudaStream_t s) {
   if (n == 0) return;
-  resid_kernel<<<grid_for(n), kThreads, 0, s>>>(n, t, inv_diag, vj, gj, vp, gp, r, gr, sc, j, st);
+  resid_kernel<<<grid_for(n), kThreads, 0, s>>>(n, t, inv_diag, mt, vj, gj, vp, gp, r, gr, sc, j,
+                                                st);
   CS_CUDA(cudaGetLastError());
 }
 
@@ -163,8 +235,33 @@ int lz_cgs_blocks(int64_t n) { return static_cast<int>(grid_for(n > 0 ? n : 1));
 void lz_cgs(int64_t n, int64_t ld, int m, const double* V, const double* G, double* r, double* gr,
             const double* proj, double* partial, unsigned* ticket, double* result, DevState* st,
             cudaStream_t s) {
-  cgs_kernel<<<grid_for(n > 0 ? n : 1), kThreads, 0, s>>>(n, ld, m, V, G, r, gr, proj, partial,
-                                                         ticket, result, st);
+  const unsigned grid = grid_for(n > 0 ? n : 1);
+#define CSG_CGS(MB) \
+  cgs_kernel<MB><<<grid, kThreads, 0, s>>>(n, ld, m, V, G, r, gr, proj, partial, ticket, result, st)
+  if (m <= 8) CSG_CGS(8);
+  else if (m <= 16) CSG_CGS(16);
+  else if (m <= 24) CSG_CGS(24);
+  else if (m <= 32) CSG_CGS(32);
+  else if (m <= 40) CSG_CGS(40);
+  else CSG_CGS(0);
+#undef CSG_CGS
+  CS_CUDA(cudaGetLastError());
+}
+
+bool lz_proj_supported(int m) { return m >= 1 && m <= 40; }
+
+size_t lz_proj_partial_doubles(int m) { return static_cast<size_t>(kProjBlocks) * m; }
+
+void lz_proj(int64_t n, int64_t ld, int m, const double* G, const double* r, double* proj,
+             double* partial, unsigned* ticket, DevState* st, cudaStream_t s) {
+#define CSG_PROJ(MB) \
+  proj_kernel<MB><<<kProjBlocks, kThreads, 0, s>>>(n, ld, m, G, r, proj, partial, ticket, st)
+  if (m <= 8) CSG_PROJ(8);
+  else if (m <= 16) CSG_PROJ(16);
+  else if (m <= 24) CSG_PROJ(24);
+  else if (m <= 32) CSG_PROJ(32);
+  else CSG_PROJ(40);
+#undef CSG_PROJ
   CS_CUDA(cudaGetLastError());
 }
 

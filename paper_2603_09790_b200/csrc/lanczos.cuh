@@ -15,15 +15,22 @@ struct LanczosScalars {
   int count;     // completed alpha entries
 };
 
-void lz_resid(int64_t n, const double* t, const double* inv_diag, const double* vj,
-              const double* gj, const double* vp, const double* gp, double* r, double* gr,
-              const LanczosScalars* sc, int j, DevState* st, cudaStream_t s);
+// r = M^-1 t - a v_j - b v_{j-1}, gr = t - a g_j - b g_{j-1}; M^-1 t from inv_diag,
+// or precomputed in mt (general preconditioners; r may alias mt)
+void lz_resid(int64_t n, const double* t, const double* inv_diag, const double* mt,
+              const double* vj, const double* gj, const double* vp, const double* gp, double* r,
+              double* gr, const LanczosScalars* sc, int j, DevState* st, cudaStream_t s);
 void lz_axpy2(int64_t n, const double* v, const double* g, double* r, double* gr,
               const double* proj, DevState* st, cudaStream_t s);
 int lz_cgs_blocks(int64_t n);
 void lz_cgs(int64_t n, int64_t ld, int m, const double* V, const double* G, double* r, double* gr,
             const double* proj, double* partial, unsigned* ticket, double* result, DevState* st,
             cudaStream_t s);
+// fast CGS projections proj[i] = G_i . r (i < m <= 40) in one pass over r and G
+bool lz_proj_supported(int m);
+size_t lz_proj_partial_doubles(int m);
+void lz_proj(int64_t n, int64_t ld, int m, const double* G, const double* r, double* proj,
+             double* partial, unsigned* ticket, DevState* st, cudaStream_t s);
 void lz_scalar(int which, int j, int steps, LanczosScalars* sc, DevState* st, cudaStream_t s);
 
 // host: eigenvalues of the symmetric tridiagonal (d[m], e[m-1]) ascending

@@ -5,6 +5,9 @@
 #include <climits>
 #include <cmath>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -146,6 +149,32 @@ void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand) {
     // both boundary ranges [ie, nslices) and [0, ib) in one wrapped launch
     launch_spmv(kind, A, g, p->slice_int_end, p->nslices + p->slice_int_begin, c->stream);
   }
+}
+
+int kernel_setup(const void* func, int threads, int smem) {
+  struct Key {
+    int dev;
+    const void* f;
+    int threads, smem;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, f, threads, smem) < std::tie(o.dev, o.f, o.threads, o.smem);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  int dev = 0;
+  CS_CUDA(cudaGetDevice(&dev));
+  const Key k{dev, func, threads, smem};
+  std::lock_guard<std::mutex> lock(mu);
+  const auto it = cache.find(k);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    CS_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem));
+  per_sm = std::max(per_sm, 1);
+  cache.emplace(k, per_sm);
+  return per_sm;
 }
 
 void allreduce_sum(cs_ctx* c, double* dev, size_t count) {
@@ -398,6 +427,12 @@ cs_ctx* ctx_create(int device) {
 
 void ctx_destroy(cs_ctx* c) {
   if (c == nullptr) return;
+  // a problem's buffers are freed on this context's stream: destroying the
+  // context first would leave cs_problem_destroy a dangling stream
+  if (c->live_problems.load() > 0)
+    fail(CS_ERR_INVALID_ARGUMENT, c->live_problems.load(),
+         "cs_ctx_destroy: " + std::to_string(c->live_problems.load()) +
+             " problem(s) of this context are still alive; destroy them first");
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto& s : c->spans) {
@@ -747,7 +782,7 @@ cs_problem* problem_generate(cs_ctx* c, int kind, int64_t nx, int64_t ny, int64_
   CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
   auto p = std::make_unique<cs_problem>();
-  p->ctx = c;
+  p->attach(c);
   p->gen_kind = kind;
   p->nx = nx, p->ny = ny, p->nz = nz;
   const int64_t plane = nx * ny;
@@ -932,6 +967,68 @@ struct UploadTrace {
 };
 }  // namespace
 
+// Column/value upload of a CSR row block, streamed: slice-aligned row chunks
+// of <= kChunkNnz entries go host -> device on the copy stream through two
+// staging buffers while the SELL-32 fill of the previous chunk runs on the
+// compute stream. Device memory: 2 chunks instead of the whole int64 CSR
+// (58.8 GB at 27-pt 512^3); the host arrays may be pageable (the caller's
+// std::vector), each chunk is one cudaMemcpyAsync per array.
+void stream_csr_fill(cs_problem* p, const int64_t* rowptr, const int64_t* col, const double* val,
+                     const int64_t* drp, int* bad) {
+  cs_ctx* c = p->ctx;
+  const int64_t n = p->n_local;
+  if (n == 0) return;
+  const char* env = std::getenv("CS_UPLOAD_CHUNK_NNZ");
+  const int64_t kChunkNnz = env ? std::max<int64_t>(std::atoll(env), 1) : (int64_t{1} << 25);
+  std::vector<int64_t> cut{0};
+  int64_t most = 0;
+  for (int64_t r = 0; r < n;) {
+    int64_t e = std::min(n, r + kSliceRows);
+    while (e < n && rowptr[std::min(n, e + kSliceRows)] - rowptr[r] <= kChunkNnz)
+      e = std::min(n, e + kSliceRows);
+    most = std::max(most, rowptr[e] - rowptr[r]);
+    cut.push_back(e);
+    r = e;
+  }
+  const size_t cap = static_cast<size_t>(std::max<int64_t>(most, 1));
+  DBuf stage[2];
+  for (auto& b : stage) b.alloc(16 * cap);
+  cudaEvent_t ready, copied[2], filled[2];
+  CS_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    CS_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    CS_CUDA(cudaEventCreateWithFlags(&filled[i], cudaEventDisableTiming));
+  }
+  CS_CUDA(cudaEventRecord(ready, c->stream));  // staging allocations are stream-ordered
+  CS_CUDA(cudaStreamWaitEvent(c->comm_stream, ready, 0));
+  for (size_t k = 0; k + 1 < cut.size(); ++k) {
+    const int b = static_cast<int>(k & 1);
+    const int64_t r0 = cut[k], r1 = cut[k + 1];
+    const int64_t e0 = rowptr[r0], cnt = rowptr[r1] - e0;
+    int64_t* scol = stage[b].as<int64_t>();
+    double* sval = reinterpret_cast<double*>(scol + cap);
+    if (k >= 2) CS_CUDA(cudaStreamWaitEvent(c->comm_stream, filled[b], 0));
+    if (cnt > 0) {
+      CS_CUDA(cudaMemcpyAsync(scol, col + e0, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice,
+                              c->comm_stream));
+      CS_CUDA(cudaMemcpyAsync(sval, val + e0, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                              c->comm_stream));
+    }
+    CS_CUDA(cudaEventRecord(copied[b], c->comm_stream));
+    CS_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
+    launch_csr_fill(n, p->row_begin, p->n_global, p->ghost_global.as<int64_t>(), p->n_ghost, drp,
+                    scol, sval, e0, r0, r1, p->slice_ptr.as<int64_t>(), p->vals.as<double>(),
+                    p->cols.as<int32_t>(), p->diag.as<double>(), bad, c->stream);
+    CS_CUDA(cudaEventRecord(filled[b], c->stream));
+  }
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  cudaEventDestroy(ready);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(filled[i]);
+  }
+}
+
 cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin, int64_t row_end,
                                  const int64_t* rowptr, const int64_t* col, const double* val) {
   if (n_global < 0 || row_begin < 0 || row_end < row_begin || row_end > n_global)
@@ -946,7 +1043,7 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
   StreamBind bind_stream_(c->stream);
   UploadTrace ut(c->stream);
   auto p = std::make_unique<cs_problem>();
-  p->ctx = c;
+  p->attach(c);
   p->n_global = n_global;
   p->row_begin = row_begin;
   p->n_local = n;
@@ -969,16 +1066,12 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
   if (p->n_ghost)
     CS_CUDA(cudaMemcpyAsync(p->ghost_global.p, p->ghosts_host.data(), sizeof(int64_t) * p->n_ghost,
                             cudaMemcpyHostToDevice, c->stream));
-  DBuf drp(sizeof(int64_t) * (n + 1)), dcol(sizeof(int64_t) * std::max<int64_t>(nnz, 1)),
-      dval(sizeof(double) * std::max<int64_t>(nnz, 1)), bad(sizeof(int));
+  // rowptr first: the slice widths validate it on the device before any
+  // column/value byte moves
+  DBuf drp(sizeof(int64_t) * (n + 1)), bad(sizeof(int));
   CS_CUDA(cudaMemcpyAsync(drp.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice,
                           c->stream));
-  if (nnz) {
-    CS_CUDA(cudaMemcpyAsync(dcol.p, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, c->stream));
-    CS_CUDA(cudaMemcpyAsync(dval.p, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
-  }
   CS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
-  ut.mark("alloc+h2d");
   p->slice_ptr.alloc(sizeof(int64_t) * (p->nslices + 1));
   if (p->nslices > 0) {
     DBuf widths(sizeof(int64_t) * p->nslices);
@@ -991,20 +1084,17 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
   int hbad = 0;
   CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   const int64_t total = read_i64(c, p->slice_ptr.as<int64_t>() + p->nslices);
+  ut.mark("rowptr h2d+widths");
   // a local validation failure must not leave peers waiting in the halo plan
   int local_err = hbad ? 1 : 0;
   if (!local_err) {
     p->vals.alloc(sizeof(double) * std::max<int64_t>(total, 1));
     p->cols.alloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
     p->diag.alloc(sizeof(double) * std::max<int64_t>(n, 1));
-    if (p->nslices > 0)
-      launch_csr_fill(n, row_begin, n_global, p->ghost_global.as<int64_t>(), p->n_ghost,
-                      drp.as<int64_t>(), dcol.as<int64_t>(), dval.as<double>(), p->nslices,
-                      p->slice_ptr.as<int64_t>(), p->vals.as<double>(), p->cols.as<int32_t>(),
-                      p->diag.as<double>(), bad.as<int>(), c->stream);
+    stream_csr_fill(p.get(), rowptr, col, val, drp.as<int64_t>(), bad.as<int>());
     CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CS_CUDA(cudaStreamSynchronize(c->stream));
-    ut.mark("widths+fill");
+    ut.mark("col/val h2d+fill (streamed)");
     local_err = hbad ? 2 : 0;
   }
   if (c->nranks > 1) {
@@ -1037,6 +1127,69 @@ cs_problem* problem_upload_csr(cs_ctx* c, int64_t n, const int64_t* rowptr, cons
   return problem_upload_block(c, n, 0, n, rowptr, col, val);
 }
 
+// Block Jacobi: the caller's dense diagonal blocks are uploaded
+// and factorised on the device; apply = two triangular solves per block.
+void problem_set_precond_block_jacobi(cs_problem* p, int bs, const double* blocks) {
+  cs_ctx* c = p->ctx;
+  if (bs < 1 || bs > 16) fail(CS_ERR_INVALID_ARGUMENT, 0, "block_jacobi: bs must be in [1, 16]");
+  CS_CUDA(cudaSetDevice(c->device));
+  StreamBind bind_stream_(c->stream);
+  const int64_t nb = (p->n_local + bs - 1) / bs;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(nb) * bs * bs;
+  DBuf f(std::max<size_t>(bytes, 8)), bad(sizeof(int));
+  if (bytes)
+    CS_CUDA(cudaMemcpyAsync(f.p, blocks, bytes, cudaMemcpyHostToDevice, c->stream));
+  const int big = INT_MAX;
+  CS_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  {
+    Launch L(c, CS_PHASE_OTHER);
+    launch_bj_factor(nb, bs, f.as<double>(), bad.as<int>(), c->stream);
+  }
+  int hbad = big;
+  CS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  if (hbad != big)
+    fail(CS_ERR_NOT_SPD, hbad,
+         "block_jacobi: diagonal block " + std::to_string(hbad) + " is not positive definite");
+  p->pc_factor = std::move(f);
+  p->pc_bs = bs;
+  p->pc_fn = nullptr;
+  p->precond = CS_PRECOND_BLOCK_JACOBI;
+}
+
+void problem_set_precond_fn(cs_problem* p, cs_precond_fn fn, void* user) {
+  if (fn == nullptr) fail(CS_ERR_INVALID_ARGUMENT, 0, "precond fn must not be NULL");
+  p->pc_fn = fn;
+  p->pc_user = user;
+  p->pc_factor.release();
+  p->pc_bs = 0;
+  p->precond = CS_PRECOND_DEVICE_FN;
+}
+
+// out = M^-1 in on the context stream for every preconditioner kind, with the
+// basis-breakdown check of column `col` (col < 0: none; pending: record in
+// st->pending, the fast algebra's speculative MPK). The caller accounts the
+// launch (Launch scope).
+void precond_apply(cs_problem* p, const double* in, double* out, DevState* st, int col,
+                   int pending) {
+  cs_ctx* c = p->ctx;
+  const int64_t n = p->n_local;
+  switch (p->precond) {
+    case CS_PRECOND_BLOCK_JACOBI:
+      launch_bj_apply(n, p->pc_bs, p->pc_factor.as<double>(), in, out, st, col, pending,
+                      c->stream);
+      return;
+    case CS_PRECOND_DEVICE_FN:
+      if (p->pc_fn(p->pc_user, in, out, n, c->stream) != 0)
+        fail(CS_ERR_GENERIC, 0, "device preconditioner apply failed");
+      CS_CUDA(cudaGetLastError());
+      if (col >= 0) launch_precond_apply(n, nullptr, out, out, st, col, pending, c->stream);
+      return;
+    default:
+      launch_precond_apply(n, p->view().inv_diag, in, out, st, col, pending, c->stream);
+  }
+}
+
 void problem_set_precond(cs_problem* p, int kind) {
   cs_ctx* c = p->ctx;
   CS_CUDA(cudaSetDevice(c->device));
@@ -1045,6 +1198,9 @@ void problem_set_precond(cs_problem* p, int kind) {
     p->precond = kind;
     return;
   }
+  if (kind == CS_PRECOND_BLOCK_JACOBI || kind == CS_PRECOND_DEVICE_FN)
+    fail(CS_ERR_INVALID_ARGUMENT, 0,
+         "set the block-Jacobi / device preconditioner with its own entry point");
   if (kind != CS_PRECOND_JACOBI) fail(CS_ERR_INVALID_ARGUMENT, 0, "unknown preconditioner");
   if (!p->inv_diag.p) p->inv_diag.alloc(sizeof(double) * std::max<int64_t>(p->n_local, 1));
   DBuf bad(sizeof(int));

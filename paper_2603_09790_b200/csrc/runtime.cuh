@@ -3,6 +3,7 @@
 // device-resident problems (SELL matrix + preconditioner + halo layout) and
 // the cached per-problem solve workspace.
 #pragma once
+#include <atomic>
 #include <nccl.h>
 
 #include <array>
@@ -102,6 +103,7 @@ struct cs_ctx {
   std::vector<csg::TimedSpan> spans;
   std::vector<cudaEvent_t> event_pool;
   int64_t allreduces = 0;
+  std::atomic<int> live_problems{0};  // problems created on this context, not yet destroyed
   // scratch
   csg::DBuf state;      // DevState
   csg::DBuf scratch;    // partials / tickets / scalars
@@ -114,6 +116,18 @@ struct cs_ctx {
 
 struct cs_problem {
   cs_ctx* ctx = nullptr;
+  // every problem is counted on its context from creation to destruction: its
+  // pooled buffers are freed on the context's stream (see ctx_destroy)
+  void attach(cs_ctx* c) {
+    ctx = c;
+    ++c->live_problems;
+  }
+  cs_problem() = default;
+  cs_problem(const cs_problem&) = delete;
+  cs_problem& operator=(const cs_problem&) = delete;
+  ~cs_problem() {
+    if (ctx) --ctx->live_problems;
+  }
   int64_t n_global = 0, row_begin = 0, n_local = 0, n_ghost = 0, ld = 0, nnz_local = 0;
   int64_t nslices = 0;
   int64_t slice_int_begin = 0, slice_int_end = 0;  // interior slices (no ghost columns)
@@ -137,6 +151,14 @@ struct cs_problem {
   int max_width = 0;
   std::vector<int64_t> ghosts_host;
   int precond = CS_PRECOND_IDENTITY;
+  // general (non-diagonal) preconditioners, SURVEY 8f4
+  int pc_bs = 0;              // block Jacobi: rows per block
+  csg::DBuf pc_factor;        // block Jacobi: Cholesky factors, bs*bs per block
+  cs_precond_fn pc_fn = nullptr;
+  void* pc_user = nullptr;
+  bool precond_general() const {
+    return precond == CS_PRECOND_BLOCK_JACOBI || precond == CS_PRECOND_DEVICE_FN;
+  }
   // cached solve workspace and Lanczos basis (reused across solves)
   int ws_s = -1;
   uint64_t ws_gen = 0;  // bumped whenever ws is (re)allocated
@@ -199,6 +221,13 @@ void collect_timing(cs_ctx* c);
 void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand_col);
 void halo_exchange(cs_problem* p, double* col);
 void allreduce_sum(cs_ctx* c, double* dev, size_t count);
+// out = M^-1 in for every preconditioner kind (+ the breakdown check of column
+// col >= 0, recorded as pending when `pending`); general kinds: block Jacobi,
+// device plugin
+void precond_apply(cs_problem* p, const double* in, double* out, DevState* st, int col,
+                   int pending);
+void problem_set_precond_block_jacobi(cs_problem* p, int bs, const double* blocks);
+void problem_set_precond_fn(cs_problem* p, cs_precond_fn fn, void* user);
 // NVLink halo: map the neighbours' workspaces (collective over the communicator;
 // every rank calls it once per solve after its workspace is final). Returns
 // whether the peer-memory path is on for this solve (all ranks agree).

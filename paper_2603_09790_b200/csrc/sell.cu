@@ -180,15 +180,20 @@ __device__ __forceinline__ int32_t local_col(int64_t c, int64_t row_begin, int64
   return static_cast<int32_t>(n + lo);
 }
 
+// Rows [r0, r1) (r0 a multiple of 32) whose column/value entries sit in
+// col/val at offset rowptr[row] - nnz_base (one streamed chunk of the upload).
 __global__ void csr_fill_kernel(int64_t n, int64_t row_begin, int64_t n_global,
                                 const int64_t* __restrict__ ghosts, int64_t n_ghost,
                                 const int64_t* __restrict__ rowptr,
-                                const int64_t* __restrict__ col, const double* __restrict__ val,
-                                int64_t nslices, const int64_t* __restrict__ slice_ptr,
+                                const int64_t* __restrict__ col_c, const double* __restrict__ val_c,
+                                int64_t nnz_base, int64_t r0, int64_t slice_end,
+                                const int64_t* __restrict__ slice_ptr,
                                 double* vals, int32_t* cols, double* diag_out, int* bad) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t slice = row >> 5;
-  if (slice >= nslices) return;
+  if (slice >= slice_end) return;
+  const int64_t* col = col_c - nnz_base;  // indexed by the global entry position
+  const double* val = val_c - nnz_base;
   const int lane = threadIdx.x & 31;
   const int64_t base = slice_ptr[slice];
   const int width = static_cast<int>((slice_ptr[slice + 1] - base) >> 5);
@@ -605,11 +610,13 @@ void launch_csr_widths(int64_t n, const int64_t* rowptr, int64_t nslices, int64_
 
 void launch_csr_fill(int64_t n, int64_t row_begin, int64_t n_global, const int64_t* ghosts,
                      int64_t n_ghost, const int64_t* rowptr, const int64_t* col, const double* val,
-                     int64_t nslices, const int64_t* slice_ptr, double* vals, int32_t* cols,
-                     double* diag, int* bad, cudaStream_t st) {
-  csr_fill_kernel<<<grid_for(nslices * 32), kThreads, 0, st>>>(
-      n, row_begin, n_global, ghosts, n_ghost, rowptr, col, val, nslices, slice_ptr, vals, cols,
-      diag, bad);
+                     int64_t nnz_base, int64_t r0, int64_t r1, const int64_t* slice_ptr,
+                     double* vals, int32_t* cols, double* diag, int* bad, cudaStream_t st) {
+  const int64_t s0 = r0 / kSliceRows, s1 = (r1 + kSliceRows - 1) / kSliceRows;
+  if (s1 <= s0) return;
+  csr_fill_kernel<<<grid_for((s1 - s0) * 32), kThreads, 0, st>>>(
+      n, row_begin, n_global, ghosts, n_ghost, rowptr, col, val, nnz_base, r0, s1, slice_ptr, vals,
+      cols, diag, bad);
   CS_CUDA(cudaGetLastError());
 }
 

@@ -311,7 +311,7 @@ __global__ void fast_setup_kernel(SmallArgs a) {
     return;
   }
   double delta;
-  const int bad = solve_dev<S>(a, m.W, 1, m.rhs, m.x, &delta, m.scr, true);
+  const int bad = solve_dev<S>(a, m.W, 1, m.rhs, m.x, &delta, m.scr, a.fast_fgs != 0);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, 1);
     return;
@@ -351,6 +351,14 @@ __global__ void fast_step_kernel(SmallArgs a) {
       st->converged = 1;
       st->done = 1;
       stop = 1;
+    } else if (a.flags) {  // multi-rank: the lowest breakdown column of any rank
+      for (int j = 0; j < s; ++j)
+        if (a.flags[j] != 0.0) {
+          st->err = make_err(4, j);
+          st->done = 1;
+          stop = 1;
+          break;
+        }
     } else if (st->pending != 0ull) {
       st->err = st->pending;
       st->done = 1;
@@ -358,13 +366,20 @@ __global__ void fast_step_kernel(SmallArgs a) {
     }
   }
   for (int e = threadIdx.x; e < q; e += blockDim.x) {
-    m.W[e] = a.W[e];
+    m.W[e] = a.Wexp ? a.Wexp[e] : a.W[e];
     m.rhs[e] = -G1[e];
   }
   __syncthreads();
   if (stop) return;
+  // explicit W_k: assembled from this outer's vectors like assemble_gram
+  // (gram.cpp:38-49), it replaces the recurrence's W_k for beta_k and as the
+  // base of W_{k+1}, so the recurrence error never compounds past one step
+  if (a.Wexp && !symmetrise_check(s, m.W)) {
+    if (threadIdx.x == 0) raise(st, 5, kSubAssembly, k);
+    return;
+  }
   double delta;
-  int bad = solve_dev<S>(a, m.W, s, m.rhs, m.x, &delta, m.scr, true);
+  int bad = solve_dev<S>(a, m.W, s, m.rhs, m.x, &delta, m.scr, a.fast_fgs != 0);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, k);
     return;
@@ -405,7 +420,7 @@ __global__ void fast_step_kernel(SmallArgs a) {
     if (threadIdx.x == 0) raise(st, 5, kSubAssembly, k + 1);
     return;
   }
-  bad = solve_dev<S>(a, m.Wn, 1, m.rhs, m.x, &delta, m.scr, true);
+  bad = solve_dev<S>(a, m.Wn, 1, m.rhs, m.x, &delta, m.scr, a.fast_fgs != 0);
   if (bad) {
     if (threadIdx.x == 0) raise(st, 5, bad, k + 1);
     return;

@@ -136,7 +136,8 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
   double* t = G + steps * ld;
   double* r = t + ld;
   double* gr = r + ld;
-  const size_t tree_part = tree_gram_partial_doubles(n, steps, 1);
+  const size_t tree_part = std::max(tree_gram_partial_doubles(n, steps, 1),
+                                    lz_proj_partial_doubles(std::min(steps, 40)));
   const size_t part = std::max<size_t>(tree_part, static_cast<size_t>(lz_cgs_blocks(n)) + 16);
   char* scr = static_cast<char*>(ctx_scratch(
       c, sizeof(LanczosScalars) + sizeof(double) * (part + spmv_dot_blocks(p->nslices)) + 4096));
@@ -157,9 +158,10 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
     auto l = L();
     launch_random_vector(n, p->row_begin, seed, G, c->stream);
   }
+  const bool general = p->precond_general();
   {
     auto l = L();
-    launch_precond_apply(n, inv, G, V, nullptr, -1, 0, c->stream);
+    precond_apply(p, G, V, nullptr, -1, 0);
   }
   auto reduce_dot = [&](const double* u, const double* v) {
     auto l = L();
@@ -199,10 +201,14 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
       auto l = L();
       lz_scalar(1, j, steps, sc, st, c->stream);
     }
+    if (general) {  // r = M^-1 t first (spectral.cpp:94)
+      auto l = L();
+      precond_apply(p, t, r, st, -1, 0);
+    }
     {
       auto l = L();
-      lz_resid(n, t, inv, vj, gj, j > 0 ? vj - ld : nullptr, j > 0 ? gj - ld : nullptr, r, gr, sc,
-               j, st, c->stream);
+      lz_resid(n, t, inv, general ? r : nullptr, vj, gj, j > 0 ? vj - ld : nullptr,
+               j > 0 ? gj - ld : nullptr, r, gr, sc, j, st, c->stream);
     }
     if (mode == CS_MODE_REFERENCE) {
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, spectral.cpp:104-108
@@ -215,9 +221,12 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
       }
       reduce_dot(r, gr);
     } else {
-      {  // classical Gram-Schmidt: all projections in one pass
+      {  // classical Gram-Schmidt: all projections in one pass over r and G
         auto l = L();
-        launch_tree_gram(n, j + 1, 1, G, ld, r, ld, sc->proj, partial, ticket + 2, st, c->stream);
+        if (lz_proj_supported(j + 1))
+          lz_proj(n, ld, j + 1, G, r, sc->proj, partial, ticket + 2, st, c->stream);
+        else
+          launch_tree_gram(n, j + 1, 1, G, ld, r, ld, sc->proj, partial, ticket + 2, st, c->stream);
       }
       allreduce_sum(c, sc->proj, j + 1);
       auto l = L();
@@ -295,10 +304,14 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
   const double sigma = (hi + lo) / (hi - lo);     // mpk.hpp:23-25
   const double gamma = 1.0;
   const bool jac = p->precond == CS_PRECOND_JACOBI;
+  // general preconditioner (block Jacobi, device plugin): the reference
+  // recurrence on zp with an identity epilogue writing zp_q, then z_q = M^-1 zp_q
+  const bool gen = p->precond_general();
+  if (gen) fast = false;
   auto zcol = [&](int q) { return bk.Z + q * ld; };
   auto zp = [&](int q) -> double* {  // zp_q storage
     if (q == 0) return bk.r;
-    if (!jac) return zcol(q);
+    if (!jac && !gen) return zcol(q);
     return (q & 1) ? bk.zpA : bk.zpB;
   };
   for (int q = 1; q < s; ++q) {
@@ -308,7 +321,7 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     g.zp1 = zp(q - 1);
     g.zp2 = q >= 2 ? (fast ? zcol(q - 2) : zp(q - 2)) : nullptr;
     g.zpout = jac && !fast ? zp(q) : nullptr;
-    g.zout = zcol(q);
+    g.zout = gen ? zp(q) : zcol(q);
     if (q == 1) {
       g.ca = alpha;
       g.cb = -sigma;
@@ -322,8 +335,13 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     g.pending = pending;
     g.st = st;
     const int kind = fast ? (q == 1 ? kMpkFirstF : kMpkMidF) : (q == 1 ? kMpkFirst : kMpkMid);
+    if (gen) g.col = -1;  // the breakdown check follows the apply
     if (p2p) spmv_p2p(p, kind, g, q);  // z_q's boundary rows go straight to the neighbours
     else spmv_halo(p, kind, g, zcol(q - 1));
+    if (gen) {
+      Launch L(p->ctx, CS_PHASE_UPDATE);
+      precond_apply(p, zp(q), zcol(q), st, q, pending);  // mpk.cpp:58-59
+    }
   }
   SpmvArgs g;
   g.x = zcol(s - 1);
@@ -480,6 +498,10 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   const int mode = cfg.mode;
   if (mode == CS_MODE_REFERENCE && c->nranks > 1)
     fail(CS_ERR_INVALID_ARGUMENT, 0, "reference mode is single-GPU");
+  const int var = cfg.variant;
+  const bool explicit_w = mode == CS_MODE_FAST && (var & CS_VAR_EXPLICIT_W) != 0;
+  const bool fast_mpk = (var & CS_VAR_REF_MPK) == 0;
+  const bool tree_ref = mode == CS_MODE_REFERENCE && (var & CS_VAR_TREE) != 0;
   const int s = cfg.s;
   const int64_t n = p->n_local, ld = p->ld;
   const int64_t launches0 = c->launches, allred0 = c->allreduces;
@@ -519,14 +541,21 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   const int hist = cfg.max_outer + 2;
   const int q = s * s;
   const bool use_pack = mode == CS_MODE_FAST && pack_supported(s);
-  const size_t partial_n = std::max(use_pack ? pack_partial_doubles(s, n) : 0,
-                                    tree_gram_partial_doubles(n, s, s)) +
+  const size_t partial_n = std::max({use_pack ? pack_partial_doubles(s, n) : size_t{0},
+                                     tree_gram_partial_doubles(n, s, s),
+                                     explicit_w ? update_gram_partial_doubles(s) : size_t{0}}) +
                            spmv_dot_blocks(p->nslices) + 64;
   char* scr = static_cast<char*>(ctx_scratch(
       c, sizeof(double) * (3 * static_cast<size_t>(hist) + 4 * q + 8 * s + 64 + partial_n) +
              64 * 256));
   Arena ar{scr};
-  double* raw = ar.take<double>(2 * q + 2 * s + 1);
+  // packed block [G1 | G2 | c1 | c2 | rr | W_k raw (explicit W only) | breakdown
+  // column flags (multi-rank only)]
+  const int off_w = 2 * q + 2 * s + 1;
+  const int off_flags = off_w + (explicit_w ? q : 0);
+  const bool rank_flags = mode == CS_MODE_FAST && c->nranks > 1;
+  const int npack = off_flags + (rank_flags ? s : 0);
+  double* raw = ar.take<double>(npack);
   double* W = ar.take<double>(q);
   double* alpha_d = ar.take<double>(s);
   double* beta_d = ar.take<double>(q);
@@ -554,6 +583,10 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   sa.rel = rel;
   sa.da = da;
   sa.db = db;
+  sa.Wexp = explicit_w ? raw + off_w : nullptr;
+  sa.flags = rank_flags ? raw + off_flags : nullptr;
+  double* flags = rank_flags ? raw + off_flags : nullptr;
+  sa.fast_fgs = (var & CS_VAR_REF_FGS) ? 0 : 1;
   const SellView A = p->view();
   UpdateArgs ua;
   ua.s = s;
@@ -570,10 +603,15 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   }
   ua.alpha = alpha_d;
   ua.st = st;
+  const bool general_pc = p->precond_general();
+  if (general_pc) {  // the update pass writes z_0 = r into a scratch, the apply follows
+    ua.inv_diag = nullptr;
+    ua.inv_const = 0.0;
+  }
 
   auto gram = [&](const double* u, int ku, const double* v, int kv, double* out) {
     Launch L(c, CS_PHASE_REDUCE);
-    if (mode == CS_MODE_REFERENCE)
+    if (mode == CS_MODE_REFERENCE && !tree_ref)
       launch_serial_gram(n, ku, kv, u, ld, v, ld, out, st, c->stream);
     else
       launch_tree_gram(n, ku, kv, u, ld, v, ld, out, partial, ticket, st, c->stream);
@@ -582,15 +620,35 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   auto packed_reduce = [&](const double* Qm, const double* Zm) {
     if (use_pack) {
       Launch L(c, CS_PHASE_REDUCE);
-      launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, c->stream);
+      launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, flags, c->stream);
     } else {
       gram(Qm, s, bk.P, s, raw);
       gram(Zm, s, bk.P, s, raw + q);
       gram(Zm, s, bk.r, 1, raw + 2 * q);
       gram(Qm, s, bk.r, 1, raw + 2 * q + s);
       gram(bk.r, 1, bk.r, 1, raw + 2 * q + 2 * s);
+      if (flags) launch_pending_flags(s, st, flags, c->stream);
     }
-    allreduce_sum(c, raw, 2 * q + 2 * s + 1);
+    allreduce_sum(c, raw, npack);
+  };
+  // The update pass of outer k forms Q_k, AQ_k, x_k, r_k, z_0. With the explicit
+  // W it also reduces W_k = Q_k^T AQ_k from the rows it writes (fused, no extra
+  // HBM traffic; a separate tree Gram for orders the fused kernel lacks). The
+  // rank partial W_k travels in the packed block's single allreduce.
+  auto update_pass = [&](bool first) {
+    ua.beta = first ? nullptr : beta_d;
+    sa.Wexp = explicit_w && !first ? raw + off_w : nullptr;  // outer 1: W_1 is explicit already
+    {
+      Launch L(c, CS_PHASE_UPDATE);
+      if (!(sa.Wexp && launch_fast_update_gram(ua, partial, ticket + 4, raw + off_w, c->stream))) {
+        launch_fast_update(ua, c->stream);
+        if (sa.Wexp) gram(bk.Q, s, bk.AQ, s, raw + off_w);
+      }
+    }
+    if (general_pc) {  // z_0 = M^-1 r_k (the pass wrote r_k into the zp scratch)
+      Launch L(c, CS_PHASE_UPDATE);
+      precond_apply(p, bk.r, bk.Z, st, 0, /*pending=*/1);
+    }
   };
   auto small = [&](void (*fn)(const SmallArgs&, cudaStream_t)) {
     Launch L(c, CS_PHASE_SMALL);
@@ -617,9 +675,9 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   }
   {
     Launch L(c, CS_PHASE_UPDATE);
-    launch_precond_apply(n, A.inv_diag, bk.r, bk.Z, st, 0, 0, c->stream);
+    precond_apply(p, bk.r, bk.Z, st, 0, 0);  // mpk.cpp:50-52
   }
-  mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st, mode == CS_MODE_FAST);
+  mpk_steps(p, bk, s, lo, hi, /*pending=*/0, st, mode == CS_MODE_FAST && fast_mpk);
   std::swap(bk.Q, bk.Z);  // q = basis.z ; aq = basis.p.columns(1, s)
   std::swap(bk.AQ, bk.P);
   ua.q = bk.Q;
@@ -636,10 +694,10 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   // ---- outer iterations
   // multi-GPU fast algebra: halo planes move by NVLink peer stores from the
   // producing kernels (no NCCL on the SpMV path); collective, every rank calls it
-  const bool p2p = mode == CS_MODE_FAST && !hooks.any() && c->nranks > 1 && p2p_setup(p, bk.Z);
+  const bool p2p = mode == CS_MODE_FAST && fast_mpk && !general_pc && !hooks.any() &&
+                   c->nranks > 1 && p2p_setup(p, bk.Z);
   auto outer_fast = [&](bool first) {
-    ua.beta = first ? nullptr : beta_d;
-    ua.zw = bk.Z;  // z_0 = M^-1 r_k for the next MPK
+    ua.zw = general_pc ? bk.zpA : bk.Z;  // z_0 = M^-1 r_k for the next MPK
     if (p2p) {  // z_0's boundary rows go to the neighbours from the update pass itself
       SpmvArgs pa;
       fill_push_args(p, pa, 0);
@@ -648,12 +706,9 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
       ua.send_lo = pa.send_lo;
       ua.hi_begin = pa.hi_begin;
     }
-    {
-      Launch L(c, CS_PHASE_UPDATE);
-      launch_fast_update(ua, c->stream);
-    }
+    update_pass(first);
     if (p2p) p->p2p_pending = true;  // released by the first MPK step's interior launch
-    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true, p2p);
+    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk, p2p);
     packed_reduce(bk.Q, bk.Z);
     small(launch_fast_step);
   };
@@ -672,7 +727,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     }
     {
       Launch L(c, CS_PHASE_UPDATE);
-      launch_precond_apply(n, A.inv_diag, bk.r, bk.Z, st, 0, 0, c->stream);
+      precond_apply(p, bk.r, bk.Z, st, 0, 0);
     }
     mpk_steps(p, bk, s, lo, hi, 0, st);    // :173-176
     gram(bk.Q, s, bk.P, s, raw + q + s + 1);  // b2, :178-179
@@ -692,16 +747,12 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   if (hooks.any()) {  // per-outer host records: one outer at a time
     for (int k = 1; k <= cfg.max_outer; ++k) {
       if (mode == CS_MODE_FAST) {
-        ua.beta = k == 1 ? nullptr : beta_d;
-        ua.zw = bk.Z;
-        {
-          Launch L(c, CS_PHASE_UPDATE);
-          launch_fast_update(ua, c->stream);
-        }
+        ua.zw = general_pc ? bk.zpA : bk.Z;
+        update_pass(k == 1);
         if (read_state(c).done) break;
-        hooks.record_gram(W);  // W_k (the recurrence's W for this outer's alpha)
+        hooks.record_gram(W);  // W_k (the one this outer's alpha was solved with)
         hooks.record_x(bk.x);
-        mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, /*fast=*/true);
+        mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk);
         packed_reduce(bk.Q, bk.Z);
         small(launch_fast_step);
       } else {
@@ -798,8 +849,9 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
   double* qv = bk.AQ;
   double* zv = bk.Z;
   const int hist = max_iter + 2;
-  const size_t partial_n = static_cast<size_t>(std::max<int64_t>(spmv_dot_blocks(p->nslices),
-                                                                 (n + 255) / 256)) * 2 + 64;
+  const size_t partial_n =
+      std::max(static_cast<size_t>(std::max<int64_t>(spmv_dot_blocks(p->nslices), (n + 255) / 256)) * 2,
+               tree_gram_partial_doubles(n, 1, 1)) + 64;
   char* scr = static_cast<char*>(
       ctx_scratch(c, sizeof(double) * (static_cast<size_t>(hist) + partial_n + 64) + 16 * 256));
   Arena ar{scr};
@@ -838,10 +890,27 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
     Launch L(c, CS_PHASE_REDUCE);
     launch_serial_gram(n, 1, 1, u, ld, v, ld, out, st, c->stream);
   };
+  // general preconditioner (block Jacobi, device plugin): z = M^-1 r by its own
+  // apply, the dots by separate reductions, p = z + beta p from z
+  const bool gen = p->precond_general();
   auto vec = [&](int which, bool dots_on) {
     Launch L(c, CS_PHASE_UPDATE);
-    launch_axpby_pcg(which, n, xv, rv, pv, qv, inv, st, partial, ticket, dots, dots_on ? 0 : 1,
-                     c->stream);
+    launch_axpby_pcg(which, n, xv, gen && which == 2 ? zv : rv, pv, qv, gen ? nullptr : inv, st,
+                     partial, ticket, dots, dots_on ? 0 : 1, c->stream);
+  };
+  auto gen_dots = [&]() {  // rr, rz after z = M^-1 r
+    {
+      Launch L(c, CS_PHASE_UPDATE);
+      precond_apply(p, rv, zv, st, -1, 0);
+    }
+    if (serial) {
+      serial_dot(rv, rv, dots);
+      serial_dot(rv, zv, dots + 1);
+    } else {
+      Launch L(c, CS_PHASE_REDUCE);
+      launch_tree_gram(n, 1, 1, rv, ld, rv, ld, dots, partial, ticket + 2, st, c->stream);
+      launch_tree_gram(n, 1, 1, rv, ld, zv, ld, dots + 1, partial, ticket + 2, st, c->stream);
+    }
   };
   auto scalar = [&](int which) {
     Launch L(c, CS_PHASE_SMALL);
@@ -857,7 +926,9 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
     spmv_halo(p, kResid, g, xv);
   }
   if (hooks.any()) hooks.record_x(xv);
-  if (serial) {
+  if (gen) {
+    gen_dots();
+  } else if (serial) {
     serial_dot(rv, rv, dots);
     {
       Launch L(c, CS_PHASE_UPDATE);
@@ -869,7 +940,10 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
   }
   allreduce_sum(c, dots, 2);
   scalar(0);
-  vec(0, false);  // p = z
+  if (gen)  // p = z
+    CS_CUDA(cudaMemcpyAsync(pv, zv, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    vec(0, false);  // p = z
   auto iteration = [&]() {
     SpmvArgs g;
     g.x = pv;
@@ -886,7 +960,10 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
     }
     allreduce_sum(c, dots, 1);
     scalar(1);
-    if (serial) {
+    if (gen) {
+      vec(1, false);
+      gen_dots();
+    } else if (serial) {
       vec(1, false);
       serial_dot(rv, rv, dots);
       {

@@ -53,7 +53,7 @@ constexpr int kWarps = 8;  // warps per 256-thread block
 #endif
 
 __device__ __forceinline__ void report(const SpmvArgs& g, int col) {
-  if (g.st == nullptr) return;
+  if (g.st == nullptr || col < 0) return;  // col < 0: checked after a separate apply
   unsigned long long* w = g.pending ? &g.st->pending : &g.st->err;
   atomicCAS(w, 0ull, make_err(4 /*CS_ERR_BASIS_BREAKDOWN*/, col));
   if (!g.pending) g.st->done = 1;
@@ -930,13 +930,8 @@ bool use_tma(const SellView& a) {
 template <int KIND, bool JAC>
 void tma_launch(const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se, cudaStream_t st) {
   const uint32_t stage = static_cast<uint32_t>(kWarps) * a.max_width * kSliceRows * sizeof(double);
-  static int configured = 0;  // this instantiation: largest dynamic smem enabled so far
-  if (static_cast<int>(2 * stage) > configured) {
-    CS_CUDA(cudaFuncSetAttribute(sell_tma_kernel<KIND, JAC>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(2 * stage)));
-    configured = static_cast<int>(2 * stage);
-  }
+  kernel_setup(reinterpret_cast<const void*>(sell_tma_kernel<KIND, JAC>), kWarps * 32,
+               static_cast<int>(2 * stage));
   sell_tma_kernel<KIND, JAC><<<tma_grid(se - sb), kWarps * 32, 2 * stage, st>>>(a, g, sb, se, stage);
 }
 
@@ -980,22 +975,12 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
       if (!std::isfinite(t.v[e])) return false;
     bool neg1 = true;  // every off-centre value is -1.0 (the 27-point Poisson operators)
     for (int e = 0; e < 27; ++e) neg1 = neg1 && (e == 13 || t.v[e] == -1.0);
-    static int configured[4] = {0, 0, 0, 0};
-    const int ki = (jac ? 1 : 0) + (neg1 ? 2 : 0);
     auto kern = jac ? (neg1 ? sell_box_kernel<KIND, true, true> : sell_box_kernel<KIND, true, false>)
                     : (neg1 ? sell_box_kernel<KIND, false, true> : sell_box_kernel<KIND, false, false>);
-    if (smem > configured[ki]) {
-      CS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      configured[ki] = smem;
-    }
-    static int per_sm[4] = {0, 0, 0, 0}, per_sm_smem[4] = {0, 0, 0, 0};  // occupancy API
-    if (per_sm_smem[ki] != smem) {
-      CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ki], kern, CS_BOX_THREADS, smem));
-      per_sm_smem[ki] = smem;
-    }
+    const int per_sm = kernel_setup(reinterpret_cast<const void*>(kern), CS_BOX_THREADS, smem);
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(
-        std::max<int64_t>(1, std::min<int64_t>(items, 148 * std::max(per_sm[ki], 1))));
+        std::max<int64_t>(1, std::min<int64_t>(items, 148 * per_sm)));
     kern<<<grid, CS_BOX_THREADS, smem, st>>>(a, g, b, t);
     return true;
   }

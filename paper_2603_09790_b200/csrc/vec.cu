@@ -14,6 +14,7 @@
 //  * "fast" reductions use fixed-shape trees (warp shuffles, fixed block
 //    count, last-block finalisation in block order): deterministic run to run,
 //    but not the serial order.
+#include <climits>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -42,6 +43,71 @@ __global__ void precond_kernel(int64_t n, const double* __restrict__ inv_diag,
   const double z = inv_diag ? __dmul_rn(inv_diag[i], in[i]) : in[i];
   out[i] = z;
   if (col >= 0 && !isfinite(z) && st != nullptr) {
+    atomicCAS(pending ? &st->pending : &st->err, 0ull, make_err(4, col));
+    if (!pending) st->done = 1;
+  }
+}
+
+// ------------------------------------------------------------------ block Jacobi
+// One thread per diagonal block. Factor: left-looking Cholesky with the
+// operation order of small_cholesky_solve (dense_ops.cpp:55-88), in place on the
+// bs x bs column-major block (lower triangle = L). Apply: forward then back
+// substitution, ascending/descending like its solve loops, separate roundings.
+__global__ void bj_factor_kernel(int64_t nblocks, int bs, double* f, int* bad_block) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  double* L = f + b * bs * bs;
+  for (int j = 0; j < bs; ++j) {
+    double d = L[j + j * bs];
+    for (int q = 0; q < j; ++q) d = __dsub_rn(d, __dmul_rn(L[j + q * bs], L[j + q * bs]));
+    if (!(d > 0.0) || !isfinite(d)) {
+      atomicMin(bad_block, static_cast<int>(b < INT_MAX ? b : INT_MAX - 1));
+      return;
+    }
+    const double dg = __dsqrt_rn(d);
+    L[j + j * bs] = dg;
+    for (int i = j + 1; i < bs; ++i) {
+      double v = L[i + j * bs];
+      for (int q = 0; q < j; ++q) v = __dsub_rn(v, __dmul_rn(L[i + q * bs], L[j + q * bs]));
+      L[i + j * bs] = __ddiv_rn(v, dg);
+    }
+    for (int i = 0; i < j; ++i) L[i + j * bs] = 0.0;  // upper triangle unused
+  }
+}
+
+template <int BS>
+__global__ void bj_apply_kernel(int64_t n, const double* __restrict__ f, const double* __restrict__ in,
+                                double* out, DevState* st, int col, int pending) {
+  if (halted(st)) return;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r0 = b * BS;
+  if (r0 >= n) return;
+  const double* L = f + b * BS * BS;
+  double x[BS];
+#pragma unroll
+  for (int i = 0; i < BS; ++i) x[i] = r0 + i < n ? in[r0 + i] : 0.0;
+#pragma unroll
+  for (int i = 0; i < BS; ++i) {
+    double v = x[i];
+#pragma unroll
+    for (int q = 0; q < i; ++q) v = __dsub_rn(v, __dmul_rn(__ldg(L + i + q * BS), x[q]));
+    x[i] = __ddiv_rn(v, __ldg(L + i + i * BS));
+  }
+#pragma unroll
+  for (int i = BS - 1; i >= 0; --i) {
+    double v = x[i];
+#pragma unroll
+    for (int q = i + 1; q < BS; ++q) v = __dsub_rn(v, __dmul_rn(__ldg(L + q + i * BS), x[q]));
+    x[i] = __ddiv_rn(v, __ldg(L + i + i * BS));
+  }
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < BS; ++i)
+    if (r0 + i < n) {
+      out[r0 + i] = x[i];
+      fin = fin && isfinite(x[i]);
+    }
+  if (col >= 0 && !fin && st != nullptr) {
     atomicCAS(pending ? &st->pending : &st->err, 0ull, make_err(4, col));
     if (!pending) st->done = 1;
   }
@@ -158,6 +224,20 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// ------------------------------------------------------------------ rank-global breakdown flags
+// flags[j] = 1.0 when this rank's speculative MPK saw a non-finite value first
+// in basis column j, else 0.0; summed by the packed block's allreduce, so every
+// rank raises the same BasisBreakdownError (the lowest column of any rank).
+__device__ __forceinline__ void write_pending_flags(int s, const DevState* st, double* flags) {
+  const unsigned long long pw = *(volatile const unsigned long long*)&st->pending;
+  const int col = pw ? static_cast<int>(pw & 0xffffffffull) : -1;
+  for (int j = threadIdx.x; j < s; j += blockDim.x) flags[j] = j == col ? 1.0 : 0.0;
+}
+
+__global__ void pending_flags_kernel(int s, const DevState* st, double* flags) {
+  write_pending_flags(s, st, flags);
+}
+
 // ------------------------------------------------------------------ packed DMMA reduction
 //
 // One pass over Q, Z, P (= A Z columns 1..s) and r produces the whole
@@ -196,7 +276,7 @@ template <int S>
 __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     pack_kernel(int64_t n, int64_t ld, const double* __restrict__ Q, const double* __restrict__ Z,
                 const double* __restrict__ P, const double* __restrict__ r, double* packed,
-                double* partial, unsigned* ticket, DevState* st) {
+                double* partial, unsigned* ticket, DevState* st, double* flags) {
   using Sh = PackShape<S>;
   if (halted(st)) return;
   extern __shared__ double smem[];
@@ -300,6 +380,7 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
   if (!last) return;
   __threadfence();
   finalize_partials(partial, gridDim.x, Sh::NOUT, packed);
+  if (flags) write_pending_flags(S, st, flags);
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
@@ -313,24 +394,16 @@ int pack_grid(int64_t n) {
 template <int S>
 void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
-                 cudaStream_t strm) {
+                 double* flags, cudaStream_t strm) {
   using Sh = PackShape<S>;
-  static bool configured = false;
-  if (!configured) {
-    CS_CUDA(cudaFuncSetAttribute(pack_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(Sh::smem_bytes)));
-    configured = true;
-  }
   // one wave of resident blocks (a grid past the resident count leaves a
   // half-occupied second wave: 444 blocks at 2 per SM measured 0.64 ms at 256^3)
-  static int per_sm = 0;
-  if (per_sm == 0)
-    CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_kernel<S>, kPackWarps * 32,
-                                                          Sh::smem_bytes));
+  const int per_sm = kernel_setup(reinterpret_cast<const void*>(pack_kernel<S>), kPackWarps * 32,
+                                  static_cast<int>(Sh::smem_bytes));
   const int64_t want = pack_grid(n);
-  const int grid = static_cast<int>(std::min<int64_t>(want, 148 * std::max(per_sm, 1)));
+  const int grid = static_cast<int>(std::min<int64_t>(want, 148 * per_sm));
   pack_kernel<S><<<grid, kPackWarps * 32, Sh::smem_bytes, strm>>>(n, ld, q, z, p, r, packed,
-                                                                  partial, ticket, st);
+                                                                  partial, ticket, st, flags);
   CS_CUDA(cudaGetLastError());
 }
 
@@ -423,6 +496,140 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
       if (!isfinite(z)) atomicCAS(&a.st->pending, 0ull, make_err(4, 0));
     }
   }
+}
+
+// update_kernel<S, true, true, true> fused with the explicit Gram of the new
+// basis: a persistent grid walks 128-row tiles; each tile's new Q and AQ rows
+// are also staged in shared memory ([column][row], stride 132 doubles: the
+// DMMA fragment loads are conflict-free) and every warp folds 16 of its rows
+// into its (Q^T AQ) accumulator tiles with FP64 mma.sync m8n8k4 (the pack
+// kernel's fragment layout). No extra HBM traffic: the Gram reads only what
+// the pass already holds. Per-warp tiles are summed in a fixed order into one
+// partial per block; the last block reduces the partials in block order.
+constexpr int kGramStride = 132;
+
+template <int S>
+__global__ void __launch_bounds__(kThreads)
+    update_gram_kernel(UpdateArgs a, Cols<S> c, double* partial, unsigned* ticket, double* wout) {
+  if (halted(a.st)) return;
+  constexpr int MT = (S + 7) / 8;
+  constexpr int SP = MT * 8;
+  __shared__ double sh_alpha[S];
+  __shared__ double sh_beta[S * S];
+  __shared__ double tile[2][SP][kGramStride];
+  __shared__ bool last;
+  for (int t = threadIdx.x; t < S; t += blockDim.x) sh_alpha[t] = a.alpha[t];
+  for (int t = threadIdx.x; t < S * S; t += blockDim.x) sh_beta[t] = a.beta[t];
+  for (int t = threadIdx.x; t < 2 * (SP - S) * kGramStride; t += blockDim.x) {
+    const int h = t / ((SP - S) * kGramStride), rem = t % ((SP - S) * kGramStride);
+    tile[h][S + rem / kGramStride][rem % kGramStride] = 0.0;  // padded columns stay zero
+  }
+  __syncthreads();
+  const bool aq_role = threadIdx.x >= kUpdRows;
+  const int rl = threadIdx.x & (kUpdRows - 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  double* const* dst = aq_role ? c.aq : c.q;
+  const double* const* src = aq_role ? c.p : c.z;
+  const double sign = aq_role ? -1.0 : 1.0;
+  double acc[MT][MT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int q = 0; q < MT; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kUpdRows;
+  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kUpdRows; t0 < a.n; t0 += stride) {
+    const int64_t i = t0 + rl;
+    const bool active = i < a.n;
+    double lo[S], hi[S];
+    double xr = 0.0;
+    if (active) {
+      xr = aq_role ? a.r[i] : a.x[i];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        lo[q] = dst[q][i];
+        hi[q] = src[q][i];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < S; ++q) lo[q] = hi[q] = 0.0;
+    }
+    // the AQ role overwrites Z column 0 (z_0) that the Q role of the same rows
+    // reads above; the previous tile's fragment loads also end here
+    __syncthreads();
+    // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39)
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const double xq = lo[q];
+#pragma unroll
+      for (int j = 0; j < S; ++j) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * S], xq));
+    }
+#pragma unroll
+    for (int j = 0; j < S; ++j) tile[aq_role][j][rl] = active ? hi[j] : 0.0;
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) dst[j][i] = hi[j];
+      // solver.cpp:159-162: x += alpha_j q_j ; r += (-alpha_j) aq_j, ascending j
+#pragma unroll
+      for (int j = 0; j < S; ++j) xr = __dadd_rn(xr, __dmul_rn(sign * sh_alpha[j], hi[j]));
+      if (aq_role) {
+        a.r[i] = xr;
+        const double z = !a.inv_diag        ? xr
+                         : a.inv_const != 0.0 ? __dmul_rn(a.inv_const, xr)
+                                              : __dmul_rn(a.inv_diag[i], xr);
+        a.zw[i] = z;
+        if (a.push_lo != nullptr && i < a.send_lo) a.push_lo[i] = z;
+        if (a.push_hi != nullptr && i >= a.hi_begin) a.push_hi[i - a.hi_begin] = z;
+        if (!isfinite(z)) atomicCAS(&a.st->pending, 0ull, make_err(4, 0));
+      } else {
+        a.x[i] = xr;
+      }
+    }
+    __syncthreads();
+    // warp w: rows [16w, 16w + 16) of the tile, 4 k-steps of 4 rows
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k0 = warp * 16 + kk * 4 + t4;
+      double fa[MT], fb[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        fa[m] = tile[0][m * 8 + g][k0];
+        fb[m] = tile[1][m * 8 + g][k0];
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int q = 0; q < MT; ++q) dmma(acc[m][q], fa[m], fb[q]);
+    }
+  }
+  __syncthreads();  // tiles are dead: reuse as [warp][S*S]
+  double* out = &tile[0][0][0];
+  static_assert(2 * SP * kGramStride >= (kThreads / 32) * S * S, "reduction scratch");
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int q = 0; q < MT; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ii = m * 8 + g, jj = q * 8 + 2 * t4 + e;
+        if (ii < S && jj < S) out[warp * S * S + ii + jj * S] = acc[m][q][e];
+      }
+  __syncthreads();
+  for (int e = threadIdx.x; e < S * S; e += blockDim.x) {
+    double sum = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) sum += out[w * S * S + e];
+    partial[static_cast<int64_t>(blockIdx.x) * S * S + e] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_partials(partial, gridDim.x, S * S, wout);
+  if (threadIdx.x == 0) *ticket = 0u;
 }
 
 template <int S>
@@ -568,6 +775,30 @@ void launch_precond_apply(int64_t n, const double* inv_diag, const double* in, d
   CS_CUDA(cudaGetLastError());
 }
 
+void launch_bj_factor(int64_t nblocks, int bs, double* f, int* bad_block, cudaStream_t s) {
+  if (nblocks == 0) return;
+  bj_factor_kernel<<<grid_for(nblocks, 128), 128, 0, s>>>(nblocks, bs, f, bad_block);
+  CS_CUDA(cudaGetLastError());
+}
+
+void launch_bj_apply(int64_t n, int bs, const double* f, const double* in, double* out,
+                     DevState* st, int col, int pending, cudaStream_t s) {
+  if (n == 0) return;
+  const int64_t nb = (n + bs - 1) / bs;
+  const unsigned grid = grid_for(nb, 128);
+#define CSG_BJ(B)                                                                               \
+  case B:                                                                                      \
+    bj_apply_kernel<B><<<grid, 128, 0, s>>>(n, f, in, out, st, col, pending);                  \
+    break
+  switch (bs) {
+    CSG_BJ(1); CSG_BJ(2); CSG_BJ(3); CSG_BJ(4); CSG_BJ(5); CSG_BJ(6); CSG_BJ(7); CSG_BJ(8);
+    CSG_BJ(9); CSG_BJ(10); CSG_BJ(11); CSG_BJ(12); CSG_BJ(13); CSG_BJ(14); CSG_BJ(15); CSG_BJ(16);
+    default: throw LibError{8, 0, "block_jacobi: bs must be in [1, 16]"};
+  }
+#undef CSG_BJ
+  CS_CUDA(cudaGetLastError());
+}
+
 void launch_random_vector(int64_t n, int64_t offset, uint64_t seed, double* out, cudaStream_t s) {
   if (n == 0) return;
   random_kernel<<<grid_for(n), kThreads, 0, s>>>(n, offset, seed, out);
@@ -609,8 +840,8 @@ size_t pack_partial_doubles(int s, int64_t n) {
 
 void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
-                 cudaStream_t strm) {
-#define CSG_PACK(SV) pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, strm)
+                 double* flags, cudaStream_t strm) {
+#define CSG_PACK(SV) pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, flags, strm)
   switch (s) {
     case 1: CSG_PACK(1); break;
     case 2: CSG_PACK(2); break;
@@ -625,6 +856,56 @@ void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z,
     default: throw LibError{9, 0, "pack: unsupported s"};
   }
 #undef CSG_PACK
+}
+
+bool update_gram_supported(int s) {
+  switch (s) {
+    case 1: case 2: case 3: case 4: case 5: case 6: case 8: case 10: case 12: case 16:
+      return true;
+    default:
+      return false;
+  }
+}
+
+constexpr int kUpdGramMaxBlocks = 148 * 8;
+
+size_t update_gram_partial_doubles(int s) {
+  return static_cast<size_t>(kUpdGramMaxBlocks) * s * s;
+}
+
+template <int S>
+void update_gram_launch(const UpdateArgs& a, double* partial, unsigned* ticket, double* wout,
+                        cudaStream_t st) {
+  const int per_sm =
+      kernel_setup(reinterpret_cast<const void*>(update_gram_kernel<S>), kThreads, 0);
+  const int64_t tiles = (a.n + kUpdRows - 1) / kUpdRows;
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>({tiles, 148 * static_cast<int64_t>(per_sm), kUpdGramMaxBlocks})));
+  update_gram_kernel<S><<<grid, kThreads, 0, st>>>(a, make_cols<S>(a), partial, ticket, wout);
+  CS_CUDA(cudaGetLastError());
+}
+
+bool launch_fast_update_gram(const UpdateArgs& a, double* partial, unsigned* ticket, double* wout,
+                             cudaStream_t st) {
+  if (a.beta == nullptr) return false;
+  switch (a.s) {
+    case 1: update_gram_launch<1>(a, partial, ticket, wout, st); return true;
+    case 2: update_gram_launch<2>(a, partial, ticket, wout, st); return true;
+    case 3: update_gram_launch<3>(a, partial, ticket, wout, st); return true;
+    case 4: update_gram_launch<4>(a, partial, ticket, wout, st); return true;
+    case 5: update_gram_launch<5>(a, partial, ticket, wout, st); return true;
+    case 6: update_gram_launch<6>(a, partial, ticket, wout, st); return true;
+    case 8: update_gram_launch<8>(a, partial, ticket, wout, st); return true;
+    case 10: update_gram_launch<10>(a, partial, ticket, wout, st); return true;
+    case 12: update_gram_launch<12>(a, partial, ticket, wout, st); return true;
+    case 16: update_gram_launch<16>(a, partial, ticket, wout, st); return true;
+    default: return false;
+  }
+}
+
+void launch_pending_flags(int s, const DevState* st, double* flags, cudaStream_t strm) {
+  pending_flags_kernel<<<1, 64, 0, strm>>>(s, st, flags);
+  CS_CUDA(cudaGetLastError());
 }
 
 void launch_fast_update(const UpdateArgs& a, cudaStream_t s) {

@@ -117,6 +117,10 @@ int ref_sym_eigvals(int s, const double* w, double* out);
 OC_DECLARE(ref_)
 OC_DECLARE(orc_)
 
+/* reference monitor_inexact (solver.cpp:275-282) over (outer_iters, delta_alpha) */
+int ref_monitor_inexact(int outer_iters, int n_da, const double* delta_alpha, double delta_cap,
+                        double* max_delta, double* budget, int* pass);
+
 /* restatement-only generators for problems the reference does not ship
  * (SURVEY a22): 7-point stencil with coefficients (cx, cy, cz); poisson7 is
  * (1,1,1) and the anisotropic config-4 operator is (1,1,100). */

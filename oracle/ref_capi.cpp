@@ -497,6 +497,20 @@ int ref_sym_eigvals(int s, const double* w, double* out) {
   });
 }
 
+// solver.cpp:275-282 over a report carrying only what the verdict reads
+int ref_monitor_inexact(int outer_iters, int n_da, const double* delta_alpha, double delta_cap,
+                        double* max_delta, double* budget, int* pass) {
+  return guarded([&] {
+    cs::SolveReport r;
+    r.outer_iters = outer_iters;
+    r.delta_alpha.assign(delta_alpha, delta_alpha + n_da);
+    const cs::InexactVerdict v = cs::monitor_inexact(r, delta_cap);
+    *max_delta = v.max_delta;
+    *budget = v.budget;
+    *pass = v.pass ? 1 : 0;
+  });
+}
+
 const char* ref_last_error(int* payload) {
   if (payload) *payload = g_payload;
   return g_msg.c_str();

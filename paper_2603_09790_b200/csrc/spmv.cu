@@ -268,8 +268,9 @@ __device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double
 }
 
 // kDot: fixed-shape block tree, then last-block finalisation in block order
+template <int NW = kWarps>
 __device__ __forceinline__ void dot_finish(const SpmvArgs& g, double dotv) {
-  __shared__ double red[kWarps];
+  __shared__ double red[NW];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -278,7 +279,7 @@ __device__ __forceinline__ void dot_finish(const SpmvArgs& g, double dotv) {
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < kWarps; ++w) s += red[w];
+    for (int w = 0; w < NW; ++w) s += red[w];
     g.partial[blockIdx.x] = s;
     __threadfence();
     const unsigned t = atomicAdd(g.ticket, 1u);
@@ -903,6 +904,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     }
     __syncthreads();  // every thread is done with slot sl before it is refilled
   }
+  if constexpr (KIND == kDot) dot_finish<CS_BOX_THREADS / 32>(g, dotv);
 }
 
 #ifndef CS_SPMV_TMA
@@ -943,7 +945,7 @@ bool box_enabled() {
 
 constexpr bool box_kind(int kind) {
   return kind == kPlain || kind == kResid || kind == kMpkFirstF || kind == kMpkMidF ||
-         kind == kMpkLast;
+         kind == kMpkLast || kind == kDot;
 }
 
 // Plane-streaming launch over the class rows [lo, hi) * 32; false: not applicable.
@@ -1087,7 +1089,7 @@ void launch_halo_release(const SpmvArgs& g, DevState* st, cudaStream_t s) {
 
 int spmv_dot_blocks(int64_t nslices) {
   const int a = spmv_grid(nslices), b = tma_grid(nslices);
-  return a > b ? a : b;
+  return std::max({a, b, 148 * 4});  // the box kernel: <= 148 x resident blocks
 }
 
 void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t sb, int64_t se,

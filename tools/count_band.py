@@ -44,6 +44,8 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_count_band.json"))
     ap.add_argument("--skip-ref", action="store_true", help="no serial reference-algebra runs")
     ap.add_argument("--variants", default="")
+    ap.add_argument("--tree-band", action="store_true",
+                    help="reference band with tree reductions (fast) instead of serial chains")
     a = ap.parse_args()
     import paper_2603_09790_b200 as cs
     from paper_2603_09790_b200 import _lib as L
@@ -97,7 +99,11 @@ def main():
             runs.append(d)
             print(json.dumps(d), flush=True)
 
-        if not a.skip_ref:
+        if a.tree_band:  # reference algebra, tree reductions, lambda perturbed
+            for eps in (0.0, 1e-13, -1e-13, 1e-12, -1e-12, 1e-11, -1e-11):
+                add(f"reference-tree lambda*(1{'-' if eps >= 0 else '+'}{abs(eps):g})", "reference",
+                    L.CS_VAR_TREE, eps)
+        elif not a.skip_ref:
             add("reference", "reference")
             for eps in (1e-13, -1e-13, 1e-12, -1e-12):
                 add(f"reference lambda*(1{'-' if eps > 0 else '+'}{abs(eps):g})", "reference", 0, eps)

@@ -1,0 +1,56 @@
+#!/bin/bash
+# One gpurun session: tag + list of steps, each step's output under gpurun_out/<tag>_<step>.*
+#   gpurun -- bash tools/gpu_session.sh <tag> <step> [<step> ...]
+# steps: info | tests | tests_fast | precond | band256 | band512 | bench | bench256 | ncu_list |
+#        ncu_box | sanitize | smoke | multi2 | bench2 | bench4
+set -u
+tag=$1; shift
+out=gpurun_out
+mkdir -p $out
+cd "${GRAFT_REPO_ROOT:-.}"
+for step in "$@"; do
+  echo "== $step $(date +%T)" >> $out/${tag}_status.txt
+  case $step in
+    info)
+      { free -g; nproc; lscpu | head -20; nvidia-smi -L; nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,memory.total --format=csv; } > $out/${tag}_info.txt 2>&1 ;;
+    tests)
+      timeout 1800 python -m pytest tests -m gpu -x -q > $out/${tag}_tests.log 2>&1 ;;
+    tests_fast)
+      timeout 1500 python -m pytest tests -m "gpu and not slow" -q > $out/${tag}_tests.log 2>&1 ;;
+    precond)
+      timeout 600 python -m pytest tests/test_gpu_precond.py -q > $out/${tag}_precond.log 2>&1 ;;
+    band256)
+      timeout 1200 python tools/count_band.py --tree-band --cases p27:256:8 --out $out/${tag}_band.json > $out/${tag}_band.log 2>&1 ;;
+    band512)
+      timeout 1800 python tools/count_band.py --tree-band --cases p27:512:8 --out $out/${tag}_band512.json > $out/${tag}_band512.log 2>&1 ;;
+    bench)
+      timeout 1500 python bench.py > $out/${tag}_bench.jsonl 2> $out/${tag}_bench.err ;;
+    bench256)
+      timeout 900 python bench.py --grid 256 > $out/${tag}_bench256.jsonl 2> $out/${tag}_bench256.err ;;
+    ncu_list)
+      timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file $out/${tag}_launches.csv python bench.py --grid 256 --steps 1 --warmup 0 \
+        --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_list.log 2>&1 ;;
+    ncu_box)
+      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sell_box_kernel \
+        -s 20 -c 1 -o $out/${tag}_box python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e \
+        --no-cpu --no-pcg > $out/${tag}_ncu_box.log 2>&1 ;;
+    sanitize)
+      for tool in memcheck synccheck racecheck; do
+        timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_case.py \
+          $([ $tool = racecheck ] && echo --quick) > $out/${tag}_sanitize_$tool.log 2>&1
+      done ;;
+    smoke)
+      timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $out/${tag}_smoke.log 2>&1 ;;
+    multi2)
+      timeout 1200 python -m pytest tests/test_gpu_multi.py -q > $out/${tag}_multi.log 2>&1 ;;
+    bench2)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29611 bench.py --gpus 2 > $out/${tag}_bench2.jsonl 2> $out/${tag}_bench2.err ;;
+    bench4)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+        --master-port 29613 bench.py --gpus 4 > $out/${tag}_bench4.jsonl 2> $out/${tag}_bench4.err ;;
+    *) echo "unknown step $step" >> $out/${tag}_status.txt ;;
+  esac
+  echo "   rc=$? $(date +%T)" >> $out/${tag}_status.txt
+done

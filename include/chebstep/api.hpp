@@ -4,8 +4,14 @@
 // Source- and link-compatible subset of the reference public headers
 // (/root/reference/proj/include/chebstep/*.hpp): same namespace, type names,
 // member order and function signatures for everything on the solve path, so
-// the reference's own callers (e.g. cli.cpp:190,242,252,269) link against this
-// library unchanged. The per-module headers next to this file (csr.hpp,
+// solve-path callers compile and link against this library unchanged. Callers
+// that also use the reference's analysis modules do not: e.g. the reference
+// cli.cpp includes moments.hpp / perf_model.hpp (cli.cpp:13-14), and
+// dense_ops.hpp:24-53 (block_combine, ldlt_pivots, InnerProduct,
+// mgs_orthogonalize_first), gram.hpp:55-78 (fgs_residual_oracle,
+// ruhe_equivalence_check, gram_kappa_check) and the dense paths of
+// spectral.hpp:35-53 are not declared here (out of scope). The repo's
+// own CLI (csrc/cli.cpp) covers solve / compare / gram-analysis. The per-module headers next to this file (csr.hpp,
 // solver.hpp, ...) all forward here. Compute entries go through the C ABI in
 // chebstep_gpu.h (CUDA kernels for sm_100a, no CPU fallback); the analysis-only
 // modules of the reference (moments, perf_model, cli, dense LAPACK paths,

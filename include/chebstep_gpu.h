@@ -117,6 +117,8 @@ typedef struct {
 #define CS_VAR_REF_FGS 4      /* fast: the reference's FGS operation sequence */
 #define CS_VAR_REF_MPK 8      /* fast: the reference's MPK epilogue (zp streams, no FMA); 1 GPU */
 #define CS_VAR_TREE 16        /* reference: fixed-shape tree reductions instead of serial chains */
+#define CS_VAR_P_FROM_Z 32    /* fast: P columns derived from Z (no P stream) */
+#define CS_VAR_P_STORED 64    /* fast: force the stored-P schedule */
 
 typedef struct {
   /* SolveReport (solver.hpp:39-68), reference semantics */

@@ -152,13 +152,42 @@ void launch_tree_gram(int64_t n, int ku, int kv, const double* u, int64_t ldu, c
                       int64_t ldv, double* g, double* partial, unsigned* ticket, DevState* st,
                       cudaStream_t s);
 size_t tree_gram_partial_doubles(int64_t n, int ku, int kv);
+// Fast algebra with P derived from Z ("PZ" schedule, diagonal preconditioners):
+// the fast MPK epilogue z_q = ca D^-1 p_q + cb z_{q-1} + cc z_{q-2} is inverted
+// instead of storing p_q = A z_{q-1}: column j of P (p_{j+1}) is
+//   j = 0: (z_1 + sigma z_0) * k1 ;  j >= 1: ((z_{j+1} + 2 sigma z_j) + z_{j-1}) * k2
+// (times diag[i] for a non-uniform Jacobi diagonal), k1 = d/alpha, k2 = d/(2 alpha).
+// The MPK's last step writes the virtual z_s (instead of p_s) to `zs`. Saves the
+// s P columns' write in the MPK and their reads in the pack and update passes.
+struct PzArgs {
+  const double* zs = nullptr;    // z_s; nullptr: P is streamed (non-PZ)
+  double sig1 = 0.0, sig2 = 0.0;  // sigma, 2 sigma
+  double k1 = 0.0, k2 = 0.0;
+  const double* diag = nullptr;   // non-uniform Jacobi: the diagonal a_ii (else nullptr)
+};
+#ifdef __CUDACC__
+// zz[0..S] = z_0 .. z_S of one row; p[j] = column j of P; the same arithmetic
+// wherever P is derived (pack, update), so both see the same bits
+template <int S>
+__device__ __forceinline__ void p_from_z(const double (&zz)[S + 1], const PzArgs& a, double di,
+                                         double (&p)[S]) {
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    double t;
+    if (j == 0) t = fma(a.sig1, zz[0], zz[1]) * a.k1;
+    else t = (fma(a.sig2, zz[j], zz[j + 1]) + zz[j - 1]) * a.k2;
+    p[j] = a.diag ? t * di : t;
+  }
+}
+#endif
 // fast packed reduction {Q^T P, Z^T P, Z^T r, Q^T r, r^T r} (2s^2+2s+1 doubles)
 bool pack_supported(int s);
 // flags (multi-rank, or nullptr): s rank-local basis-breakdown column flags
-// written by the last block (see launch_pending_flags)
+// written by the last block (see launch_pending_flags). pz.zs != nullptr: P is
+// derived from Z (p unused).
 void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket,
-                 DevState* st, double* flags, cudaStream_t strm);
+                 DevState* st, double* flags, cudaStream_t strm, const PzArgs& pz = PzArgs{});
 // flags[j] = 1.0 iff this rank's pending basis breakdown is in column j
 void launch_pending_flags(int s, const DevState* st, double* flags, cudaStream_t strm);
 size_t pack_partial_doubles(int s, int64_t n);
@@ -184,6 +213,7 @@ struct UpdateArgs {
   double* push_lo = nullptr;
   double* push_hi = nullptr;
   int64_t send_lo = 0, hi_begin = 0;
+  PzArgs pz;  // pz.zs != nullptr: P derived from Z (p unused)
 };
 void launch_fast_update(const UpdateArgs& a, cudaStream_t s);  // beta block update + x/r + z0
 // The same beta pass fused with the explicit Gram W = Q_new^T AQ_new of the

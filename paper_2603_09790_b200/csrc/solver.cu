@@ -297,8 +297,10 @@ Blocks workspace(cs_problem* p, int s) {
 }
 
 // MPK steps 1..s on a basis whose z_0 is already in Z column 0 (mpk.cpp:53-69).
+// zs != nullptr (fast, diagonal M): PZ schedule -- no P column is written; the
+// last step writes the virtual z_s instead of p_s (see PzArgs).
 void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int pending,
-               DevState* st, bool fast = false, bool p2p = false) {
+               DevState* st, bool fast = false, bool p2p = false, double* zs = nullptr) {
   const int64_t ld = p->ld;
   const double alpha = 2.0 / (hi - lo);           // mpk.hpp:22
   const double sigma = (hi + lo) / (hi - lo);     // mpk.hpp:23-25
@@ -314,14 +316,15 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     if (!jac && !gen) return zcol(q);
     return (q & 1) ? bk.zpA : bk.zpB;
   };
-  for (int q = 1; q < s; ++q) {
+  const bool pz = zs != nullptr && fast && !gen;
+  for (int q = 1; q < (pz ? s + 1 : s); ++q) {
     SpmvArgs g;
     g.x = zcol(q - 1);
-    g.y = bk.P + (q - 1) * ld;
+    g.y = pz ? nullptr : bk.P + (q - 1) * ld;
     g.zp1 = zp(q - 1);
     g.zp2 = q >= 2 ? (fast ? zcol(q - 2) : zp(q - 2)) : nullptr;
     g.zpout = jac && !fast ? zp(q) : nullptr;
-    g.zout = gen ? zp(q) : zcol(q);
+    g.zout = gen ? zp(q) : (pz && q == s) ? zs : zcol(q);
     if (q == 1) {
       g.ca = alpha;
       g.cb = -sigma;
@@ -336,13 +339,16 @@ void mpk_steps(cs_problem* p, const Blocks& bk, int s, double lo, double hi, int
     g.st = st;
     const int kind = fast ? (q == 1 ? kMpkFirstF : kMpkMidF) : (q == 1 ? kMpkFirst : kMpkMid);
     if (gen) g.col = -1;  // the breakdown check follows the apply
-    if (p2p) spmv_p2p(p, kind, g, q);  // z_q's boundary rows go straight to the neighbours
+    if (pz && q == s) g.col = s - 1;  // z_s stands for p_s (mpk.cpp:69 checks p_s)
+    // z_q's boundary rows go straight to the neighbours (z_s feeds no SpMV)
+    if (p2p) spmv_p2p(p, kind, g, pz && q == s ? -1 : q);
     else spmv_halo(p, kind, g, zcol(q - 1));
     if (gen) {
       Launch L(p->ctx, CS_PHASE_UPDATE);
       precond_apply(p, zp(q), zcol(q), st, q, pending);  // mpk.cpp:58-59
     }
   }
+  if (pz) return;
   SpmvArgs g;
   g.x = zcol(s - 1);
   g.y = bk.P + (s - 1) * ld;
@@ -608,6 +614,22 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     ua.inv_diag = nullptr;
     ua.inv_const = 0.0;
   }
+  // PZ schedule (diagonal M, specialised order): P derived from Z in the pack
+  // and update passes, z_s in the (otherwise unused) P block's first column
+  const bool pz_on = mode == CS_MODE_FAST && fast_mpk && !general_pc && use_pack &&
+                     update_gram_supported(s) && (var & CS_VAR_P_FROM_Z) != 0 &&
+                     (var & CS_VAR_P_STORED) == 0;
+  PzArgs pz;
+  if (pz_on) {
+    const double alpha = 2.0 / (hi - lo), sigma = (hi + lo) / (hi - lo);  // mpk.hpp:22-25
+    const bool jac = p->precond == CS_PRECOND_JACOBI;
+    const double d = jac && ua.inv_const != 0.0 ? 1.0 / ua.inv_const : 1.0;
+    pz.sig1 = sigma;
+    pz.sig2 = 2.0 * sigma;
+    pz.k1 = d / alpha;
+    pz.k2 = d / (2.0 * alpha);
+    pz.diag = jac && ua.inv_const == 0.0 ? p->diag.as<double>() : nullptr;
+  }
 
   auto gram = [&](const double* u, int ku, const double* v, int kv, double* out) {
     Launch L(c, CS_PHASE_REDUCE);
@@ -617,10 +639,11 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
       launch_tree_gram(n, ku, kv, u, ld, v, ld, out, partial, ticket, st, c->stream);
   };
   // packed one-allreduce block {Q^T P, Z^T P, Z^T r, Q^T r, r^T r}
-  auto packed_reduce = [&](const double* Qm, const double* Zm) {
+  auto packed_reduce = [&](const double* Qm, const double* Zm, const PzArgs& pza = PzArgs{}) {
     if (use_pack) {
       Launch L(c, CS_PHASE_REDUCE);
-      launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, flags, c->stream);
+      launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, flags, c->stream,
+                  pza);
     } else {
       gram(Qm, s, bk.P, s, raw);
       gram(Zm, s, bk.P, s, raw + q);
@@ -684,6 +707,10 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   ua.aq = bk.AQ;
   ua.z = bk.Z;
   ua.p = bk.P;
+  if (pz_on) {  // after the setup MPK the P block is free: it holds z_s from now on
+    pz.zs = bk.P;
+    ua.pz = pz;
+  }
   if (mode == CS_MODE_FAST) {
     std::swap(bk.P, bk.AQ);  // pack wants P = A Q here
     packed_reduce(bk.Q, bk.Q);
@@ -708,8 +735,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     }
     update_pass(first);
     if (p2p) p->p2p_pending = true;  // released by the first MPK step's interior launch
-    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk, p2p);
-    packed_reduce(bk.Q, bk.Z);
+    mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk, p2p, pz_on ? bk.P : nullptr);
+    packed_reduce(bk.Q, bk.Z, pz);
     small(launch_fast_step);
   };
   auto outer_ref = [&]() {
@@ -752,8 +779,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
         if (read_state(c).done) break;
         hooks.record_gram(W);  // W_k (the one this outer's alpha was solved with)
         hooks.record_x(bk.x);
-        mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk);
-        packed_reduce(bk.Q, bk.Z);
+        mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk, false, pz_on ? bk.P : nullptr);
+        packed_reduce(bk.Q, bk.Z, pz);
         small(launch_fast_step);
       } else {
         outer_ref();

@@ -251,7 +251,7 @@ __device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double
     g.zout[row] = z;
     if (!isfinite(z)) report(g, g.col);
   } else if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF) {
-    g.y[row] = acc;
+    if (g.y) g.y[row] = acc;  // nullptr: P derived from Z later (PZ schedule)
     const double dp = JAC ? acc * e.einv : acc;
     double z = fma(g.cb, e.exd, g.ca * dp);
     if constexpr (KIND == kMpkMidF) z = fma(g.cc, e.e2, z);

@@ -272,11 +272,11 @@ struct PackShape {
 #ifndef CS_PACK_MINB
 #define CS_PACK_MINB 2
 #endif
-template <int S>
+template <int S, bool PZ>
 __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     pack_kernel(int64_t n, int64_t ld, const double* __restrict__ Q, const double* __restrict__ Z,
                 const double* __restrict__ P, const double* __restrict__ r, double* packed,
-                double* partial, unsigned* ticket, DevState* st, double* flags) {
+                double* partial, unsigned* ticket, DevState* st, double* flags, PzArgs pz) {
   using Sh = PackShape<S>;
   if (halted(st)) return;
   extern __shared__ double smem[];
@@ -304,11 +304,24 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     const int64_t row = ch * 32 + lane;
     const bool ok = row < n;
     double qv[S], zv[S], pv[S];
+    if constexpr (PZ) {
+      double zz[S + 1];
 #pragma unroll
-    for (int i = 0; i < S; ++i) {
-      qv[i] = ok ? __ldcs(Q + i * ld + row) : 0.0;
-      zv[i] = ok ? __ldcs(Z + i * ld + row) : 0.0;
-      pv[i] = ok ? __ldcs(P + i * ld + row) : 0.0;
+      for (int i = 0; i < S; ++i) {
+        qv[i] = ok ? __ldcs(Q + i * ld + row) : 0.0;
+        zz[i] = ok ? __ldcs(Z + i * ld + row) : 0.0;
+        zv[i] = zz[i];
+      }
+      zz[S] = ok ? __ldcs(pz.zs + row) : 0.0;
+      const double di = pz.diag && ok ? __ldg(pz.diag + row) : 1.0;
+      p_from_z<S>(zz, pz, di, pv);
+    } else {
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        qv[i] = ok ? __ldcs(Q + i * ld + row) : 0.0;
+        zv[i] = ok ? __ldcs(Z + i * ld + row) : 0.0;
+        pv[i] = ok ? __ldcs(P + i * ld + row) : 0.0;
+      }
     }
     const double rv = ok ? __ldcs(r + row) : 0.0;
     rr = fma(rv, rv, rr);
@@ -394,16 +407,18 @@ int pack_grid(int64_t n) {
 template <int S>
 void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
-                 double* flags, cudaStream_t strm) {
+                 double* flags, cudaStream_t strm, const PzArgs& pz) {
   using Sh = PackShape<S>;
+  const bool pzm = pz.zs != nullptr;
+  auto kern = pzm ? pack_kernel<S, true> : pack_kernel<S, false>;
   // one wave of resident blocks (a grid past the resident count leaves a
   // half-occupied second wave: 444 blocks at 2 per SM measured 0.64 ms at 256^3)
-  const int per_sm = kernel_setup(reinterpret_cast<const void*>(pack_kernel<S>), kPackWarps * 32,
+  const int per_sm = kernel_setup(reinterpret_cast<const void*>(kern), kPackWarps * 32,
                                   static_cast<int>(Sh::smem_bytes));
   const int64_t want = pack_grid(n);
   const int grid = static_cast<int>(std::min<int64_t>(want, 148 * per_sm));
-  pack_kernel<S><<<grid, kPackWarps * 32, Sh::smem_bytes, strm>>>(n, ld, q, z, p, r, packed,
-                                                                  partial, ticket, st, flags);
+  kern<<<grid, kPackWarps * 32, Sh::smem_bytes, strm>>>(n, ld, q, z, p, r, packed, partial, ticket,
+                                                        st, flags, pz);
   CS_CUDA(cudaGetLastError());
 }
 
@@ -431,8 +446,20 @@ struct Cols {
 // halves are independent, so each thread holds 2s operands instead of 4s.
 constexpr int kUpdRows = 128;
 
-template <int S, bool BETA, bool XR, bool Z0>
+// AQ role of the PZ schedule: the new-basis part P of this row derived from Z
+template <int S>
+__device__ __forceinline__ void p_row_from_z(const UpdateArgs& a, const Cols<S>& c, int64_t i,
+                                             double (&p)[S]) {
+  double zz[S + 1];
+#pragma unroll
+  for (int q = 0; q < S; ++q) zz[q] = c.z[q][i];
+  zz[S] = a.pz.zs[i];
+  p_from_z<S>(zz, a.pz, a.pz.diag ? a.pz.diag[i] : 1.0, p);
+}
+
+template <int S, bool BETA, bool XR, bool Z0, bool PZ = false>
 __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S > 0 ? S : kMaxS)> c) {
+  static_assert(!PZ || (S > 0 && BETA), "PZ needs a compile-time order and the beta path");
   if (halted(a.st)) return;
   constexpr int SM = S > 0 ? S : kMaxS;
   const int s = S > 0 ? S : a.s;
@@ -455,8 +482,10 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
     for (int q = 0; q < SM; ++q)
       if (q < s) {
         lo[q] = dst[q][i];
-        hi[q] = BETA ? src[q][i] : 0.0;
+        hi[q] = BETA && !(PZ && aq_role) ? src[q][i] : 0.0;
       }
+    if constexpr (PZ)
+      if (aq_role) p_row_from_z<SM>(a, c, i, hi);
   }
   // The AQ role overwrites Z column 0 with z_0 = M^-1 r below, which the Q role
   // of the same rows reads above: every load of the block precedes every store.
@@ -508,7 +537,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
 // partial per block; the last block reduces the partials in block order.
 constexpr int kGramStride = 132;
 
-template <int S>
+template <int S, bool PZ>
 __global__ void __launch_bounds__(kThreads)
     update_gram_kernel(UpdateArgs a, Cols<S> c, double* partial, unsigned* ticket, double* wout) {
   if (halted(a.st)) return;
@@ -548,8 +577,10 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         lo[q] = dst[q][i];
-        hi[q] = src[q][i];
+        if (!(PZ && aq_role)) hi[q] = src[q][i];
       }
+      if constexpr (PZ)
+        if (aq_role) p_row_from_z<S>(a, c, i, hi);
     } else {
 #pragma unroll
       for (int q = 0; q < S; ++q) lo[q] = hi[q] = 0.0;
@@ -649,7 +680,13 @@ template <bool BETA, bool XR, bool Z0>
 void update_dispatch(const UpdateArgs& a, cudaStream_t st) {
   const unsigned grid = grid_for(a.n, kUpdRows);
   if (a.n == 0) return;
-#define CSG_UPD(SV) \
+#define CSG_UPD(SV)                                                                          \
+  if constexpr (BETA && SV > 0) {                                                            \
+    if (a.pz.zs) {                                                                           \
+      update_kernel<SV, BETA, XR, Z0, true><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a)); \
+      break;                                                                                 \
+    }                                                                                        \
+  }                                                                                          \
   update_kernel<SV, BETA, XR, Z0><<<grid, kThreads, 0, st>>>(a, make_cols<SV ? SV : kMaxS>(a))
   switch (a.s) {
     case 1: CSG_UPD(1); break;
@@ -662,7 +699,10 @@ void update_dispatch(const UpdateArgs& a, cudaStream_t st) {
     case 10: CSG_UPD(10); break;
     case 12: CSG_UPD(12); break;
     case 16: CSG_UPD(16); break;
-    default: CSG_UPD(0); break;
+    default:
+      if (BETA && a.pz.zs) throw LibError{9, 0, "update: P-from-Z needs a specialised order"};
+      CSG_UPD(0);
+      break;
   }
 #undef CSG_UPD
   CS_CUDA(cudaGetLastError());
@@ -840,8 +880,8 @@ size_t pack_partial_doubles(int s, int64_t n) {
 
 void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
-                 double* flags, cudaStream_t strm) {
-#define CSG_PACK(SV) pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, flags, strm)
+                 double* flags, cudaStream_t strm, const PzArgs& pz) {
+#define CSG_PACK(SV) pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, flags, strm, pz)
   switch (s) {
     case 1: CSG_PACK(1); break;
     case 2: CSG_PACK(2); break;
@@ -876,12 +916,12 @@ size_t update_gram_partial_doubles(int s) {
 template <int S>
 void update_gram_launch(const UpdateArgs& a, double* partial, unsigned* ticket, double* wout,
                         cudaStream_t st) {
-  const int per_sm =
-      kernel_setup(reinterpret_cast<const void*>(update_gram_kernel<S>), kThreads, 0);
+  auto kern = a.pz.zs ? update_gram_kernel<S, true> : update_gram_kernel<S, false>;
+  const int per_sm = kernel_setup(reinterpret_cast<const void*>(kern), kThreads, 0);
   const int64_t tiles = (a.n + kUpdRows - 1) / kUpdRows;
   const int grid = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>({tiles, 148 * static_cast<int64_t>(per_sm), kUpdGramMaxBlocks})));
-  update_gram_kernel<S><<<grid, kThreads, 0, st>>>(a, make_cols<S>(a), partial, ticket, wout);
+  kern<<<grid, kThreads, 0, st>>>(a, make_cols<S>(a), partial, ticket, wout);
   CS_CUDA(cudaGetLastError());
 }
 

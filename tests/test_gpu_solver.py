@@ -229,14 +229,75 @@ def test_baseline_config2_reference_mode_bitwise(cs):
     assert res.report.rel_residual[-1] == g["final_rel_residual"]
     assert _serial_sum(res.x) == g["x_sum"]
     assert np.sqrt(_serial_sum(res.x * res.x)) == g["x_norm"]
-    # fast algebra on the same problem: converged, true residual at tolerance,
-    # solution norm agreeing with the reference (the iteration count is chaotic
-    # at this size under any non-bitwise rounding -- SURVEY App. B)
+    # fast algebra (the shipped path, device Lanczos) on the same problem: x within
+    # 1e-8 of the reference's bitwise x, and the outer count inside the reference
+    # algebra's own band under 1e-13 spectrum perturbations / tree reductions
+    # (tests/golden/count_bands.json, measured by tools/count_band.py: at s = 8 the
+    # reference itself moves 374..435 for lambda * (1 -+ 1e-13))
+    lo, hi = _band("p27:256:8")
+    for lam in (None, (g["lambda_min"], g["lambda_max"])):
+        cfg = cs.SolverConfig(s=8, tol=1e-8, max_outer=5000,
+                              spectrum=cs.SpectrumEstimate(*lam) if lam else None)
+        fast = p.pcg_s_solve(cfg=cfg)
+        assert fast.report.converged
+        assert _relx(fast.x, res.x) <= TOL_X, _relx(fast.x, res.x)
+        assert lo - 1 <= fast.report.outer_iters <= hi + 1, (fast.report.outer_iters, lo, hi)
+        r = 1.0 - p.spmv(fast.x)
+        assert np.linalg.norm(r) / np.sqrt(p.n_global) < 2e-8
+
+
+def _band(case):
+    import json, os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "count_bands.json")) as f:
+        return tuple(json.load(f)["cases"][case]["band"])
+
+
+def _golden(key):
+    import json, os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "outer_counts.json")) as f:
+        return json.load(f)[key]
+
+
+# BASELINE-scale goldens of the compiled reference (tests/golden/outer_counts.json):
+# (case, stencil, n, s). s = 4 is stable under every rounding change measured (band
+# of width 0): the fast count must equal it within +-1. s = 8 is chaotic in the
+# reference algebra itself: the fast count must lie in the measured band.
+GOLDEN_FAST = [("p27:96:8", 27, 96, 8), ("p27:128:8", 27, 128, 8), ("p27:128:4", 27, 128, 4),
+               ("p7:256:4", 7, 256, 4)]
+
+
+@pytest.mark.parametrize("case,stencil,n,s", GOLDEN_FAST, ids=[c[0] for c in GOLDEN_FAST])
+def test_fast_mode_vs_golden_counts(cs, case, stencil, n, s):
+    g = _golden(f"p{stencil}_{n}x{n}x{n}_s{s}_nu30_jacobi_1e-08")
+    lo, hi = _band(case)
+    p = cs.DeviceProblem.generate("poisson27" if stencil == 27 else "poisson7", n, n, n)
+    p.set_precond("jacobi")
+    res = p.pcg_s_solve(cfg=cs.SolverConfig(s=s, tol=1e-8, max_outer=5000))
+    rep = res.report
+    assert rep.converged
+    if lo == hi:
+        assert abs(rep.outer_iters - g["outer_iters"]) <= 1, (rep.outer_iters, g["outer_iters"])
+    assert lo - 1 <= rep.outer_iters <= hi + 1, (rep.outer_iters, lo, hi)
+    # the reference's x (its norm, %.17g in the golden) to the 1e-8 criterion
+    assert abs(np.linalg.norm(res.x) / g["x_norm"] - 1) <= TOL_X
+    assert abs(rep.spectrum_used.lambda_min / g["lambda_min"] - 1) < 1e-9
+    p.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case,n", [("p27:96:8", 96), ("p27:128:8", 128)])
+def test_fast_mode_x_vs_reference_x(cs, case, n):
+    """x of the shipped fast path within 1e-8 of the reference's bitwise x (the GPU
+    reference algebra with the reference's spectrum reproduces the golden count)."""
+    g = _golden(f"p27_{n}x{n}x{n}_s8_nu30_jacobi_1e-08")
+    p = cs.DeviceProblem.generate("poisson27", n, n, n).set_precond("jacobi")
+    spec = cs.SpectrumEstimate(g["lambda_min"], g["lambda_max"])
+    ref = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=5000, mode="reference",
+                                            spectrum=spec))
+    assert ref.report.outer_iters == g["outer_iters"]
     fast = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=5000))
-    assert fast.report.converged
-    assert abs(np.linalg.norm(fast.x) / g["x_norm"] - 1) < 1e-7
-    r = 1.0 - p.spmv(fast.x)
-    assert np.linalg.norm(r) / np.sqrt(p.n_global) < 2e-8
+    assert _relx(fast.x, ref.x) <= TOL_X
+    p.close()
 
 
 def test_analysis_hooks_reference_mode(cs, port, ref):

@@ -84,6 +84,8 @@ def main():
                     "outer": r.outer_iters, "converged": bool(r.converged),
                     "final_rel": r.rel_residual[-1], "max_delta_alpha": max(r.delta_alpha),
                     "x_norm": float(np.linalg.norm(res.x)), "wall_s": round(dt, 2),
+                    "t_solve_ms": round(r.t_solve_ms, 2),
+                    "ms_per_outer": round(r.t_solve_ms / max(r.outer_iters, 1), 4),
                     "golden_outer": gcount}, res.x
 
         xref = None
@@ -114,7 +116,9 @@ def main():
                     ("fast + reference FGS", L.CS_VAR_REF_FGS | L.CS_VAR_RECUR_W),
                     ("fast + reference MPK", L.CS_VAR_REF_MPK | L.CS_VAR_RECUR_W),
                     ("fast + explicit W + ref FGS + ref MPK",
-                     L.CS_VAR_EXPLICIT_W | L.CS_VAR_REF_FGS | L.CS_VAR_REF_MPK)]
+                     L.CS_VAR_EXPLICIT_W | L.CS_VAR_REF_FGS | L.CS_VAR_REF_MPK),
+                    ("fast + P from Z", L.CS_VAR_P_FROM_Z),
+                    ("fast + P from Z + explicit W", L.CS_VAR_P_FROM_Z | L.CS_VAR_EXPLICIT_W)]
         if a.variants:
             keep = set(a.variants.split(","))
             variants = [v for v in variants if str(v[1]) in keep]

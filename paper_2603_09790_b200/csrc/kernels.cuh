@@ -37,8 +37,10 @@ void launch_halo_gather(int64_t count, const int32_t* idx, const double* x, doub
                         cudaStream_t st);
 // SELL -> CSR row lengths and fill (global columns via row_begin / ghost map)
 void launch_sell_row_len(const SellView& a, int64_t* len, cudaStream_t st);
+// rows [r0, r1) (r0 % 32 == 0), entries written at col/val[rowptr[row] - base]
 void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* ghost_global,
-                        const int64_t* rowptr, int64_t* col, double* val, cudaStream_t st);
+                        const int64_t* rowptr, int64_t* col, double* val, int64_t r0, int64_t r1,
+                        int64_t base, cudaStream_t st);
 void scan_rowptr(const int64_t* len, int64_t n, int64_t* rowptr, void* tmp, size_t* tmp_bytes,
                  cudaStream_t st);
 // SELL-32 -> SELL-32P(U) conversion (see SellView): plan per-slice kinds, sizes

@@ -162,14 +162,20 @@ int kernel_setup(const void* func, int threads, int smem) {
   };
   static std::mutex mu;
   static std::map<Key, int> cache;
+  static std::map<std::pair<int, const void*>, int> opted;  // attribute value per (device, kernel)
   int dev = 0;
   CS_CUDA(cudaGetDevice(&dev));
   const Key k{dev, func, threads, smem};
   std::lock_guard<std::mutex> lock(mu);
   const auto it = cache.find(k);
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024)
+  // the attribute is a per-kernel upper bound: only ever raise it (a later,
+  // smaller launch must not lower the bound an earlier, larger one relies on)
+  int& cur = opted[{dev, func}];
+  if (smem > 48 * 1024 && smem > cur) {
     CS_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cur = smem;
+  }
   int per_sm = 0;
   CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem));
   per_sm = std::max(per_sm, 1);
@@ -1233,17 +1239,68 @@ void problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* 
   } else {
     CS_CUDA(cudaMemsetAsync(rp.p, 0, sizeof(int64_t), c->stream));
   }
-  const int64_t nnz = read_i64(c, rp.as<int64_t>() + n);
-  DBuf dc(sizeof(int64_t) * std::max<int64_t>(nnz, 1)), dv(sizeof(double) * std::max<int64_t>(nnz, 1));
-  if (n > 0)
-    launch_sell_to_csr(A, p->row_begin, p->ghost_global.as<int64_t>(), rp.as<int64_t>(),
-                       dc.as<int64_t>(), dv.as<double>(), c->stream);
   CS_CUDA(cudaMemcpyAsync(rowptr, rp.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
-  if (nnz) {
-    CS_CUDA(cudaMemcpyAsync(col, dc.p, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, c->stream));
-    CS_CUDA(cudaMemcpyAsync(val, dv.p, sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
-  }
   CS_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t nnz = rowptr[n];
+  if (nnz == 0) return;
+  // slice-aligned row chunks of <= 32M entries through two device stages: the
+  // conversion of chunk k+1 overlaps the download of chunk k, and device memory
+  // stays at 2 chunks (the whole int64 CSR is 58.8 GB at 27-pt 512^3)
+  constexpr int64_t kChunk = int64_t{1} << 25;
+  std::vector<int64_t> cut{0};
+  int64_t most = 0;
+  for (int64_t r = 0; r < n;) {
+    int64_t e = std::min(n, r + kSliceRows);
+    while (e < n && rowptr[std::min(n, e + kSliceRows)] - rowptr[r] <= kChunk)
+      e = std::min(n, e + kSliceRows);
+    most = std::max(most, rowptr[e] - rowptr[r]);
+    cut.push_back(e);
+    r = e;
+  }
+  const size_t cap = static_cast<size_t>(std::max<int64_t>(most, 1));
+  DBuf stage[2];
+  for (auto& b : stage) b.alloc(16 * cap);
+  cudaEvent_t conv[2], dl[2];
+  for (int i = 0; i < 2; ++i) {
+    CS_CUDA(cudaEventCreateWithFlags(&conv[i], cudaEventDisableTiming));
+    CS_CUDA(cudaEventCreateWithFlags(&dl[i], cudaEventDisableTiming));
+  }
+  const size_t nk = cut.size() - 1;
+  auto stage_ptr = [&](size_t k) { return stage[k & 1].as<int64_t>(); };
+  auto convert = [&](size_t k) {
+    const int b = static_cast<int>(k & 1);
+    if (k >= 2) CS_CUDA(cudaStreamWaitEvent(c->stream, dl[b], 0));  // stage's last download
+    int64_t* dc = stage_ptr(k);
+    launch_sell_to_csr(A, p->row_begin, p->ghost_global.as<int64_t>(), rp.as<int64_t>(), dc,
+                       reinterpret_cast<double*>(dc + cap), cut[k], cut[k + 1], rowptr[cut[k]],
+                       c->stream);
+    CS_CUDA(cudaEventRecord(conv[b], c->stream));
+  };
+  // software pipeline: chunk k+1 converts on the GPU while the host drains chunk
+  // k (a copy into pageable memory returns when it has landed)
+  convert(0);
+  for (size_t k = 0; k < nk; ++k) {
+    if (k + 1 < nk) convert(k + 1);
+    const int b = static_cast<int>(k & 1);
+    const int64_t e0 = rowptr[cut[k]], cnt = rowptr[cut[k + 1]] - e0;
+    CS_CUDA(cudaStreamWaitEvent(c->comm_stream, conv[b], 0));
+    if (cnt) {
+      int64_t* dc = stage_ptr(k);
+      CS_CUDA(cudaMemcpyAsync(col + e0, dc, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost,
+                              c->comm_stream));
+      CS_CUDA(cudaMemcpyAsync(val + e0, reinterpret_cast<double*>(dc + cap), sizeof(double) * cnt,
+                              cudaMemcpyDeviceToHost, c->comm_stream));
+    }
+    CS_CUDA(cudaEventRecord(dl[b], c->comm_stream));
+  }
+  CS_CUDA(cudaStreamSynchronize(c->comm_stream));
+  CS_CUDA(cudaStreamWaitEvent(c->stream, dl[0], 0));  // the stages are freed on c->stream
+  CS_CUDA(cudaStreamWaitEvent(c->stream, dl[1], 0));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(conv[i]);
+    cudaEventDestroy(dl[i]);
+  }
 }
 
 }  // namespace csg

@@ -277,16 +277,17 @@ __global__ void sell_row_len_kernel(SellView a, int64_t* len) {
   len[row] = cnt;
 }
 
+// rows [r0, r1) (r0 % 32 == 0); entries land at col/val[rowptr[row] - base]
 __global__ void sell_to_csr_kernel(SellView a, int64_t row_begin,
                                    const int64_t* __restrict__ ghost_global,
                                    const int64_t* __restrict__ rowptr, int64_t* col,
-                                   double* val) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= a.n_local) return;
+                                   double* val, int64_t r0, int64_t r1, int64_t base) {
+  const int64_t row = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= r1 || row >= a.n_local) return;
   const int64_t slice = row >> 5;
   const int lane = threadIdx.x & 31;
   const int width = slot_count(a, slice);
-  int64_t o = rowptr[row];
+  int64_t o = rowptr[row] - base;
   for (int k = 0; k < width; ++k) {
     const int32_t c = slot_col(a, slice, k, lane, row);
     if (c < 0) continue;
@@ -642,9 +643,11 @@ void launch_sell_row_len(const SellView& a, int64_t* len, cudaStream_t st) {
 }
 
 void launch_sell_to_csr(const SellView& a, int64_t row_begin, const int64_t* ghost_global,
-                        const int64_t* rowptr, int64_t* col, double* val, cudaStream_t st) {
-  sell_to_csr_kernel<<<grid_for(a.n_local), kThreads, 0, st>>>(a, row_begin, ghost_global, rowptr,
-                                                              col, val);
+                        const int64_t* rowptr, int64_t* col, double* val, int64_t r0, int64_t r1,
+                        int64_t base, cudaStream_t st) {
+  if (r1 <= r0) return;
+  sell_to_csr_kernel<<<grid_for(r1 - r0), kThreads, 0, st>>>(a, row_begin, ghost_global, rowptr,
+                                                            col, val, r0, r1, base);
   CS_CUDA(cudaGetLastError());
 }
 

@@ -23,6 +23,8 @@ for step in "$@"; do
       timeout 1200 python tools/count_band.py --tree-band --cases p27:256:8 --out $out/${tag}_band.json > $out/${tag}_band.log 2>&1 ;;
     band512)
       timeout 1800 python tools/count_band.py --tree-band --cases p27:512:8 --out $out/${tag}_band512.json > $out/${tag}_band512.log 2>&1 ;;
+    bandpz)
+      timeout 1500 python tools/count_band.py --skip-ref --variants 0,1,32,33 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4,p27:256:8,p27:512:8 --out $out/${tag}_bandpz.json > $out/${tag}_bandpz.log 2>&1 ;;
     bench)
       timeout 1500 python bench.py > $out/${tag}_bench.jsonl 2> $out/${tag}_bench.err ;;
     bench256)

@@ -137,7 +137,7 @@ def nnz_of(stencil, nx, ny, nz):
 
 
 def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=True,
-                   diag_stream=True):
+                   diag_stream=True, pz=False):
     """Algorithmic bytes of every SpMV-phase kernel of one solve:
     the matrix in the format actually stored (SELL-32P: FP64 value slots +
     per-slice column/pattern/meta bytes) read once, x read once, each output
@@ -155,15 +155,23 @@ def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=Tr
         b_mid = mat_bytes + 2 * v + 2 * v + j + (v if jacobi else 0) + v
     b_last = b_spmv
     per_mpk = b_last if s == 1 else b_first + (s - 2) * b_mid + b_last
-    mpks = 1 + outer  # setup MPK + one (speculative) MPK per outer iteration (fast algebra)
-    return b_resid + lanczos_steps * b_dot + mpks * per_mpk, b_spmv
+    setup_mpk = per_mpk  # the setup MPK always stores P (it becomes AQ_1)
+    if pz and mode == "fast":  # no p_q written; the last step writes z_s (a mid-type step)
+        per_mpk = (b_first - v) if s == 1 else (b_first - v) + (s - 1) * (b_mid - v)
+    # setup MPK + one (speculative) MPK per outer iteration (fast algebra)
+    return b_resid + lanczos_steps * b_dot + outer * per_mpk + setup_mpk, b_spmv
 
 
-def outer_bytes_format(mat_bytes, n, s, diag_stream=True):
+def outer_bytes_format(mat_bytes, n, s, diag_stream=True, pz=False):
     """Per-outer algorithmic bytes of the fast schedule in the stored format:
-    s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+6)."""
+    s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+6).
+    PZ schedule (P derived from Z): MPK steps write no p (the last writes z_s),
+    pack 8n(2s+2), update 8n(5s+6)."""
     v = 8 * n
     j = v if diag_stream else 0
+    if pz:
+        mpk = (mat_bytes + 2 * v + j) + (s - 1) * (mat_bytes + 3 * v + j)
+        return mpk + v * (2 * s + 2) + v * (5 * s + (6 if diag_stream else 5))
     mpk = (mat_bytes + 3 * v + j) + (s - 2) * (mat_bytes + 4 * v + j) + (mat_bytes + 2 * v) \
         if s > 1 else mat_bytes + 2 * v
     return mpk + v * (3 * s + 1) + v * (6 * s + (6 if diag_stream else 5))
@@ -352,17 +360,21 @@ def run_ours(args):
     # words (its tables are kernel parameters); other formats their SELL arrays
     mat = 4 * 32 * prob.slices if prob.cdia_classes > 0 else prob.device_bytes
     dstream = not prob.cdia_uniform_diag  # CDIA: 1/a_ii is a kernel constant
+    pz = bool(rep.schedule & 1)  # CS_SCHED_P_FROM_Z
     alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode,
-                                 diag_stream=dstream)
+                                 diag_stream=dstream, pz=pz)
     v8 = 8 * nl
     outers_t = sum(r.outer_iters for r in reps_t)
+    upd_vec = (5 if pz else 6) * args.s + (6 if dstream else 5)
     alg_phase = {
         "spmv": sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps,
-                                   args.mode, diag_stream=dstream)[0] for r in reps_t),
-        # Q, Z, AQ, P, x, r (+ D^-1 unless uniform) read; Q, AQ, x, r, z_0 written
-        "update": outers_t * v8 * (6 * args.s + (6 if dstream else 5)),
-        # Q, Z, P, r read once (one launch per outer + the setup one)
-        "reduce": (outers_t + len(reps_t)) * v8 * (3 * args.s + 1),
+                                   args.mode, diag_stream=dstream, pz=pz)[0] for r in reps_t),
+        # Q, Z, AQ, P (PZ: Z + z_s instead of P), x, r (+ D^-1 unless uniform) read;
+        # Q, AQ, x, r, z_0 written
+        "update": outers_t * v8 * upd_vec,
+        # Q, Z, P, r read once (PZ: Q, Z, z_s, r); one launch per outer + the setup one
+        "reduce": outers_t * v8 * ((2 * args.s + 2) if pz else (3 * args.s + 1))
+        + len(reps_t) * v8 * (3 * args.s + 1),
     }
     names = {"spmv": "sell_box_kernel<kMpk*> (plane-streaming FP64 SpMV over the 3x3x3 constant-"
                      "diagonal class: bulk-copied plane stages, fused MPK epilogue; gather "
@@ -399,7 +411,7 @@ def run_ours(args):
             "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}
     # whole-solve bandwidth against B_outer
     solve_outer_ms = rep.t_solve_ms / max(rep.outer_iters, 1)
-    b_out = outer_bytes_format(mat, nl, args.s, dstream)
+    b_out = outer_bytes_format(mat, nl, args.s, dstream, pz)
     b_survey = outer_bytes(nnz_l, nl, args.s)
     solve_level = {"t_outer_ms": solve_outer_ms, "B_outer_GB": b_out / 1e9,
                    "achieved_GBps": b_out / (solve_outer_ms / 1e3) / 1e9,

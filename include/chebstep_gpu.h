@@ -117,8 +117,9 @@ typedef struct {
 #define CS_VAR_REF_FGS 4      /* fast: the reference's FGS operation sequence */
 #define CS_VAR_REF_MPK 8      /* fast: the reference's MPK epilogue (zp streams, no FMA); 1 GPU */
 #define CS_VAR_TREE 16        /* reference: fixed-shape tree reductions instead of serial chains */
-#define CS_VAR_P_FROM_Z 32    /* fast: P columns derived from Z (no P stream) */
-#define CS_VAR_P_STORED 64    /* fast: force the stored-P schedule */
+#define CS_VAR_P_FROM_Z 32    /* fast: P columns derived from Z (no P stream) --
+                                 the default wherever it applies; the bit is accepted */
+#define CS_VAR_P_STORED 64    /* fast: the stored-P schedule (round-1 default) */
 
 typedef struct {
   /* SolveReport (solver.hpp:39-68), reference semantics */
@@ -144,7 +145,12 @@ typedef struct {
   double* true_rel_residual;
   double* a_norm_error;
   double* iterates;
+  int schedule;                   /* CS_SCHED_* bits of the fast schedule that ran */
 } cs_report;
+
+/* cs_report.schedule bits */
+#define CS_SCHED_P_FROM_Z 1   /* P derived from Z (no P stream) */
+#define CS_SCHED_EXPLICIT_W 2 /* W_k reduced from the vectors each outer */
 
 /* ------------------------------------------------------------ errors / info */
 const char* cs_last_error(int* payload);

@@ -66,7 +66,7 @@ class CsReport(C.Structure):
                 ("t_lanczos_ms", C.c_double), ("t_solve_ms", C.c_double),
                 ("n_kappa", C.c_int), ("n_true", C.c_int), ("n_aerr", C.c_int), ("n_iter", C.c_int),
                 ("kappa_w", _dp), ("gram_history", _dp), ("true_rel_residual", _dp),
-                ("a_norm_error", _dp), ("iterates", _dp)]
+                ("a_norm_error", _dp), ("iterates", _dp), ("schedule", C.c_int)]
 
 
 # name -> (restype, argtypes); every symbol of include/chebstep_gpu.h

@@ -690,6 +690,7 @@ class SolveReport:
     a_norm_error: np.ndarray = field(default_factory=lambda: np.zeros(0))
     iterates: list = field(default_factory=list)
     device_allreduces: int = 0
+    schedule: int = 0  # CS_SCHED_* bits of the fast schedule that ran
     kernel_launches: int = 0
     t_lanczos_ms: float = 0.0
     t_solve_ms: float = 0.0
@@ -733,6 +734,7 @@ def _unpack(rep: CsReport, bufs) -> SolveReport:
         rep.allreduce_count, rep.local_update_flops, rep.gram_solve_flops,
         SpectrumEstimate(rep.lambda_min, rep.lambda_max, "lanczos", 0.9, 1.1))
     out.device_allreduces, out.kernel_launches = rep.device_allreduces, rep.kernel_launches
+    out.schedule = rep.schedule
     out.t_lanczos_ms, out.t_solve_ms = rep.t_lanczos_ms, rep.t_solve_ms
     hooks, s, n = bufs[3] if len(bufs) > 3 else ({}, 0, 0)
     if "kappa" in hooks:

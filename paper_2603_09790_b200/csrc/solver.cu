@@ -521,6 +521,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   CS_CUDA(cudaMemcpyAsync(bk.b, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
 
   std::memset(rep, 0, offsetof(cs_report, cap));
+  rep->schedule = 0;
   rep->n_rel = rep->n_da = rep->n_db = 0;
   const double bnorm = host_norm(p, bk.b, mode);  // solver.cpp:93
   if (bnorm == 0.0) {
@@ -617,8 +618,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   // PZ schedule (diagonal M, specialised order): P derived from Z in the pack
   // and update passes, z_s in the (otherwise unused) P block's first column
   const bool pz_on = mode == CS_MODE_FAST && fast_mpk && !general_pc && use_pack &&
-                     update_gram_supported(s) && (var & CS_VAR_P_FROM_Z) != 0 &&
-                     (var & CS_VAR_P_STORED) == 0;
+                     update_gram_supported(s) && (var & CS_VAR_P_STORED) == 0;
   PzArgs pz;
   if (pz_on) {
     const double alpha = 2.0 / (hi - lo), sigma = (hi + lo) / (hi - lo);  // mpk.hpp:22-25
@@ -794,10 +794,41 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     }
     issued = cfg.max_outer;
   }
+  // Single-GPU fast solves replay whole batches of outer iterations as one CUDA
+  // graph: after the first (eager) batch, the next batch is captured once and
+  // relaunched -- every launch of an outer has the same arguments (state lives
+  // on the device), so the graph is exact; it removes the per-kernel launch
+  // gaps that dominate small (L2-resident) problems. Not with timing spans,
+  // hooks, several ranks (NCCL / peer-halo epochs) or CS_GRAPHS=0.
+  static const bool graphs_env = [] {
+    const char* e = std::getenv("CS_GRAPHS");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const bool use_graph = graphs_env && mode == CS_MODE_FAST && c->nranks == 1 && !c->timing &&
+                         !hooks.any();
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
   for (; issued < cfg.max_outer;) {
-    for (int bi = 0; bi < batch && issued < cfg.max_outer; ++bi, ++issued) {
-      if (mode == CS_MODE_FAST) outer_fast(issued == 0);
-      else outer_ref();
+    if (use_graph && issued > 0 && issued + batch <= cfg.max_outer) {
+      if (gexec == nullptr) {
+        const int64_t l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        CS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (int bi = 0; bi < batch; ++bi) outer_fast(false);
+        CS_CUDA(cudaStreamEndCapture(c->stream, &g));
+        CS_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+        CS_CUDA(cudaGraphDestroy(g));
+        graph_launches = c->launches - l0;
+      } else {
+        c->launches += graph_launches;
+      }
+      CS_CUDA(cudaGraphLaunch(gexec, c->stream));
+      issued += batch;
+    } else {
+      for (int bi = 0; bi < batch && issued < cfg.max_outer; ++bi, ++issued) {
+        if (mode == CS_MODE_FAST) outer_fast(issued == 0);
+        else outer_ref();
+      }
     }
     CS_CUDA(cudaMemcpyAsync(const_cast<int*>(&flag[slot]), &st->done, sizeof(int),
                             cudaMemcpyDeviceToHost, c->stream));
@@ -811,6 +842,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     slot ^= 1;
   }
   const double t_solve = timer.stop();
+  if (gexec) cudaGraphExecDestroy(gexec);
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   collect_timing(c);
@@ -853,6 +885,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   rep->kernel_launches = c->launches - launches0;
   rep->t_lanczos_ms = t_lz;
   rep->t_solve_ms = t_solve;
+  rep->schedule = (pz_on ? CS_SCHED_P_FROM_Z : 0) | (explicit_w ? CS_SCHED_EXPLICIT_W : 0);
 }
 
 // ====================================================================== classical PCG
@@ -893,6 +926,7 @@ void pcg_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev, dou
   CS_CUDA(cudaMemcpyAsync(xv, x0_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   CS_CUDA(cudaMemcpyAsync(bv, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   std::memset(rep, 0, offsetof(cs_report, cap));
+  rep->schedule = 0;
   rep->n_rel = rep->n_da = rep->n_db = 0;
   const double bnorm = host_norm(p, bv, mode);
   if (bnorm == 0.0) {

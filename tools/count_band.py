@@ -102,7 +102,8 @@ def main():
             print(json.dumps(d), flush=True)
 
         if a.tree_band:  # reference algebra, tree reductions, lambda perturbed
-            for eps in (0.0, 1e-13, -1e-13, 1e-12, -1e-12, 1e-11, -1e-11):
+            for eps in (0.0, 1e-13, -1e-13, 1e-12, -1e-12, 1e-11, -1e-11, 1e-10, -1e-10, 1e-9,
+                        -1e-9):
                 add(f"reference-tree lambda*(1{'-' if eps >= 0 else '+'}{abs(eps):g})", "reference",
                     L.CS_VAR_TREE, eps)
         elif not a.skip_ref:
@@ -110,15 +111,14 @@ def main():
             for eps in (1e-13, -1e-13, 1e-12, -1e-12):
                 add(f"reference lambda*(1{'-' if eps > 0 else '+'}{abs(eps):g})", "reference", 0, eps)
             add("reference, tree reductions", "reference", L.CS_VAR_TREE)
-        variants = [("fast (recurrence W, round 1)", L.CS_VAR_RECUR_W),
+        variants = [("fast, stored P (round 1)", L.CS_VAR_P_STORED),
                     ("fast shipped", 0),
                     ("fast + explicit W", L.CS_VAR_EXPLICIT_W),
-                    ("fast + reference FGS", L.CS_VAR_REF_FGS | L.CS_VAR_RECUR_W),
-                    ("fast + reference MPK", L.CS_VAR_REF_MPK | L.CS_VAR_RECUR_W),
+                    ("fast + reference FGS", L.CS_VAR_REF_FGS),
+                    ("fast + reference MPK", L.CS_VAR_REF_MPK),
                     ("fast + explicit W + ref FGS + ref MPK",
                      L.CS_VAR_EXPLICIT_W | L.CS_VAR_REF_FGS | L.CS_VAR_REF_MPK),
-                    ("fast + P from Z", L.CS_VAR_P_FROM_Z),
-                    ("fast + P from Z + explicit W", L.CS_VAR_P_FROM_Z | L.CS_VAR_EXPLICIT_W)]
+                    ("fast, stored P + explicit W", L.CS_VAR_P_STORED | L.CS_VAR_EXPLICIT_W)]
         if a.variants:
             keep = set(a.variants.split(","))
             variants = [v for v in variants if str(v[1]) in keep]

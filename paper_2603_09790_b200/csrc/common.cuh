@@ -94,6 +94,7 @@ struct CdiaClass {  // host side
   // 3x3x3 box in natural ordering, off[9g+3i+j] = g*P + i*L + j - (P+L+1)
   // (P % 4 == 0, P >= 3L, L >= 3): plane-streaming kernel (sell_box_kernel)
   int64_t boxP = 0, boxL = 0;
+  bool geo = false;  // box class with geometric participation (separable fast SpMV)
 };
 
 struct SellView {

@@ -74,6 +74,10 @@ void launch_cdia_bits(int64_t nslices, int64_t n_local, int ncls, const int64_t*
                       const int64_t* ckeys, const int32_t* nofs, const int64_t* meta,
                       const int64_t* pkey, const int2* pat, uint32_t* bits, int* bad,
                       int* nodiag, cudaStream_t st);
+// 3x3x3 box class rows [r0, r1) with plane stride P: *bad = 1 unless every
+// participation word is geometric (see sell.cu cdia_geo_kernel)
+void launch_cdia_geo_check(const uint32_t* bits, int64_t r0, int64_t r1, int64_t P, int* bad,
+                           cudaStream_t st);
 void launch_compress_fill(int64_t nslices, const int64_t* slice_ptr, const int32_t* cols,
                           const double* vals, ColMap cm, const int64_t* kind,
                           const int64_t* slice_tab, const int32_t* slice_rep,

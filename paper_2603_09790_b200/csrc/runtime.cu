@@ -654,6 +654,20 @@ void build_cdia(cs_problem* p) {
       cls[k].boxL = L;
     }
   }
+  {  // geometric participation of the box classes (separable fast SpMV)
+    DBuf geo(sizeof(int) * std::max<size_t>(cls.size(), 1));
+    CS_CUDA(cudaMemsetAsync(geo.p, 0, geo.bytes, c->stream));
+    for (size_t k = 0; k < cls.size(); ++k)
+      if (cls[k].boxL > 0)
+        launch_cdia_geo_check(p->pbits.as<uint32_t>(), cls[k].s0 * kSliceRows,
+                              std::min(cls[k].s1 * kSliceRows, p->n_local), cls[k].boxP,
+                              geo.as<int>() + k, c->stream);
+    std::vector<int> hg(cls.size());
+    CS_CUDA(cudaMemcpyAsync(hg.data(), geo.p, sizeof(int) * cls.size(), cudaMemcpyDeviceToHost,
+                            c->stream));
+    CS_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t k = 0; k < cls.size(); ++k) cls[k].geo = cls[k].boxL > 0 && hg[k] == 0;
+  }
   for (size_t k = 0; k < cls.size(); ++k) {
     cls[k].t.diag = 0.0;
     if (hf[1 + k]) continue;

@@ -764,6 +764,36 @@ __global__ void cdia_bits_kernel(int64_t nslices, int64_t n_local, int ncls,
   bits[row] = w;
 }
 
+// Is a 3x3x3 box class "geometric" (the separable plane-sum SpMV applies)?
+// Every row's 27-bit participation word must be the outer product of its own
+// x / y / z face bits (bit 9g+3i+j = z[g] & y[i] & x[j], with x = {b12, 1, b14},
+// y = {b10, 1, b16}, z = {b4, 1, b22}), and its x / y face bits must equal those
+// of the row one plane below when that row is in the class too.
+__global__ void cdia_geo_kernel(const uint32_t* __restrict__ bits, int64_t r0, int64_t r1,
+                                int64_t P, int* bad) {
+  const int64_t r = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  const uint32_t w = bits[r];
+  const uint32_t fx[3] = {(w >> 12) & 1u, 1u, (w >> 14) & 1u};
+  const uint32_t fy[3] = {(w >> 10) & 1u, 1u, (w >> 16) & 1u};
+  const uint32_t fz[3] = {(w >> 4) & 1u, 1u, (w >> 22) & 1u};
+  uint32_t e = 0;
+  for (int g = 0; g < 3; ++g)
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) e |= (fz[g] & fy[i] & fx[j]) << (9 * g + 3 * i + j);
+  bool ok = e == (w & 0x7FFFFFFu);
+  constexpr uint32_t kXY = (1u << 10) | (1u << 12) | (1u << 14) | (1u << 16);
+  if (r - P >= r0) ok = ok && ((bits[r - P] ^ w) & kXY) == 0u;
+  if (!ok) atomicExch(bad, 1);
+}
+
+void launch_cdia_geo_check(const uint32_t* bits, int64_t r0, int64_t r1, int64_t P, int* bad,
+                           cudaStream_t st) {
+  if (r1 <= r0) return;
+  cdia_geo_kernel<<<grid_for(r1 - r0), kThreads, 0, st>>>(bits, r0, r1, P, bad);
+  CS_CUDA(cudaGetLastError());
+}
+
 void launch_cdia_bits(int64_t nslices, int64_t n_local, int ncls, const int64_t* starts,
                       const int64_t* ckeys, const int32_t* nofs, const int64_t* meta,
                       const int64_t* pkey, const int2* pat, uint32_t* bits, int* bad,

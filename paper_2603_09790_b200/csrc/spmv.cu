@@ -667,6 +667,8 @@ struct BoxGeom {
   int xs;             // x doubles per stage (even)
   int ns;             // ring stages
   uint32_t stage_bytes;
+  int sep = 0;        // separable plane sums (fast kinds, NEG1, geometric class)
+  double dp1 = 0.0;   // centre value + 1 (separable: y = dp1 * x_c - sum of present x)
 };
 
 // a block's stage sequence: items [i0, i1) (item = column * nplanes + plane)
@@ -771,6 +773,35 @@ __device__ __forceinline__ void box_terms(const CdiaTable& t, const double* xs, 
     if (MODE < 2 || ((bk >> e) & 1u)) term(acc0, e, v[e]);
 }
 
+// Separable variant for the fast kinds (no bitwise-order requirement) on
+// geometric classes whose off-centre values are all -1: the plane-(k-1) box
+// sum B = sum of the present x in the 3x3 window is formed ONCE per row
+// position from three masked line sums (8 adds instead of 27), then added to
+// the plane-k row (its lower plane, if present), the plane-(k-1) row and the
+// plane-(k-2) row (its upper plane, if present); the row's value is
+// (a_ii + 1) x_c - S. fxy: any live row's word (x/y face bits agree across the
+// planes of a geometric class).
+__device__ __forceinline__ void box_terms_sep(const double* xs, int L, uint32_t fxy, bool zl,
+                                              bool zu, double& acc0, double& acc1, double& acc2,
+                                              double& cen) {
+  const bool xl = (fxy >> 12) & 1u, xr = (fxy >> 14) & 1u;
+  const bool yd = (fxy >> 10) & 1u, yu = (fxy >> 16) & 1u;
+  double ls[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double a = xs[i * L], m = xs[i * L + 1], c = xs[i * L + 2];
+    if (i == 1) cen = m;
+    double t = xl ? a + m : m;
+    ls[i] = xr ? t + c : t;
+  }
+  double bsum = ls[1];
+  if (yd) bsum += ls[0];
+  if (yu) bsum += ls[2];
+  acc0 = zl ? bsum : 0.0;
+  acc1 += bsum;
+  if (zu) acc2 += bsum;
+}
+
 #ifndef CS_BOX_MINB
 #define CS_BOX_MINB 1
 #endif
@@ -842,7 +873,23 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     const int lim_k = k < m1 ? max(0, min(width, R1 - rbk)) : 0;
     const int lim_1 = k - 1 >= m0 && k - 1 < m1 ? max(0, min(width, R1 - rb1)) : 0;
     const int lim_2 = k - 2 >= m0 ? max(0, min(width, end2 - rb2)) : 0;
+    constexpr bool kSepKind = NEG1 && (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot);
     uint32_t bk[R], mk[R];
+    double acc0[R], acc1[R], acc2[R], cen[R];
+    if (kSepKind && b.sep) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int i = threadIdx.x + j * CS_BOX_THREADS;
+        bk[j] = i < lim_k ? bs[i] : 0u;
+        acc1[j] = ap[j];
+        acc2[j] = ap2[j];
+        box_terms_sep(xs + i, L, bk[j] | bp[j] | bp2[j], (bk[j] >> 4) & 1u, (bp2[j] >> 22) & 1u,
+                      acc0[j], acc1[j], acc2[j], cen[j]);
+        acc2[j] = fma(b.dp1, cen2[j], -acc2[j]);  // (a_ii + 1) x_c - S, completed rows only
+      }
+      goto epilogue;
+    }
+    {
     bool agree = true, full = true;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -857,7 +904,6 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
       agree = agree && (!l0 || g0 == m) && (!l1 || g1 == m) && (!l2 || g2 == m);
       full = full && m == 0x1FFu;
     }
-    double acc0[R], acc1[R], acc2[R], cen[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       acc0[j] = 0.0;
@@ -881,6 +927,8 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
         box_terms<2, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
                            mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
     }
+    }
+  epilogue:
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int i = threadIdx.x + j * CS_BOX_THREADS;
@@ -980,6 +1028,12 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
     auto kern = jac ? (neg1 ? sell_box_kernel<KIND, true, true> : sell_box_kernel<KIND, true, false>)
                     : (neg1 ? sell_box_kernel<KIND, false, true> : sell_box_kernel<KIND, false, false>);
     const int per_sm = kernel_setup(reinterpret_cast<const void*>(kern), CS_BOX_THREADS, smem);
+    // separable plane sums for the fast kinds on geometric -1 classes (CS_BOX_SEP=0: off)
+    const char* sep_e = std::getenv("CS_BOX_SEP");  // per launch, like CS_SPMV_BOX
+    const bool sep_env = sep_e == nullptr || std::atoi(sep_e) != 0;
+    b.sep = sep_env && neg1 && cl.geo &&
+            (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot);
+    b.dp1 = t.v[13] + 1.0;
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(items, 148 * per_sm)));

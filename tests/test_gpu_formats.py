@@ -6,7 +6,7 @@ CS_SELL_EXPLICIT=1 (explicit int32 columns everywhere), CS_SELL_VALUES=1
 (pattern slices keep their value slots), CS_SELL_CDIA=0 (uniform tables, no
 constant-diagonal classes). For each format: the SpMV equals the CPU oracle
 bit for bit, and a fast-algebra solve is bitwise identical to the default
-format's (same spectrum injected)."""
+format's (same spectrum injected; exact-order box kernel, CS_BOX_SEP=0)."""
 import os
 
 import numpy as np
@@ -46,7 +46,10 @@ def _oracle(port, kind, dims, coef):
 
 
 @pytest.mark.parametrize("kind,dims,coef", CASES)
-def test_formats_spmv_and_solve_bitwise(cs, port, kind, dims, coef):
+def test_formats_spmv_and_solve_bitwise(cs, port, kind, dims, coef, monkeypatch):
+    # the exact-order kernels (the box kernel's separable fast variant is another
+    # rounding; tests/test_gpu_box.py bounds it)
+    monkeypatch.setenv("CS_BOX_SEP", "0")
     o = _oracle(port, kind, dims, coef)
     x = np.random.default_rng(5).standard_normal(o.n)
     want = port.spmv(o, x)

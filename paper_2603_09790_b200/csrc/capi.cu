@@ -64,15 +64,19 @@ void need(const void* p, const char* what) {
 }
 
 // device copy of a host array
+constexpr size_t kLargeCopy = size_t{32} << 20;  // staged above this (runtime.cu)
+
 struct HostIn {
   DBuf d;
   HostIn(cs_ctx* c, const void* h, size_t bytes) : d(bytes) {
-    if (bytes) CS_CUDA(cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    if (bytes >= kLargeCopy) h2d_large(c, d.p, h, bytes);
+    else if (bytes) CS_CUDA(cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, c->stream));
   }
 };
 
 void to_host(cs_ctx* c, void* h, const void* d, size_t bytes) {
-  if (bytes) CS_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+  if (bytes >= kLargeCopy) d2h_large(c, h, d, bytes);
+  else if (bytes) CS_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c->stream));
 }
 
 void sync(cs_ctx* c) { CS_CUDA(cudaStreamSynchronize(c->stream)); }

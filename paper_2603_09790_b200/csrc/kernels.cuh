@@ -162,13 +162,14 @@ size_t tree_gram_partial_doubles(int64_t n, int ku, int kv);
 // the fast MPK epilogue z_q = ca D^-1 p_q + cb z_{q-1} + cc z_{q-2} is inverted
 // instead of storing p_q = A z_{q-1}: column j of P (p_{j+1}) is
 //   j = 0: (z_1 + sigma z_0) * k1 ;  j >= 1: ((z_{j+1} + 2 sigma z_j) + z_{j-1}) * k2
-// (times diag[i] for a non-uniform Jacobi diagonal), k1 = d/alpha, k2 = d/(2 alpha).
+// times a_ii (diag[i], or the uniform value; 1 for identity), k1 = 1/alpha, k2 = 1/(2 alpha).
 // The MPK's last step writes the virtual z_s (instead of p_s) to `zs`. Saves the
 // s P columns' write in the MPK and their reads in the pack and update passes.
 struct PzArgs {
   const double* zs = nullptr;    // z_s; nullptr: P is streamed (non-PZ)
   double sig1 = 0.0, sig2 = 0.0;  // sigma, 2 sigma
-  double k1 = 0.0, k2 = 0.0;
+  double k1 = 0.0, k2 = 0.0;      // 1/alpha, 1/(2 alpha)
+  double dconst = 1.0;            // the uniform diagonal a_ii (Jacobi), 1 (identity)
   const double* diag = nullptr;   // non-uniform Jacobi: the diagonal a_ii (else nullptr)
 };
 #ifdef __CUDACC__
@@ -182,7 +183,7 @@ __device__ __forceinline__ void p_from_z(const double (&zz)[S + 1], const PzArgs
     double t;
     if (j == 0) t = fma(a.sig1, zz[0], zz[1]) * a.k1;
     else t = (fma(a.sig2, zz[j], zz[j + 1]) + zz[j - 1]) * a.k2;
-    p[j] = a.diag ? t * di : t;
+    p[j] = t * di;  // di = a_ii of the row (diag[i] or the uniform value): format-independent
   }
 }
 #endif

@@ -77,19 +77,26 @@ __global__ void __launch_bounds__(kThreads)
   if (i < n) {
     double rv = r[i], gv = gr[i];
     if constexpr (MB > 0) {
-      double vv[MB], gg[MB];
+      // chunks of 8 pairs: 16 loads in flight per thread at a register count
+      // that keeps several blocks resident (all 2m at once needed ~200 registers)
+      constexpr int kC = 8;
+#pragma unroll 1
+      for (int c0 = 0; c0 < MB; c0 += kC) {
+        if (c0 >= m) break;
+        double vv[kC], gg[kC];
 #pragma unroll
-      for (int c = 0; c < MB; ++c)
-        if (c < m) {
-          vv[c] = __ldcs(V + c * ld + i);
-          gg[c] = __ldcs(G + c * ld + i);
-        }
+        for (int c = 0; c < kC; ++c)
+          if (c0 + c < m) {
+            vv[c] = __ldcs(V + (c0 + c) * ld + i);
+            gg[c] = __ldcs(G + (c0 + c) * ld + i);
+          }
 #pragma unroll
-      for (int c = 0; c < MB; ++c)
-        if (c < m) {
-          rv = fma(-sp[c], vv[c], rv);
-          gv = fma(-sp[c], gg[c], gv);
-        }
+        for (int c = 0; c < kC; ++c)
+          if (c0 + c < m) {
+            rv = fma(-sp[c0 + c], vv[c], rv);
+            gv = fma(-sp[c0 + c], gg[c], gv);
+          }
+      }
     } else {
       for (int c = 0; c < m; ++c) {
         rv = fma(-sp[c], V[c * ld + i], rv);

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <tuple>
 #include <cstdio>
 #include <cstdlib>
@@ -457,6 +458,7 @@ void ctx_destroy(cs_ctx* c) {
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->comm_stream);
   cudaFreeHost(c->pinned);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
   delete c;
 }
 
@@ -993,13 +995,106 @@ struct UploadTrace {
 // compute stream. Device memory: 2 chunks instead of the whole int64 CSR
 // (58.8 GB at 27-pt 512^3); the host arrays may be pageable (the caller's
 // std::vector), each chunk is one cudaMemcpyAsync per array.
+// Host copy of `bytes` split over `threads` workers (pageable -> page-locked
+// staging: one thread's memcpy reaches ~11 GB/s, the DMA from page-locked
+// memory ~55 GB/s).
+void parallel_copy(void* dst, const void* src, size_t bytes, int threads) {
+  if (threads <= 1 || bytes < (size_t{8} << 20)) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t part = (bytes / threads + 4095) & ~size_t{4095};
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) {
+    const size_t b0 = t * part;
+    if (b0 >= bytes) break;
+    const size_t len = std::min(part, bytes - b0);
+    pool.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, len);
+    });
+  }
+  std::memcpy(dst, src, std::min(part, bytes));
+  for (auto& th : pool) th.join();
+}
+
+int upload_threads() {
+  const char* e = std::getenv("CS_UPLOAD_THREADS");
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  return e ? std::max(1, std::atoi(e)) : std::min(hw, 16);
+}
+
+// two page-locked staging buffers of `bytes` each, cached on the context
+char* host_stage(cs_ctx* c, size_t bytes) {
+  if (c->host_stage_bytes < bytes) {
+    if (c->host_stage) cudaFreeHost(c->host_stage);
+    c->host_stage = nullptr;
+    c->host_stage_bytes = 0;
+    CS_CUDA(cudaHostAlloc(&c->host_stage, 2 * bytes, cudaHostAllocPortable));
+    c->host_stage_bytes = bytes;
+  }
+  return static_cast<char*>(c->host_stage);
+}
+
+// Large host<->device copies of caller (pageable) memory through the context's
+// page-locked staging: 64 MB chunks, host threads fill / drain one buffer while
+// the DMA of the other runs. Both are ordered on c->stream.
+constexpr size_t kStageChunk = size_t{64} << 20;
+
+void h2d_large(cs_ctx* c, void* dev, const void* host, size_t bytes) {
+  char* hs = host_stage(c, std::max(c->host_stage_bytes, kStageChunk));
+  const size_t chunk = c->host_stage_bytes;
+  const int nt = upload_threads();
+  cudaEvent_t ev[2];
+  for (auto& e : ev) CS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (size_t off = 0, k = 0; off < bytes; off += chunk, ++k) {
+    const int b = static_cast<int>(k & 1);
+    const size_t len = std::min(chunk, bytes - off);
+    if (k >= 2) CS_CUDA(cudaEventSynchronize(ev[b]));
+    parallel_copy(hs + b * chunk, static_cast<const char*>(host) + off, len, nt);
+    CS_CUDA(cudaMemcpyAsync(static_cast<char*>(dev) + off, hs + b * chunk, len,
+                            cudaMemcpyHostToDevice, c->stream));
+    CS_CUDA(cudaEventRecord(ev[b], c->stream));
+  }
+  CS_CUDA(cudaStreamSynchronize(c->stream));  // the staging may be reused right after
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
+void d2h_large(cs_ctx* c, void* host, const void* dev, size_t bytes) {
+  char* hs = host_stage(c, std::max(c->host_stage_bytes, kStageChunk));
+  const size_t chunk = c->host_stage_bytes;
+  const int nt = upload_threads();
+  cudaEvent_t ev[2];
+  for (auto& e : ev) CS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const size_t nk = (bytes + chunk - 1) / chunk;
+  auto issue = [&](size_t k) {
+    const size_t off = k * chunk, len = std::min(chunk, bytes - off);
+    CS_CUDA(cudaMemcpyAsync(hs + (k & 1) * chunk, static_cast<const char*>(dev) + off, len,
+                            cudaMemcpyDeviceToHost, c->stream));
+    CS_CUDA(cudaEventRecord(ev[k & 1], c->stream));
+  };
+  if (nk) issue(0);
+  for (size_t k = 0; k < nk; ++k) {
+    CS_CUDA(cudaEventSynchronize(ev[k & 1]));
+    if (k + 1 < nk) issue(k + 1);  // the next DMA runs while this chunk drains
+    const size_t off = k * chunk, len = std::min(chunk, bytes - off);
+    parallel_copy(static_cast<char*>(host) + off, hs + (k & 1) * chunk, len, nt);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
 void stream_csr_fill(cs_problem* p, const int64_t* rowptr, const int64_t* col, const double* val,
                      const int64_t* drp, int* bad) {
   cs_ctx* c = p->ctx;
   const int64_t n = p->n_local;
   if (n == 0) return;
+  // staged (default): host threads copy each chunk into page-locked memory while
+  // the previous chunk's DMA and SELL fill run; CS_UPLOAD_STAGED=0: one
+  // cudaMemcpyAsync per array per chunk straight from the caller's memory
+  const char* senv = std::getenv("CS_UPLOAD_STAGED");
+  const bool staged = senv == nullptr || std::atoi(senv) != 0;
   const char* env = std::getenv("CS_UPLOAD_CHUNK_NNZ");
-  const int64_t kChunkNnz = env ? std::max<int64_t>(std::atoll(env), 1) : (int64_t{1} << 25);
+  const int64_t kChunkNnz = env ? std::max<int64_t>(std::atoll(env), 1)
+                                : (staged ? int64_t{1} << 23 : int64_t{1} << 25);
   std::vector<int64_t> cut{0};
   int64_t most = 0;
   for (int64_t r = 0; r < n;) {
@@ -1021,6 +1116,8 @@ void stream_csr_fill(cs_problem* p, const int64_t* rowptr, const int64_t* col, c
   }
   CS_CUDA(cudaEventRecord(ready, c->stream));  // staging allocations are stream-ordered
   CS_CUDA(cudaStreamWaitEvent(c->comm_stream, ready, 0));
+  char* hs = staged ? host_stage(c, 16 * cap) : nullptr;
+  const int nthreads = upload_threads();
   for (size_t k = 0; k + 1 < cut.size(); ++k) {
     const int b = static_cast<int>(k & 1);
     const int64_t r0 = cut[k], r1 = cut[k + 1];
@@ -1028,7 +1125,16 @@ void stream_csr_fill(cs_problem* p, const int64_t* rowptr, const int64_t* col, c
     int64_t* scol = stage[b].as<int64_t>();
     double* sval = reinterpret_cast<double*>(scol + cap);
     if (k >= 2) CS_CUDA(cudaStreamWaitEvent(c->comm_stream, filled[b], 0));
-    if (cnt > 0) {
+    if (cnt > 0 && staged) {
+      char* hb = hs + static_cast<size_t>(b) * 16 * cap;
+      if (k >= 2) CS_CUDA(cudaEventSynchronize(copied[b]));  // its last DMA has drained
+      parallel_copy(hb, col + e0, sizeof(int64_t) * cnt, nthreads);
+      parallel_copy(hb + 8 * cap, val + e0, sizeof(double) * cnt, nthreads);
+      CS_CUDA(cudaMemcpyAsync(scol, hb, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice,
+                              c->comm_stream));
+      CS_CUDA(cudaMemcpyAsync(sval, hb + 8 * cap, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                              c->comm_stream));
+    } else if (cnt > 0) {
       CS_CUDA(cudaMemcpyAsync(scol, col + e0, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice,
                               c->comm_stream));
       CS_CUDA(cudaMemcpyAsync(sval, val + e0, sizeof(double) * cnt, cudaMemcpyHostToDevice,
@@ -1042,6 +1148,7 @@ void stream_csr_fill(cs_problem* p, const int64_t* rowptr, const int64_t* col, c
     CS_CUDA(cudaEventRecord(filled[b], c->stream));
   }
   CS_CUDA(cudaStreamSynchronize(c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->comm_stream));
   cudaEventDestroy(ready);
   for (int i = 0; i < 2; ++i) {
     cudaEventDestroy(copied[i]);

@@ -110,6 +110,8 @@ struct cs_ctx {
   csg::DBuf normbuf;    // ||b|| reduction scratch
   size_t scratch_bytes = 0;
   void* pinned = nullptr;  // pinned host staging for flags
+  void* host_stage = nullptr;    // 2 x host_stage_bytes page-locked upload staging
+  size_t host_stage_bytes = 0;
   unsigned char uuid[16] = {};
   bool uuid_known = false;
 };
@@ -221,6 +223,10 @@ void collect_timing(cs_ctx* c);
 void spmv_halo(cs_problem* p, int kind, SpmvArgs g, double* operand_col);
 void halo_exchange(cs_problem* p, double* col);
 void allreduce_sum(cs_ctx* c, double* dev, size_t count);
+// large pageable host <-> device copies through page-locked staging (host
+// threads + DMA overlapped); complete when they return
+void h2d_large(cs_ctx* c, void* dev, const void* host, size_t bytes);
+void d2h_large(cs_ctx* c, void* host, const void* dev, size_t bytes);
 // out = M^-1 in for every preconditioner kind (+ the breakdown check of column
 // col >= 0, recorded as pending when `pending`); general kinds: block Jacobi,
 // device plugin

@@ -6,6 +6,8 @@
 // an 4-byte convergence flag every `check_every` outer iterations while the
 // next batch is already queued (stop decisions are taken on the device).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -491,6 +493,24 @@ struct Hooks {
 
 }  // namespace
 
+namespace {
+// CS_TRACE=1: host-side phase times of a solve (synchronising; diagnostics only)
+struct SolveTrace {
+  cudaStream_t st;
+  bool on = std::getenv("CS_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit SolveTrace(cudaStream_t s) : st(s) {}
+  void mark(const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cs-trace]   solve %s %.1f ms\n", phase,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+}  // namespace
+
 void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
                     const cs_config& cfg, double* x_dev, cs_report* rep) {
   cs_ctx* c = p->ctx;
@@ -513,8 +533,10 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   const int64_t launches0 = c->launches, allred0 = c->allreduces;
   const double nglob = static_cast<double>(p->n_global);
 
+  SolveTrace trace(c->stream);
   Blocks bk = workspace(p, s);
   DevState* st = c->state.as<DevState>();
+  trace.mark("workspace");
 
   // vectors in: x (ghost slots filled by the halo), b
   CS_CUDA(cudaMemcpyAsync(bk.x, x0_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
@@ -532,6 +554,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     if (rep->rel_residual && rep->cap > 0) rep->rel_residual[0] = 0.0;
     return;
   }
+  trace.mark("vectors+bnorm");
   double lo = cfg.lambda_min, hi = cfg.lambda_max, t_lz = 0.0;
   if (!cfg.has_spectrum) {
     estimate_interval_dev(p, cfg.lanczos_steps, cfg.seed, mode, &lo, &hi, &t_lz);
@@ -541,6 +564,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
       CS_CUDA(cudaMemcpyAsync(bk.b, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
     }
   }
+  trace.mark("lanczos");
   rep->lambda_min = lo;
   rep->lambda_max = hi;
   if (!(hi > lo) || !(lo > 0.0) || !std::isfinite(hi))  // mpk.cpp:11-16
@@ -602,11 +626,13 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   ua.x = bk.x;
   ua.r = bk.r;
   ua.inv_diag = A.inv_diag;
+  double diag_const = 0.0;  // the uniform a_ii when every row shares it (CDIA), else 0
   {  // one diagonal value for every row (constant-coefficient stencils): 1/a_ii as a constant
     double d0 = A.ncdia > 0 ? A.cdia[0].t.diag : 0.0;
     for (int k = 1; k < A.ncdia; ++k)
       if (std::memcmp(&A.cdia[k].t.diag, &d0, sizeof d0) != 0) d0 = 0.0;
     ua.inv_const = A.inv_diag != nullptr && d0 != 0.0 ? 1.0 / d0 : 0.0;  // = inv_diag_kernel
+    diag_const = A.inv_diag != nullptr ? d0 : 0.0;
   }
   ua.alpha = alpha_d;
   ua.st = st;
@@ -623,12 +649,12 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   if (pz_on) {
     const double alpha = 2.0 / (hi - lo), sigma = (hi + lo) / (hi - lo);  // mpk.hpp:22-25
     const bool jac = p->precond == CS_PRECOND_JACOBI;
-    const double d = jac && ua.inv_const != 0.0 ? 1.0 / ua.inv_const : 1.0;
     pz.sig1 = sigma;
     pz.sig2 = 2.0 * sigma;
-    pz.k1 = d / alpha;
-    pz.k2 = d / (2.0 * alpha);
-    pz.diag = jac && ua.inv_const == 0.0 ? p->diag.as<double>() : nullptr;
+    pz.k1 = 1.0 / alpha;
+    pz.k2 = 1.0 / (2.0 * alpha);
+    pz.dconst = jac && diag_const != 0.0 ? diag_const : 1.0;
+    pz.diag = jac && diag_const == 0.0 ? p->diag.as<double>() : nullptr;
   }
 
   auto gram = [&](const double* u, int ku, const double* v, int kv, double* out) {
@@ -842,6 +868,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
     slot ^= 1;
   }
   const double t_solve = timer.stop();
+  trace.mark("setup+outer loop");
   if (gexec) cudaGraphExecDestroy(gexec);
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
@@ -886,6 +913,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   rep->t_lanczos_ms = t_lz;
   rep->t_solve_ms = t_solve;
   rep->schedule = (pz_on ? CS_SCHED_P_FROM_Z : 0) | (explicit_w ? CS_SCHED_EXPLICIT_W : 0);
+  trace.mark("report");
 }
 
 // ====================================================================== classical PCG

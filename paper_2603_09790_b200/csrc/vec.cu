@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
         zv[i] = zz[i];
       }
       zz[S] = ok ? __ldcs(pz.zs + row) : 0.0;
-      const double di = pz.diag && ok ? __ldg(pz.diag + row) : 1.0;
+      const double di = pz.diag ? (ok ? __ldg(pz.diag + row) : 1.0) : pz.dconst;
       p_from_z<S>(zz, pz, di, pv);
     } else {
 #pragma unroll
@@ -454,7 +454,7 @@ __device__ __forceinline__ void p_row_from_z(const UpdateArgs& a, const Cols<S>&
 #pragma unroll
   for (int q = 0; q < S; ++q) zz[q] = c.z[q][i];
   zz[S] = a.pz.zs[i];
-  p_from_z<S>(zz, a.pz, a.pz.diag ? a.pz.diag[i] : 1.0, p);
+  p_from_z<S>(zz, a.pz, a.pz.diag ? a.pz.diag[i] : a.pz.dconst, p);
 }
 
 template <int S, bool BETA, bool XR, bool Z0, bool PZ = false>
@@ -492,14 +492,18 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
   if constexpr (Z0) __syncthreads();
   if (!active) return;
   if constexpr (BETA) {
-    // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39)
+    // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39);
+    // the fast pass (Z0) contracts each term into one FMA (half the FP64 issue)
 #pragma unroll
     for (int q = 0; q < SM; ++q)
       if (q < s) {
         const double xq = lo[q];
 #pragma unroll
         for (int j = 0; j < SM; ++j)
-          if (j < s) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * s], xq));
+          if (j < s) {
+            if constexpr (Z0) hi[j] = fma(sh_beta[q + j * s], xq, hi[j]);
+            else hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * s], xq));
+          }
       }
 #pragma unroll
     for (int j = 0; j < SM; ++j)
@@ -510,7 +514,10 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
     const double sign = aq_role ? -1.0 : 1.0;
 #pragma unroll
     for (int j = 0; j < SM; ++j)
-      if (j < s) acc = __dadd_rn(acc, __dmul_rn(sign * sh_alpha[j], BETA ? hi[j] : lo[j]));
+      if (j < s) {
+        if constexpr (Z0) acc = fma(sign * sh_alpha[j], BETA ? hi[j] : lo[j], acc);
+        else acc = __dadd_rn(acc, __dmul_rn(sign * sh_alpha[j], BETA ? hi[j] : lo[j]));
+      }
     if (aq_role) a.r[i] = acc;
     else a.x[i] = acc;
   }
@@ -588,12 +595,12 @@ __global__ void __launch_bounds__(kThreads)
     // the AQ role overwrites Z column 0 (z_0) that the Q role of the same rows
     // reads above; the previous tile's fragment loads also end here
     __syncthreads();
-    // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39)
+    // out_j = y_j + sum_q c_qj x_q, ascending q for every j (fused as in update_kernel)
 #pragma unroll
     for (int q = 0; q < S; ++q) {
       const double xq = lo[q];
 #pragma unroll
-      for (int j = 0; j < S; ++j) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * S], xq));
+      for (int j = 0; j < S; ++j) hi[j] = fma(sh_beta[q + j * S], xq, hi[j]);
     }
 #pragma unroll
     for (int j = 0; j < S; ++j) tile[aq_role][j][rl] = active ? hi[j] : 0.0;
@@ -602,7 +609,7 @@ __global__ void __launch_bounds__(kThreads)
       for (int j = 0; j < S; ++j) dst[j][i] = hi[j];
       // solver.cpp:159-162: x += alpha_j q_j ; r += (-alpha_j) aq_j, ascending j
 #pragma unroll
-      for (int j = 0; j < S; ++j) xr = __dadd_rn(xr, __dmul_rn(sign * sh_alpha[j], hi[j]));
+      for (int j = 0; j < S; ++j) xr = fma(sign * sh_alpha[j], hi[j], xr);
       if (aq_role) {
         a.r[i] = xr;
         const double z = !a.inv_diag        ? xr

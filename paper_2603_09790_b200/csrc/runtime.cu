@@ -451,6 +451,7 @@ void ctx_destroy(cs_ctx* c) {
   c->scratch.release();
   c->normbuf.release();
   c->state.release();
+  c->lz.release();
   cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
   cudaEventDestroy(c->ev_ready);

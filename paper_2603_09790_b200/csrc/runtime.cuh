@@ -108,6 +108,10 @@ struct cs_ctx {
   csg::DBuf state;      // DevState
   csg::DBuf scratch;    // partials / tickets / scalars
   csg::DBuf normbuf;    // ||b|| reduction scratch
+  // Lanczos basis (2 x steps vectors + 3) of the last estimate, reused by every
+  // problem of this context (one solve at a time): 86 GB at 512^3, so a fresh
+  // problem per call (the reference-signature entry) must not re-map it
+  csg::DBuf lz;
   size_t scratch_bytes = 0;
   void* pinned = nullptr;  // pinned host staging for flags
   void* host_stage = nullptr;    // 2 x host_stage_bytes page-locked upload staging
@@ -165,7 +169,6 @@ struct cs_problem {
   int ws_s = -1;
   uint64_t ws_gen = 0;  // bumped whenever ws is (re)allocated
   csg::DBuf ws;
-  csg::DBuf lz;
   // NVLink peer-memory halo of the fast MPK (z-slab problems):
   // the neighbours' workspaces and receive counters mapped by CUDA IPC
   struct PeerMap {

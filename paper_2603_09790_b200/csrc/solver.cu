@@ -118,22 +118,22 @@ void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, do
   CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
   const int64_t n = p->n_local, ld = p->ld;
-  // The 2*steps basis vectors are cached on the problem; when HBM is short
-  // (512^3: 86 GB of basis next to a 43 GB matrix) the solve workspace is
-  // released first and reallocated after the estimate.
+  // The 2*steps basis vectors are cached on the context (every problem of it
+  // reuses them); when HBM is short (512^3: 86 GB of basis next to the solve
+  // workspace) this problem's workspace is released first and rebuilt after.
   const size_t lz_bytes = sizeof(double) * (static_cast<size_t>(2 * steps + 3) * ld);
-  if (p->lz.bytes < lz_bytes) {
+  if (c->lz.bytes < lz_bytes) {
     CS_CUDA(cudaStreamSynchronize(c->stream));
-    p->lz.release();
+    c->lz.release();
     size_t free_b = 0, total_b = 0;
     CS_CUDA(cudaMemGetInfo(&free_b, &total_b));
     if (free_b < lz_bytes + (size_t{1} << 30)) {
       p->ws.release();
       p->ws_s = -1;
     }
-    p->lz.alloc(lz_bytes);
+    c->lz.alloc(lz_bytes);
   }
-  double* V = p->lz.as<double>();
+  double* V = c->lz.as<double>();
   double* G = V + steps * ld;
   double* t = G + steps * ld;
   double* r = t + ld;

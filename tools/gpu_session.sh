@@ -58,6 +58,15 @@ for step in "$@"; do
     bench4)
       timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
         --master-port 29613 bench.py --gpus 4 > $out/${tag}_bench4.jsonl 2> $out/${tag}_bench4.err ;;
+    bench4w)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+        --master-port 29615 bench.py --gpus 4 --grid 256 --scaling weak --no-cpu > $out/${tag}_bench4w.jsonl 2> $out/${tag}_bench4w.err ;;
+    bench2s256)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29617 bench.py --gpus 2 --grid 256 --no-cpu > $out/${tag}_bench2s256.jsonl 2> $out/${tag}_bench2s256.err ;;
+    bench4s256)
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+        --master-port 29619 bench.py --gpus 4 --grid 256 --no-cpu > $out/${tag}_bench4s256.jsonl 2> $out/${tag}_bench4s256.err ;;
     *) echo "unknown step $step" >> $out/${tag}_status.txt ;;
   esac
   echo "   rc=$? $(date +%T)" >> $out/${tag}_status.txt

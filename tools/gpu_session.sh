@@ -31,6 +31,13 @@ for step in "$@"; do
       timeout 1200 ncu --set full --clock-control none --import-source on \
         -k regex:"pack_kernel|update_kernel|sell_box_kernel" -s 40 -c 3 -o $out/${tag}_pz \
         python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_pz.log 2>&1 ;;
+    ncu_hot)
+      for spec in "box:sell_box_kernel:70:2" "upd:update_kernel:6:1" "pack:pack_kernel:6:1" "lz:cgs_kernel|proj_kernel:70:2"; do
+        IFS=: read nm rx sk cn <<< "$spec"
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $sk -c $cn \
+          -o $out/${tag}_$nm python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg \
+          > $out/${tag}_ncu_$nm.log 2>&1
+      done ;;
     bench)
       timeout 1500 python bench.py > $out/${tag}_bench.jsonl 2> $out/${tag}_bench.err ;;
     bench256)

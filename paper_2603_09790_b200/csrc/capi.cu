@@ -491,6 +491,7 @@ int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
       g.cb = -0.5;
       g.cc = -1.0;
       const int k = kind == 0 ? kPlain : kind == 1 ? kMpkMid : kMpkMidF;
+      if (k == kMpkMidF && std::getenv("CS_BENCH_NOP")) g.y = nullptr;  // PZ-schedule step
       run = [&, k] { launch_spmv(k, p->view(), g, 0, p->nslices, c->stream); };
     } else if (kind == 3) {
       unsigned* ticket = reinterpret_cast<unsigned*>(sm + 4 * S * S + 2048);

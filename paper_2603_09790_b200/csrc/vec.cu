@@ -457,9 +457,15 @@ __device__ __forceinline__ void p_row_from_z(const UpdateArgs& a, const Cols<S>&
   p_from_z<S>(zz, a.pz, a.pz.diag ? a.pz.diag[i] : a.pz.dconst, p);
 }
 
+// Lanes 0-15 of a warp take the Q role of 16 rows, lanes 16-31 the AQ role of
+// the SAME rows (each load instruction moves two full 128-byte segments). The
+// AQ role overwrites Z column 0 with z_0 = M^-1 r, which the Q role of its row
+// reads: the pair shares a warp, so a warp barrier (or, in the PZ schedule, the
+// shuffle that hands the Q lane's Z row to its AQ lane) orders the load before
+// the store -- no block-wide barrier.
 template <int S, bool BETA, bool XR, bool Z0, bool PZ = false>
 __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S > 0 ? S : kMaxS)> c) {
-  static_assert(!PZ || (S > 0 && BETA), "PZ needs a compile-time order and the beta path");
+  static_assert(!PZ || (S > 0 && BETA && Z0), "PZ: compile-time order, fast beta pass");
   if (halted(a.st)) return;
   constexpr int SM = S > 0 ? S : kMaxS;
   const int s = S > 0 ? S : a.s;
@@ -469,29 +475,41 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
   if constexpr (BETA)
     for (int t = threadIdx.x; t < s * s; t += blockDim.x) sh_beta[t] = a.beta[t];
   __syncthreads();
-  const bool aq_role = threadIdx.x >= kUpdRows;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * kUpdRows + (threadIdx.x & (kUpdRows - 1));
+  const int lane = threadIdx.x & 31;
+  const bool aq_role = lane >= 16;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kUpdRows + (threadIdx.x >> 5) * 16 + (lane & 15);
   const bool active = i < a.n;
   double* const* dst = aq_role ? c.aq : c.q;      // updated in place
   const double* const* src = aq_role ? c.p : c.z; // new basis part
   double acc = 0.0;
   double lo[SM], hi[SM];
+#pragma unroll
+  for (int q = 0; q < SM; ++q) lo[q] = hi[q] = 0.0;
+  double zs_i = 0.0, d_i = 1.0;
   if (active) {
     if constexpr (XR) acc = aq_role ? a.r[i] : a.x[i];
 #pragma unroll
     for (int q = 0; q < SM; ++q)
       if (q < s) {
         lo[q] = dst[q][i];
-        hi[q] = BETA && !(PZ && aq_role) ? src[q][i] : 0.0;
+        if (BETA && !(PZ && aq_role)) hi[q] = src[q][i];
       }
     if constexpr (PZ)
-      if (aq_role) p_row_from_z<SM>(a, c, i, hi);
+      if (aq_role) {
+        zs_i = a.pz.zs[i];
+        d_i = a.pz.diag ? a.pz.diag[i] : a.pz.dconst;
+      }
   }
-  // The AQ role overwrites Z column 0 with z_0 = M^-1 r below, which the Q role
-  // of the same rows reads above: every load of the block precedes every store.
-  if constexpr (Z0) __syncthreads();
-  if (!active) return;
-  if constexpr (BETA) {
+  if constexpr (PZ) {  // every lane: the Q lane's Z row to its AQ lane
+    double zz[SM + 1];
+#pragma unroll
+    for (int q = 0; q < SM; ++q) zz[q] = __shfl_xor_sync(0xffffffffu, hi[q], 16);
+    zz[SM] = zs_i;
+    if (aq_role) p_from_z<SM>(zz, a.pz, d_i, hi);
+  } else if constexpr (Z0) {
+    __syncwarp();
+  }
+  if (!active) return;  if constexpr (BETA) {
     // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39);
     // the fast pass (Z0) contracts each term into one FMA (half the FP64 issue)
 #pragma unroll
@@ -553,12 +571,18 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ double sh_alpha[S];
   __shared__ double sh_beta[S * S];
   __shared__ double tile[2][SP][kGramStride];
+  // Q role's Z rows for the AQ role (static shared memory allows it up to s = 8;
+  // larger orders reload Z from global memory)
+  constexpr bool kShZ = PZ && S <= 8;
+  __shared__ double sh_z[kShZ ? S : 1][kShZ ? kUpdRows : 1];
   __shared__ bool last;
   for (int t = threadIdx.x; t < S; t += blockDim.x) sh_alpha[t] = a.alpha[t];
   for (int t = threadIdx.x; t < S * S; t += blockDim.x) sh_beta[t] = a.beta[t];
-  for (int t = threadIdx.x; t < 2 * (SP - S) * kGramStride; t += blockDim.x) {
-    const int h = t / ((SP - S) * kGramStride), rem = t % ((SP - S) * kGramStride);
-    tile[h][S + rem / kGramStride][rem % kGramStride] = 0.0;  // padded columns stay zero
+  if constexpr (SP > S) {
+    for (int t = threadIdx.x; t < 2 * (SP - S) * kGramStride; t += blockDim.x) {
+      const int h = t / ((SP - S) * kGramStride), rem = t % ((SP - S) * kGramStride);
+      tile[h][S + rem / kGramStride][rem % kGramStride] = 0.0;  // padded columns stay zero
+    }
   }
   __syncthreads();
   const bool aq_role = threadIdx.x >= kUpdRows;
@@ -579,6 +603,7 @@ __global__ void __launch_bounds__(kThreads)
     const bool active = i < a.n;
     double lo[S], hi[S];
     double xr = 0.0;
+    double zs_i = 0.0, d_i = 1.0;
     if (active) {
       xr = aq_role ? a.r[i] : a.x[i];
 #pragma unroll
@@ -586,8 +611,17 @@ __global__ void __launch_bounds__(kThreads)
         lo[q] = dst[q][i];
         if (!(PZ && aq_role)) hi[q] = src[q][i];
       }
-      if constexpr (PZ)
+      if constexpr (kShZ) {
+        if (!aq_role) {
+#pragma unroll
+          for (int q = 0; q < S; ++q) sh_z[q][rl] = hi[q];
+        } else {
+          zs_i = a.pz.zs[i];
+          d_i = a.pz.diag ? a.pz.diag[i] : a.pz.dconst;
+        }
+      } else if constexpr (PZ) {
         if (aq_role) p_row_from_z<S>(a, c, i, hi);
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < S; ++q) lo[q] = hi[q] = 0.0;
@@ -595,6 +629,15 @@ __global__ void __launch_bounds__(kThreads)
     // the AQ role overwrites Z column 0 (z_0) that the Q role of the same rows
     // reads above; the previous tile's fragment loads also end here
     __syncthreads();
+    if constexpr (kShZ) {
+      if (aq_role && active) {
+        double zz[S + 1];
+#pragma unroll
+        for (int q = 0; q < S; ++q) zz[q] = sh_z[q][rl];
+        zz[S] = zs_i;
+        p_from_z<S>(zz, a.pz, d_i, hi);
+      }
+    }
     // out_j = y_j + sum_q c_qj x_q, ascending q for every j (fused as in update_kernel)
 #pragma unroll
     for (int q = 0; q < S; ++q) {
@@ -688,7 +731,7 @@ void update_dispatch(const UpdateArgs& a, cudaStream_t st) {
   const unsigned grid = grid_for(a.n, kUpdRows);
   if (a.n == 0) return;
 #define CSG_UPD(SV)                                                                          \
-  if constexpr (BETA && SV > 0) {                                                            \
+  if constexpr (BETA && Z0 && SV > 0) {                                                      \
     if (a.pz.zs) {                                                                           \
       update_kernel<SV, BETA, XR, Z0, true><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a)); \
       break;                                                                                 \

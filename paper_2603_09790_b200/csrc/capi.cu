@@ -495,9 +495,14 @@ int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
       run = [&, k] { launch_spmv(k, p->view(), g, 0, p->nslices, c->stream); };
     } else if (kind == 3) {
       unsigned* ticket = reinterpret_cast<unsigned*>(sm + 4 * S * S + 2048);
-      run = [&, ticket] {
+      PzArgs pz;
+      if (std::getenv("CS_BENCH_PZ")) {
+        pz.zs = v + 2 * S * ld;
+        pz.sig1 = 1.0, pz.sig2 = 2.0, pz.k1 = 0.5, pz.k2 = 0.25, pz.dconst = 26.0;
+      }
+      run = [&, ticket, pz] {
         launch_pack(S, n, ld, v, v + S * ld, v + 2 * S * ld, v + 3 * S * ld, sm, part.as<double>(),
-                    ticket, nullptr, nullptr, c->stream);
+                    ticket, nullptr, nullptr, c->stream, pz);
       };
     } else {
       ua.s = S;
@@ -514,6 +519,11 @@ int cs_bench_spmv(cs_problem* p, int kind, int reps, double* ms_per_launch) {
       ua.alpha = sm;
       ua.beta = sm + S;
       ua.st = c->state.as<DevState>();
+      if (std::getenv("CS_BENCH_PZ")) {  // the PZ schedule's pass (P derived from Z)
+        ua.pz.zs = v + 3 * S * ld;
+        ua.pz.sig1 = 1.0, ua.pz.sig2 = 2.0, ua.pz.k1 = 0.5, ua.pz.k2 = 0.25, ua.pz.dconst = 26.0;
+        ua.inv_const = 1.0 / 26.0;
+      }
       CS_CUDA(cudaMemsetAsync(c->state.p, 0, sizeof(DevState), c->stream));
       run = [&] { launch_fast_update(ua, c->stream); };
     }

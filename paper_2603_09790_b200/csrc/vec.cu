@@ -457,6 +457,12 @@ __device__ __forceinline__ void p_row_from_z(const UpdateArgs& a, const Cols<S>&
   p_from_z<S>(zz, a.pz, a.pz.diag ? a.pz.diag[i] : a.pz.dconst, p);
 }
 
+#ifndef CS_UPD_FMA
+#define CS_UPD_FMA 1  // fast pass: one FMA per term (0: separate mul / add as the reference)
+#endif
+#ifndef CS_UPD_PAIRED
+#define CS_UPD_PAIRED 1  // Q/AQ roles of a row in one warp (0: block halves + block barrier)
+#endif
 // Lanes 0-15 of a warp take the Q role of 16 rows, lanes 16-31 the AQ role of
 // the SAME rows (each load instruction moves two full 128-byte segments). The
 // AQ role overwrites Z column 0 with z_0 = M^-1 r, which the Q role of its row
@@ -476,8 +482,10 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
     for (int t = threadIdx.x; t < s * s; t += blockDim.x) sh_beta[t] = a.beta[t];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const bool aq_role = lane >= 16;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * kUpdRows + (threadIdx.x >> 5) * 16 + (lane & 15);
+  const bool aq_role = CS_UPD_PAIRED ? lane >= 16 : threadIdx.x >= kUpdRows;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kUpdRows +
+                    (CS_UPD_PAIRED ? (threadIdx.x >> 5) * 16 + (lane & 15)
+                                   : (threadIdx.x & (kUpdRows - 1)));
   const bool active = i < a.n;
   double* const* dst = aq_role ? c.aq : c.q;      // updated in place
   const double* const* src = aq_role ? c.p : c.z; // new basis part
@@ -500,14 +508,18 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
         d_i = a.pz.diag ? a.pz.diag[i] : a.pz.dconst;
       }
   }
-  if constexpr (PZ) {  // every lane: the Q lane's Z row to its AQ lane
+  if constexpr (PZ && CS_UPD_PAIRED) {  // every lane: the Q lane's Z row to its AQ lane
     double zz[SM + 1];
 #pragma unroll
     for (int q = 0; q < SM; ++q) zz[q] = __shfl_xor_sync(0xffffffffu, hi[q], 16);
     zz[SM] = zs_i;
     if (aq_role) p_from_z<SM>(zz, a.pz, d_i, hi);
+  } else if constexpr (PZ) {
+    if (aq_role && active) p_row_from_z<SM>(a, c, i, hi);
+    __syncthreads();
   } else if constexpr (Z0) {
-    __syncwarp();
+    if (CS_UPD_PAIRED) __syncwarp();
+    else __syncthreads();
   }
   if (!active) return;  if constexpr (BETA) {
     // out_j = y_j + sum_q c_qj x_q, ascending q for every j (dense_ops.cpp:35-39);
@@ -519,7 +531,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
 #pragma unroll
         for (int j = 0; j < SM; ++j)
           if (j < s) {
-            if constexpr (Z0) hi[j] = fma(sh_beta[q + j * s], xq, hi[j]);
+            if constexpr (Z0 && CS_UPD_FMA) hi[j] = fma(sh_beta[q + j * s], xq, hi[j]);
             else hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * s], xq));
           }
       }
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(UpdateArgs a, Cols<(S 
 #pragma unroll
     for (int j = 0; j < SM; ++j)
       if (j < s) {
-        if constexpr (Z0) acc = fma(sign * sh_alpha[j], BETA ? hi[j] : lo[j], acc);
+        if constexpr (Z0 && CS_UPD_FMA) acc = fma(sign * sh_alpha[j], BETA ? hi[j] : lo[j], acc);
         else acc = __dadd_rn(acc, __dmul_rn(sign * sh_alpha[j], BETA ? hi[j] : lo[j]));
       }
     if (aq_role) a.r[i] = acc;

@@ -38,6 +38,8 @@ for step in "$@"; do
           -o $out/${tag}_$nm python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg \
           > $out/${tag}_ncu_$nm.log 2>&1
       done ;;
+    updsweep)
+      timeout 900 bash tools/upd_sweep.sh > $out/${tag}_updsweep.txt 2>&1 ;;
     boxsweep)
       timeout 900 bash tools/box_sweep.sh > $out/${tag}_boxsweep.txt 2>&1 ;;
     bench)

@@ -18,7 +18,8 @@ res = {}
 print(f"format: slices={p.slices} pattern={p.pattern_slices} uniform={p.uniform_slices} "
       f"table_entries={p.pattern_entries} bytes={mat}")
 for kind, byts in (("plain", mat + 2 * v), ("mpk_ref", mat + 7 * v), ("mpk_fast", mat + 5 * v),
-                   ("pack8", 25 * v), ("update8", 54 * v)):
+                   ("pack8", (18 if os.environ.get("CS_BENCH_PZ") else 25) * v),
+                   ("update8", (45 if os.environ.get("CS_BENCH_PZ") else 54) * v)):
     if kind not in a.kinds.split(","):
         continue
     ms = p.bench_spmv(kind, a.reps)

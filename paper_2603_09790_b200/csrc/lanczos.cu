@@ -178,6 +178,125 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// ---- G-only Lanczos (fast mode, diagonal M = D: identity or Jacobi). The M
+// inner-product pairs satisfy v = D^-1 g and r = D^-1 gr exactly in exact
+// arithmetic, so only the g_j are stored (half the basis: 43 GB at 512^3) and
+// v, r are formed per row where needed (dinv: a_ii^-1 vector, or the uniform
+// constant dconst when dinv is null).
+
+// gr = t - a g_j - b g_{j-1} (spectral.cpp:93-102 on the g side), written, and
+// in the same pass proj_i = g_i . (D^-1 gr) for i < m = j + 1
+template <int MB>
+__global__ void __launch_bounds__(kThreads)
+    lz2_resid_proj_kernel(int64_t n, int64_t ld, int m, const double* __restrict__ t,
+                          const double* __restrict__ G, const double* __restrict__ dinv,
+                          double dconst, double* gr, const LanczosScalars* sc, int j,
+                          double* proj, double* partial, unsigned* ticket, DevState* st) {
+  if (halted(st)) return;
+  __shared__ double red[MB][kThreads / 32];
+  __shared__ bool last;
+  const double a = sc->alpha[j], b = j > 0 ? sc->beta[j - 1] : 0.0;
+  double acc[MB];
+#pragma unroll
+  for (int c = 0; c < MB; ++c) acc[c] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    double gv = fma(-a, __ldg(G + j * ld + i), __ldcs(t + i));
+    if (j > 0) gv = fma(-b, __ldg(G + (j - 1) * ld + i), gv);
+    gr[i] = gv;
+    const double rv = gv * (dinv ? __ldg(dinv + i) : dconst);
+#pragma unroll
+    for (int c = 0; c < MB; ++c)
+      if (c < m) acc[c] = fma(__ldcs(G + c * ld + i), rv, acc[c]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < MB; ++c) {
+    if (c < m) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], off);
+      if (lane == 0) red[c][warp] = acc[c];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < m; c += kThreads) {
+    double sum = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) sum += red[c][w];
+    partial[static_cast<int64_t>(blockIdx.x) * m + c] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_partials(partial, gridDim.x, m, proj);
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// gr -= sum_i proj_i g_i (8-pair chunks), fused with the dot (D^-1 gr) . gr
+__global__ void __launch_bounds__(kThreads)
+    lz2_cgs_kernel(int64_t n, int64_t ld, int m, const double* __restrict__ G,
+                   const double* __restrict__ dinv, double dconst, double* gr, const double* proj,
+                   double* partial, unsigned* ticket, double* result, DevState* st) {
+  if (halted(st)) return;
+  __shared__ double sp[kLanczosMax];
+  __shared__ double red[kThreads / 32];
+  __shared__ bool last;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) sp[t] = proj[t];
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double d = 0.0;
+  if (i < n) {
+    double gv = gr[i];
+    constexpr int kC = 8;
+#pragma unroll 1
+    for (int c0 = 0; c0 < m; c0 += kC) {
+      double gg[kC];
+#pragma unroll
+      for (int c = 0; c < kC; ++c)
+        if (c0 + c < m) gg[c] = __ldcs(G + (c0 + c) * ld + i);
+#pragma unroll
+      for (int c = 0; c < kC; ++c)
+        if (c0 + c < m) gv = fma(-sp[c0 + c], gg[c], gv);
+    }
+    gr[i] = gv;
+    d = gv * (dinv ? __ldg(dinv + i) : dconst) * gv;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) d += __shfl_down_sync(0xffffffffu, d, off);
+  if (lane == 0) red[warp] = d;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) sum += red[w];
+    partial[blockIdx.x] = sum;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    finalize_partials(partial, gridDim.x, 1, result);
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+}
+
+// g_{j+1} = gr / beta_j, v = D^-1 g_{j+1}
+__global__ void lz2_scale_kernel(int64_t n, const double* __restrict__ gr,
+                                 const double* __restrict__ dinv, double dconst, double* g,
+                                 double* v, const LanczosScalars* sc, DevState* st) {
+  if (halted(st)) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double gv = __ddiv_rn(gr[i], sc->denom);
+  g[i] = gv;
+  v[i] = gv * (dinv ? dinv[i] : dconst);
+}
+
 // scalar steps: 0 normalise start (nrm = sqrt(v.g) > 0), 1 alpha_j (finite),
 // 2 beta_j = sqrt(max(0, r.gr)) with the invariant-subspace exit.
 __global__ void scalar_kernel(int which, int j, int steps, LanczosScalars* sc, DevState* st) {
@@ -252,6 +371,36 @@ void lz_cgs(int64_t n, int64_t ld, int m, const double* V, const double* G, doub
   else if (m <= 40) CSG_CGS(40);
   else CSG_CGS(0);
 #undef CSG_CGS
+  CS_CUDA(cudaGetLastError());
+}
+
+void lz2_resid_proj(int64_t n, int64_t ld, int m, const double* t, const double* G,
+                    const double* dinv, double dconst, double* gr, const LanczosScalars* sc, int j,
+                    double* proj, double* partial, unsigned* ticket, DevState* st, cudaStream_t s) {
+#define CSG_RP(MB)                                                                             \
+  lz2_resid_proj_kernel<MB><<<kProjBlocks, kThreads, 0, s>>>(n, ld, m, t, G, dinv, dconst, gr, \
+                                                             sc, j, proj, partial, ticket, st)
+  if (m <= 8) CSG_RP(8);
+  else if (m <= 16) CSG_RP(16);
+  else if (m <= 24) CSG_RP(24);
+  else if (m <= 32) CSG_RP(32);
+  else CSG_RP(40);
+#undef CSG_RP
+  CS_CUDA(cudaGetLastError());
+}
+
+void lz2_cgs(int64_t n, int64_t ld, int m, const double* G, const double* dinv, double dconst,
+             double* gr, const double* proj, double* partial, unsigned* ticket, double* result,
+             DevState* st, cudaStream_t s) {
+  lz2_cgs_kernel<<<grid_for(n > 0 ? n : 1), kThreads, 0, s>>>(n, ld, m, G, dinv, dconst, gr, proj,
+                                                             partial, ticket, result, st);
+  CS_CUDA(cudaGetLastError());
+}
+
+void lz2_scale(int64_t n, const double* gr, const double* dinv, double dconst, double* g, double* v,
+               const LanczosScalars* sc, DevState* st, cudaStream_t s) {
+  if (n == 0) return;
+  lz2_scale_kernel<<<grid_for(n), kThreads, 0, s>>>(n, gr, dinv, dconst, g, v, sc, st);
   CS_CUDA(cudaGetLastError());
 }
 

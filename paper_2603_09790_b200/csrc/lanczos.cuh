@@ -31,6 +31,16 @@ bool lz_proj_supported(int m);
 size_t lz_proj_partial_doubles(int m);
 void lz_proj(int64_t n, int64_t ld, int m, const double* G, const double* r, double* proj,
              double* partial, unsigned* ticket, DevState* st, cudaStream_t s);
+// G-only fast Lanczos for diagonal M (v = D^-1 g, r = D^-1 gr never stored);
+// dinv = a_ii^-1 vector or nullptr with the uniform dconst (1 for identity)
+void lz2_resid_proj(int64_t n, int64_t ld, int m, const double* t, const double* G,
+                    const double* dinv, double dconst, double* gr, const LanczosScalars* sc, int j,
+                    double* proj, double* partial, unsigned* ticket, DevState* st, cudaStream_t s);
+void lz2_cgs(int64_t n, int64_t ld, int m, const double* G, const double* dinv, double dconst,
+             double* gr, const double* proj, double* partial, unsigned* ticket, double* result,
+             DevState* st, cudaStream_t s);
+void lz2_scale(int64_t n, const double* gr, const double* dinv, double dconst, double* g, double* v,
+               const LanczosScalars* sc, DevState* st, cudaStream_t s);
 void lz_scalar(int which, int j, int steps, LanczosScalars* sc, DevState* st, cudaStream_t s);
 
 // host: eigenvalues of the symmetric tridiagonal (d[m], e[m-1]) ascending

@@ -458,7 +458,7 @@ __device__ __forceinline__ void p_row_from_z(const UpdateArgs& a, const Cols<S>&
 }
 
 #ifndef CS_UPD_FMA
-#define CS_UPD_FMA 1  // fast pass: one FMA per term (0: separate mul / add as the reference)
+#define CS_UPD_FMA 0  // 1: one FMA per term in the fast pass (measured slower: profiles/r02_update_pack_sweep.txt)
 #endif
 #ifndef CS_UPD_PAIRED
 #define CS_UPD_PAIRED 1  // Q/AQ roles of a row in one warp (0: block halves + block barrier)

@@ -1169,6 +1169,7 @@ cs_problem* problem_upload_block(cs_ctx* c, int64_t n_global, int64_t row_begin,
   if (nnz < 0) fail(CS_ERR_INVALID_MATRIX, 0, "row_offsets[n] must equal nnz");
   CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
+  NvtxRange nvtx_("cs:upload CSR (streamed) + SELL/CDIA conversion");
   UploadTrace ut(c->stream);
   auto p = std::make_unique<cs_problem>();
   p->attach(c);

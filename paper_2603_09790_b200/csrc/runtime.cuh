@@ -5,6 +5,7 @@
 #pragma once
 #include <atomic>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <array>
 #include <cstdlib>
@@ -212,6 +213,15 @@ struct cs_problem {
 namespace csg {
 
 // launch accounting + optional CUDA-event timing of every kernel
+// NVTX range for Nsight timelines (header-only NVTX v3: no link dependency,
+// a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct Launch {
   cs_ctx* c;
   int phase;

@@ -111,6 +111,7 @@ double host_norm(cs_problem* p, const double* v, int mode) {
 void estimate_interval_dev(cs_problem* p, int steps, uint64_t seed, int mode, double* lo,
                            double* hi, double* t_ms) {
   cs_ctx* c = p->ctx;
+  NvtxRange nvtx_("cs:estimate_interval (Lanczos)");
   if (steps < 2) fail(CS_ERR_INVALID_ARGUMENT, 0, "estimate_interval: steps >= 2");
   if (steps > kLanczosMax) fail(CS_ERR_INVALID_ARGUMENT, 0, "estimate_interval: steps > 256");
   if (mode == CS_MODE_REFERENCE && c->nranks > 1)
@@ -597,6 +598,7 @@ struct SolveTrace {
 void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
                     const cs_config& cfg, double* x_dev, cs_report* rep) {
   cs_ctx* c = p->ctx;
+  NvtxRange nvtx_("cs:pcg_s_solve");
   CS_CUDA(cudaSetDevice(c->device));
   StreamBind bind_stream_(c->stream);
   // SolverConfig::validate, solver.cpp:15-22
@@ -917,6 +919,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
                          !hooks.any();
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
+  NvtxRange nvtx_loop("cs:outer iterations");
   for (; issued < cfg.max_outer;) {
     if (use_graph && issued > 0 && issued + batch <= cfg.max_outer) {
       if (gexec == nullptr) {

@@ -40,6 +40,13 @@ for step in "$@"; do
       done ;;
     updsweep)
       timeout 900 bash tools/upd_sweep.sh > $out/${tag}_updsweep.txt 2>&1 ;;
+    lzprobe)
+      { python tools/lz_probe.py 256 3; CS_LZ_GONLY=0 python tools/lz_probe.py 256 3;
+        python tools/lz_probe.py 512 2; CS_LZ_GONLY=0 python tools/lz_probe.py 512 2;
+        timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+          --log-file $out/${tag}_lz_launches.csv python tools/lz_probe.py 256 1;
+        CS_LZ_GONLY=0 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+          --log-file $out/${tag}_lz_launches_vg.csv python tools/lz_probe.py 256 1; } > $out/${tag}_lzprobe.txt 2>&1 ;;
     boxsweep)
       timeout 900 bash tools/box_sweep.sh > $out/${tag}_boxsweep.txt 2>&1 ;;
     bench)

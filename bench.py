@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
+    ap.add_argument("--variant", type=int, default=0, help="CS_VAR_* bits (A/B runs)")
     return ap.parse_args()
 
 
@@ -314,7 +315,7 @@ def run_ours(args):
     x0 = torch.zeros(nl, dtype=torch.float64, device=dev)
     x = torch.empty(nl, dtype=torch.float64, device=dev)
     cfg = cs.SolverConfig(s=args.s, tol=args.tol, max_outer=50000, fgs=cs.FgsConfig(nu=args.nu),
-                          mode=args.mode)
+                          mode=args.mode, variant=args.variant)
     torch.cuda.synchronize()
 
     def step():
@@ -509,7 +510,7 @@ def e2e(args, cs, ctx, prob, world, torch):
     import numpy as np
     nl, ng = prob.n_local, prob.n_global
     cfg = cs.SolverConfig(s=args.s, tol=args.tol, max_outer=50000, fgs=cs.FgsConfig(nu=args.nu),
-                          mode=args.mode)
+                          mode=args.mode, variant=args.variant)
     nnz = prob.nnz_local
     csr_bytes = 8 * (nl + 1) + 16 * nnz
     avail = host_mem_available()

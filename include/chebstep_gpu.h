@@ -120,6 +120,9 @@ typedef struct {
 #define CS_VAR_P_FROM_Z 32    /* fast: P columns derived from Z (no P stream) --
                                  the default wherever it applies; the bit is accepted */
 #define CS_VAR_P_STORED 64    /* fast: the stored-P schedule (round-1 default) */
+#define CS_VAR_TRUE_R 128     /* fast, PZ schedule: r_{k+1} = b - A x_{k+1} from one residual
+                                 SpMV instead of r_k - AQ alpha (no AQ block) */
+#define CS_VAR_RECUR_R 256    /* fast: force the recursive residual (AQ block) */
 
 typedef struct {
   /* SolveReport (solver.hpp:39-68), reference semantics */
@@ -151,6 +154,7 @@ typedef struct {
 /* cs_report.schedule bits */
 #define CS_SCHED_P_FROM_Z 1   /* P derived from Z (no P stream) */
 #define CS_SCHED_EXPLICIT_W 2 /* W_k reduced from the vectors each outer */
+#define CS_SCHED_TRUE_R 4     /* r from b - A x each outer (no AQ block) */
 
 /* ------------------------------------------------------------ errors / info */
 const char* cs_last_error(int* payload);

@@ -95,7 +95,10 @@ void launch_inv_diag(int64_t n, const double* diag, double* inv_diag, int* bad, 
 enum SpmvKind {
   kPlain = 0, kResid = 1, kMpkFirst = 2, kMpkMid = 3, kMpkLast = 4, kDot = 5,
   // fast algebra: z_q = ca*D^-1 p_q + cb*z_{q-1} + cc*z_{q-2}, no zp vectors, D from the row
-  kMpkFirstF = 6, kMpkMidF = 7
+  kMpkFirstF = 6, kMpkMidF = 7,
+  // true-residual schedule (CS_VAR_TRUE_R): r = b - A x and z_0 = M^-1 r in one
+  // pass (breakdown check on z_0 as basis column 0, NVLink push of z_0)
+  kResidF = 8
 };
 struct SpmvArgs {
   const double* x = nullptr;   // operand (owned + ghost slots)
@@ -223,6 +226,10 @@ struct UpdateArgs {
   PzArgs pz;  // pz.zs != nullptr: P derived from Z (p unused)
 };
 void launch_fast_update(const UpdateArgs& a, cudaStream_t s);  // beta block update + x/r + z0
+// true-residual schedule: Q <- Z + Q beta (beta != nullptr), x += Q alpha; no AQ
+// block, no r (the next residual SpMV forms r and z_0); push_* carry x's rows.
+// false: s has no specialised order (nothing launched).
+bool launch_fast_update_tr(const UpdateArgs& a, cudaStream_t s);
 // The same beta pass fused with the explicit Gram W = Q_new^T AQ_new of the
 // vectors it writes (raw, unsymmetrised s x s into wout via per-block partials
 // and last-block finalisation). false: s not supported, nothing launched.

@@ -730,6 +730,10 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   // and update passes, z_s in the (otherwise unused) P block's first column
   const bool pz_on = mode == CS_MODE_FAST && fast_mpk && !general_pc && use_pack &&
                      update_gram_supported(s) && (var & CS_VAR_P_STORED) == 0;
+  // true-residual schedule: r_{k+1} = b - A x_{k+1} (+ z_0) in one residual SpMV,
+  // the update pass keeps only Q and x (no AQ block, no recursive r)
+  const bool tr_on = pz_on && !explicit_w && (var & CS_VAR_TRUE_R) != 0 &&
+                     (var & CS_VAR_RECUR_R) == 0;
   PzArgs pz;
   if (pz_on) {
     const double alpha = 2.0 / (hi - lo), sigma = (hi + lo) / (hi - lo);  // mpk.hpp:22-25
@@ -772,6 +776,12 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   auto update_pass = [&](bool first) {
     ua.beta = first ? nullptr : beta_d;
     sa.Wexp = explicit_w && !first ? raw + off_w : nullptr;  // outer 1: W_1 is explicit already
+    if (tr_on) {
+      Launch L(c, CS_PHASE_UPDATE);
+      if (!launch_fast_update_tr(ua, c->stream))
+        fail(CS_ERR_INVALID_ARGUMENT, 0, "true-residual schedule: unsupported s");
+      return;
+    }
     {
       Launch L(c, CS_PHASE_UPDATE);
       if (!(sa.Wexp && launch_fast_update_gram(ua, partial, ticket + 4, raw + off_w, c->stream))) {
@@ -834,18 +844,35 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   // producing kernels (no NCCL on the SpMV path); collective, every rank calls it
   const bool p2p = mode == CS_MODE_FAST && fast_mpk && !general_pc && !hooks.any() &&
                    c->nranks > 1 && p2p_setup(p, bk.Z);
+  // x's column in the workspace, counted in ld strides from Z (the same on every
+  // rank): where the true-residual update pushes x's boundary rows
+  const int x_col = static_cast<int>((bk.x - bk.Z) / ld);
+  // r_k = b - A x_k and z_0 = M^-1 r_k in one SpMV (true-residual schedule)
+  auto residual_z0 = [&](bool peer) {
+    SpmvArgs g;
+    g.x = bk.x;
+    g.y = bk.r;
+    g.b = bk.b;
+    g.zout = bk.Z;
+    g.col = 0;
+    g.pending = 1;
+    g.st = st;
+    if (peer) spmv_p2p(p, kResidF, g, 0);  // z_0's boundary rows to the neighbours
+    else spmv_halo(p, kResidF, g, bk.x);
+  };
   auto outer_fast = [&](bool first) {
     ua.zw = general_pc ? bk.zpA : bk.Z;  // z_0 = M^-1 r_k for the next MPK
-    if (p2p) {  // z_0's boundary rows go to the neighbours from the update pass itself
+    if (p2p) {  // z_0's (true residual: x's) boundary rows go to the neighbours from the update pass
       SpmvArgs pa;
-      fill_push_args(p, pa, 0);
+      fill_push_args(p, pa, tr_on ? x_col : 0);
       ua.push_lo = pa.push_lo;
       ua.push_hi = pa.push_hi;
       ua.send_lo = pa.send_lo;
       ua.hi_begin = pa.hi_begin;
     }
     update_pass(first);
-    if (p2p) p->p2p_pending = true;  // released by the first MPK step's interior launch
+    if (p2p) p->p2p_pending = true;  // released by the next SpMV's interior launch
+    if (tr_on) residual_z0(p2p);
     mpk_steps(p, bk, s, lo, hi, /*pending=*/1, st, fast_mpk, p2p, pz_on ? bk.P : nullptr);
     packed_reduce(bk.Q, bk.Z, pz);
     small(launch_fast_step);
@@ -887,6 +914,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
       if (mode == CS_MODE_FAST) {
         ua.zw = general_pc ? bk.zpA : bk.Z;
         update_pass(k == 1);
+        if (tr_on) residual_z0(false);
         if (read_state(c).done) break;
         hooks.record_gram(W);  // W_k (the one this outer's alpha was solved with)
         hooks.record_x(bk.x);
@@ -998,7 +1026,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   rep->kernel_launches = c->launches - launches0;
   rep->t_lanczos_ms = t_lz;
   rep->t_solve_ms = t_solve;
-  rep->schedule = (pz_on ? CS_SCHED_P_FROM_Z : 0) | (explicit_w ? CS_SCHED_EXPLICIT_W : 0);
+  rep->schedule = (pz_on ? CS_SCHED_P_FROM_Z : 0) | (explicit_w ? CS_SCHED_EXPLICIT_W : 0) |
+                  (tr_on ? CS_SCHED_TRUE_R : 0);
   trace.mark("report");
 }
 

@@ -217,6 +217,10 @@ __device__ __forceinline__ EpiOps epi_load(const SellView& a, const SpmvArgs& g,
                                            double cinv = 0.0) {
   EpiOps e;
   if constexpr (KIND == kResid) e.e1 = g.b[row];
+  if constexpr (KIND == kResidF) {
+    e.e1 = g.b[row];
+    if constexpr (JAC) e.einv = cinv != 0.0 ? cinv : a.inv_diag[row];
+  }
   if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
     e.e1 = g.zp1[row];
     if constexpr (KIND == kMpkMid) e.e2 = g.zp2[row];
@@ -238,6 +242,13 @@ __device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double
     g.y[row] = acc;
   } else if constexpr (KIND == kResid) {
     g.y[row] = __dsub_rn(e.e1, acc);
+  } else if constexpr (KIND == kResidF) {
+    const double r = e.e1 - acc;
+    g.y[row] = r;
+    const double z = JAC ? r * e.einv : r;
+    g.zout[row] = z;
+    zv = z;
+    if (!isfinite(z)) report(g, g.col);
   } else if constexpr (KIND == kMpkFirst || KIND == kMpkMid) {
     g.y[row] = acc;
     const double y2 = (KIND == kMpkFirst) ? e.e1 : e.e2;
@@ -376,7 +387,7 @@ __global__ void __launch_bounds__(kWarps * 32, CDN != 0 ? CS_SPMV_CD_MINB : CS_S
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
-  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
   constexpr bool CD = CDN != 0;
   __shared__ SlotRec stab[CD ? 1 : kStabMax];
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(kWarps * 32, CS_SPMV_ZB_MINB)
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wstride = static_cast<int64_t>(gridDim.x) * kWarps;
-  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
   const int P = static_cast<int>(sp * kSliceRows);
   const double* __restrict__ x = g.x;
@@ -815,7 +826,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     __syncthreads();
   }
   constexpr bool kE2 = KIND == kMpkMidF;
-  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF;
   constexpr int R = CS_BOX_ROWS;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
   extern __shared__ __align__(128) unsigned char box_smem[];
@@ -873,7 +884,8 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     const int lim_k = k < m1 ? max(0, min(width, R1 - rbk)) : 0;
     const int lim_1 = k - 1 >= m0 && k - 1 < m1 ? max(0, min(width, R1 - rb1)) : 0;
     const int lim_2 = k - 2 >= m0 ? max(0, min(width, end2 - rb2)) : 0;
-    constexpr bool kSepKind = NEG1 && (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot);
+    constexpr bool kSepKind =
+        NEG1 && (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot || KIND == kResidF);
     uint32_t bk[R], mk[R];
     double acc0[R], acc1[R], acc2[R], cen[R];
     if (kSepKind && b.sep) {
@@ -938,7 +950,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
         eo.exd = cen2[j];
         eo.einv = JAC ? t.inv : 1.0;
         if constexpr (kE2) eo.e2 = zs[i];
-        if constexpr (KIND == kResid) eo.e1 = g.b[r2];
+        if constexpr (KIND == kResid || KIND == kResidF) eo.e1 = g.b[r2];
         double zv = 0.0;
         epi_store<KIND, JAC>(g, r2, acc2[j], eo, dotv, zv);
         if constexpr (kPush)
@@ -993,7 +1005,7 @@ bool box_enabled() {
 
 constexpr bool box_kind(int kind) {
   return kind == kPlain || kind == kResid || kind == kMpkFirstF || kind == kMpkMidF ||
-         kind == kMpkLast || kind == kDot;
+         kind == kMpkLast || kind == kDot || kind == kResidF;
 }
 
 // Plane-streaming launch over the class rows [lo, hi) * 32; false: not applicable.
@@ -1032,7 +1044,7 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
     const char* sep_e = std::getenv("CS_BOX_SEP");  // per launch, like CS_SPMV_BOX
     const bool sep_env = sep_e == nullptr || std::atoi(sep_e) != 0;
     b.sep = sep_env && neg1 && cl.geo &&
-            (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot);
+            (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot || KIND == kResidF);
     b.dp1 = t.v[13] + 1.0;
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(
@@ -1164,6 +1176,7 @@ void launch_spmv(int kind, const SellView& a, const SpmvArgs& g, int64_t sb, int
     case kDot: launch_kind<kDot>(false, a, g, sb, se, st); break;
     case kMpkFirstF: launch_kind<kMpkFirstF>(jac, a, g, sb, se, st); break;
     case kMpkMidF: launch_kind<kMpkMidF>(jac, a, g, sb, se, st); break;
+    case kResidF: launch_kind<kResidF>(jac, a, g, sb, se, st); break;
     default: throw LibError{9, 0, "bad spmv kind"};
   }
   CS_CUDA(cudaGetLastError());

@@ -725,6 +725,45 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// True-residual schedule (CS_VAR_TRUE_R): the pass keeps only the
+// Q role -- Q_j <- Z_j + sum_q beta_qj Q_q, x <- x + sum_j alpha_j Q_j, in the
+// fast pass's operation order -- and no AQ block or recursive r: the next
+// launch forms r = b - A x and z_0 = M^-1 r (kResidF). One row per thread;
+// x's boundary rows go to the neighbours' ghost slots for that residual.
+// Bytes per row: 8 (3s + 2) instead of 8 (5s + 6).
+template <int S, bool BETA>
+__global__ void __launch_bounds__(kThreads) update_tr_kernel(UpdateArgs a, Cols<S> c) {
+  if (halted(a.st)) return;
+  __shared__ double sh_alpha[S];
+  __shared__ double sh_beta[BETA ? S * S : 1];
+  for (int t = threadIdx.x; t < S; t += blockDim.x) sh_alpha[t] = a.alpha[t];
+  if constexpr (BETA)
+    for (int t = threadIdx.x; t < S * S; t += blockDim.x) sh_beta[t] = a.beta[t];
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  if (i >= a.n) return;
+  double acc = a.x[i];
+  double lo[S], hi[S];
+#pragma unroll
+  for (int q = 0; q < S; ++q) {
+    lo[q] = c.q[q][i];
+    if constexpr (BETA) hi[q] = c.z[q][i];
+  }
+  if constexpr (BETA) {
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+#pragma unroll
+      for (int j = 0; j < S; ++j) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * S], lo[q]));
+#pragma unroll
+    for (int j = 0; j < S; ++j) c.q[j][i] = hi[j];
+  }
+#pragma unroll
+  for (int j = 0; j < S; ++j) acc = __dadd_rn(acc, __dmul_rn(sh_alpha[j], BETA ? hi[j] : lo[j]));
+  a.x[i] = acc;
+  if (a.push_lo != nullptr && i < a.send_lo) a.push_lo[i] = acc;
+  if (a.push_hi != nullptr && i >= a.hi_begin) a.push_hi[i - a.hi_begin] = acc;
+}
+
 template <int S>
 Cols<S> make_cols(const UpdateArgs& a) {
   Cols<S> c{};
@@ -1015,6 +1054,24 @@ void launch_fast_update(const UpdateArgs& a, cudaStream_t s) {
     update_dispatch<true, true, true>(a, s);
   else
     update_dispatch<false, true, true>(a, s);
+}
+
+bool launch_fast_update_tr(const UpdateArgs& a, cudaStream_t st) {
+  if (a.n == 0) return true;
+  const unsigned grid = grid_for(a.n);
+#define CSG_TR(SV)                                                                          \
+  case SV:                                                                                  \
+    if (a.beta) update_tr_kernel<SV, true><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a)); \
+    else update_tr_kernel<SV, false><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a));       \
+    break
+  switch (a.s) {
+    CSG_TR(1); CSG_TR(2); CSG_TR(3); CSG_TR(4); CSG_TR(5); CSG_TR(6); CSG_TR(8);
+    CSG_TR(10); CSG_TR(12); CSG_TR(16);
+    default: return false;
+  }
+#undef CSG_TR
+  CS_CUDA(cudaGetLastError());
+  return true;
 }
 
 void launch_ref_xr_update(const UpdateArgs& a, cudaStream_t s) {

@@ -21,18 +21,22 @@ def _gpus():
         return 0
 
 
-@pytest.mark.parametrize("stencil,n,nz,mm", [("poisson27", 40, 48, False),
-                                             ("poisson7", 32, 40, False),
-                                             ("poisson27", 24, 32, True)])
-def test_multi_gpu_parity(stencil, n, nz, mm, tmp_path):
+@pytest.mark.parametrize("stencil,n,nz,mm,variant", [("poisson27", 40, 48, False, 256),
+                                                     ("poisson27", 40, 48, False, 128),
+                                                     ("poisson7", 32, 40, False, 0),
+                                                     ("poisson27", 24, 32, True, 0)])
+def test_multi_gpu_parity(stencil, n, nz, mm, variant, tmp_path):
+    """variant 256 / 128: the recursive / true-residual fast schedule (the true
+    residual moves x's boundary planes by peer stores from the update pass and
+    z_0's from the residual SpMV)."""
     ng = _gpus()
     if ng < 2:
         pytest.skip("needs >= 2 GPUs")
     world = ng  # every GPU of the box (2, 4 or 8 ranks)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + 7 * mm),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + 7 * mm + variant % 7),
            os.path.join(ROOT, "tools", "mgpu_check.py"), "--grid", str(n), "--nz", str(nz),
-           "--stencil", stencil] + (["--mm"] if mm else [])
+           "--stencil", stencil, "--variant", str(variant)] + (["--mm"] if mm else [])
     env = dict(os.environ, MGPU_TMP=str(tmp_path))
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     line = [l for l in out.stdout.splitlines() if l.startswith("MGPU ")]

@@ -92,13 +92,19 @@ FAST_CASES = [
 ]
 
 
+# fast schedules: the recursive residual r_k - AQ alpha (AQ block kept) and the
+# true residual b - A x_k from one SpMV per outer (no AQ block)
+VARIANTS = [("recursive_r", 256), ("true_r", 128)]
+
+
+@pytest.mark.parametrize("variant", [v[1] for v in VARIANTS], ids=[v[0] for v in VARIANTS])
 @pytest.mark.parametrize("case", FAST_CASES, ids=lambda c: "-".join(map(str, c)))
-def test_pcgs_fast_mode_parity(cs, port, case):
+def test_pcgs_fast_mode_parity(cs, port, case, variant):
     name, s, nu, gram = case
     o = _problem(port, name)
     x_o, r_o = port.pcg_s_solve(o, s=s, nu=nu, gram=gram, tol=1e-8, max_outer=5000)
     cfg = cs.SolverConfig(s=s, tol=1e-8, max_outer=5000, fgs=cs.FgsConfig(nu=nu),
-                          gram_solver=cs.GramSolverKind[gram], mode="fast")
+                          gram_solver=cs.GramSolverKind[gram], mode="fast", variant=variant)
     res = cs.pcg_s_solve(_csr(cs, o), np.ones(o.n), np.zeros(o.n),
                          cs.JacobiPreconditioner(_csr(cs, o)), cfg)
     rep = res.report
@@ -266,13 +272,15 @@ GOLDEN_FAST = [("p27:96:8", 27, 96, 8), ("p27:128:8", 27, 128, 8), ("p27:128:4",
                ("p7:256:4", 7, 256, 4)]
 
 
+@pytest.mark.parametrize("variant", [v[1] for v in VARIANTS], ids=[v[0] for v in VARIANTS])
 @pytest.mark.parametrize("case,stencil,n,s", GOLDEN_FAST, ids=[c[0] for c in GOLDEN_FAST])
-def test_fast_mode_vs_golden_counts(cs, case, stencil, n, s):
+def test_fast_mode_vs_golden_counts(cs, case, stencil, n, s, variant):
     g = _golden(f"p{stencil}_{n}x{n}x{n}_s{s}_nu30_jacobi_1e-08")
     lo, hi = _band(case)
     p = cs.DeviceProblem.generate("poisson27" if stencil == 27 else "poisson7", n, n, n)
     p.set_precond("jacobi")
-    res = p.pcg_s_solve(cfg=cs.SolverConfig(s=s, tol=1e-8, max_outer=5000))
+    res = p.pcg_s_solve(cfg=cs.SolverConfig(s=s, tol=1e-8, max_outer=5000, variant=variant))
+    assert bool(res.report.schedule & 4) == (variant == 128)  # CS_SCHED_TRUE_R
     rep = res.report
     assert rep.converged
     if lo == hi:
@@ -295,8 +303,9 @@ def test_fast_mode_x_vs_reference_x(cs, case, n):
     ref = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=5000, mode="reference",
                                             spectrum=spec))
     assert ref.report.outer_iters == g["outer_iters"]
-    fast = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=5000))
-    assert _relx(fast.x, ref.x) <= TOL_X
+    for variant in (256, 128):  # recursive and true residual
+        fast = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=5000, variant=variant))
+        assert _relx(fast.x, ref.x) <= TOL_X, (variant, _relx(fast.x, ref.x))
     p.close()
 
 

@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--cases", default="p27:128:8,p27:96:8,p27:128:4,p7:256:4,p27:256:8")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_count_band.json"))
     ap.add_argument("--skip-ref", action="store_true", help="no serial reference-algebra runs")
+    ap.add_argument("--ref-only", action="store_true",
+                    help="only the exact-lambda serial reference run (for rel_x_vs_ref)")
     ap.add_argument("--variants", default="")
     ap.add_argument("--tree-band", action="store_true",
                     help="reference band with tree reductions (fast) instead of serial chains")
@@ -106,6 +108,8 @@ def main():
                         -1e-9):
                 add(f"reference-tree lambda*(1{'-' if eps >= 0 else '+'}{abs(eps):g})", "reference",
                     L.CS_VAR_TREE, eps)
+        elif a.ref_only:
+            add("reference", "reference")
         elif not a.skip_ref:
             add("reference", "reference")
             for eps in (1e-13, -1e-13, 1e-12, -1e-12):
@@ -118,7 +122,9 @@ def main():
                     ("fast + reference MPK", L.CS_VAR_REF_MPK),
                     ("fast + explicit W + ref FGS + ref MPK",
                      L.CS_VAR_EXPLICIT_W | L.CS_VAR_REF_FGS | L.CS_VAR_REF_MPK),
-                    ("fast, stored P + explicit W", L.CS_VAR_P_STORED | L.CS_VAR_EXPLICIT_W)]
+                    ("fast, stored P + explicit W", L.CS_VAR_P_STORED | L.CS_VAR_EXPLICIT_W),
+                    ("fast, true residual", L.CS_VAR_TRUE_R),
+                    ("fast, recursive residual", L.CS_VAR_RECUR_R)]
         if a.variants:
             keep = set(a.variants.split(","))
             variants = [v for v in variants if str(v[1]) in keep]

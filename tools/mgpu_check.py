@@ -57,6 +57,7 @@ def main():
     ap.add_argument("--nz", type=int, default=0)
     ap.add_argument("--s", type=int, default=4)
     ap.add_argument("--stencil", default="poisson27")
+    ap.add_argument("--variant", type=int, default=0, help="CS_VAR_* bits of the fast solves")
     ap.add_argument("--mm", action="store_true",
                     help="general CSR path: a locally shuffled operator read from a Matrix "
                          "Market file (irregular, owner-grouped halo)")
@@ -106,7 +107,7 @@ def main():
     res["spmv_bitwise"] = bool(y.tobytes() == port.spmv(o, xg)[b0:e0].tobytes())
     # distributed fast-mode solve vs the oracle
     x_o, r_o = port.pcg_s_solve(o, s=a.s, tol=1e-8, max_outer=5000)
-    sol = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000))
+    sol = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000, variant=a.variant))
     parts = [None] * world
     dist.all_gather_object(parts, (b0, sol.x))
     x = np.concatenate([v for _, v in sorted(parts, key=lambda t: t[0])])
@@ -115,10 +116,12 @@ def main():
     res["x_rel"] = float(np.linalg.norm(x - x_o) / np.linalg.norm(x_o))
     res["allreduces"] = sol.report.device_allreduces
     res["halo_mode"] = p.halo_mode
+    res["schedule"] = sol.report.schedule
     # the same solve with the NCCL halo: the transport must not change a bit
     os.environ["CS_P2P_HALO"] = "0"
     sol_n = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000,
-                                              spectrum=sol.report.spectrum_used))
+                                              spectrum=sol.report.spectrum_used,
+                                              variant=a.variant))
     os.environ.pop("CS_P2P_HALO")
     res["halo_mode_off"] = p.halo_mode
     res["transport_bitwise"] = bool(sol_n.x.tobytes() == sol.x.tobytes()

@@ -95,6 +95,9 @@ struct CdiaClass {  // host side
   // (P % 4 == 0, P >= 3L, L >= 3): plane-streaming kernel (sell_box_kernel)
   int64_t boxP = 0, boxL = 0;
   bool geo = false;  // box class with geometric participation (separable fast SpMV)
+  // geo and the z face bits are plane-uniform (only the first plane may lack its
+  // lower neighbour, only the last its upper one): zl0 / zuN are those two bits
+  bool zuni = false, zl0 = false, zuN = false;
 };
 
 struct SellView {

@@ -669,7 +669,19 @@ void build_cdia(cs_problem* p) {
     CS_CUDA(cudaMemcpyAsync(hg.data(), geo.p, sizeof(int) * cls.size(), cudaMemcpyDeviceToHost,
                             c->stream));
     CS_CUDA(cudaStreamSynchronize(c->stream));
-    for (size_t k = 0; k < cls.size(); ++k) cls[k].geo = cls[k].boxL > 0 && hg[k] == 0;
+    for (size_t k = 0; k < cls.size(); ++k) {
+      cls[k].geo = cls[k].boxL > 0 && (hg[k] & 1) == 0;
+      cls[k].zuni = cls[k].geo && (hg[k] & 2) == 0;
+      if (!cls[k].zuni) continue;
+      const int64_t r0 = cls[k].s0 * kSliceRows, r1 = std::min(cls[k].s1 * kSliceRows, p->n_local);
+      const int64_t last = r0 + (r1 - r0 - 1) / cls[k].boxP * cls[k].boxP;
+      uint32_t w[2];
+      CS_CUDA(cudaMemcpyAsync(&w[0], p->pbits.as<uint32_t>() + r0, 4, cudaMemcpyDeviceToHost, c->stream));
+      CS_CUDA(cudaMemcpyAsync(&w[1], p->pbits.as<uint32_t>() + last, 4, cudaMemcpyDeviceToHost, c->stream));
+      CS_CUDA(cudaStreamSynchronize(c->stream));
+      cls[k].zl0 = (w[0] >> 4) & 1u;
+      cls[k].zuN = (w[1] >> 22) & 1u;
+    }
   }
   for (size_t k = 0; k < cls.size(); ++k) {
     cls[k].t.diag = 0.0;

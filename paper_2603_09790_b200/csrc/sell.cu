@@ -784,7 +784,17 @@ __global__ void cdia_geo_kernel(const uint32_t* __restrict__ bits, int64_t r0, i
   bool ok = e == (w & 0x7FFFFFFu);
   constexpr uint32_t kXY = (1u << 10) | (1u << 12) | (1u << 14) | (1u << 16);
   if (r - P >= r0) ok = ok && ((bits[r - P] ^ w) & kXY) == 0u;
-  if (!ok) atomicExch(bad, 1);
+  if (!ok) atomicOr(bad, 1);
+  // bit 1: the z face bits are not plane-uniform -- every plane but the first has
+  // its lower neighbour plane (bit 4), every plane but the last its upper one
+  // (bit 22), and the first / last plane share one value each. Without it the
+  // separable kernel takes the z bits from plane flags and the x / y bits from
+  // one plane per column: no participation-word stream.
+  const int64_t m = (r - r0) / P, last = (r1 - r0 - 1) / P;
+  bool zok = m == 0 ? (((w ^ bits[r0]) >> 4) & 1u) == 0u : ((w >> 4) & 1u) != 0u;
+  if (m == last) zok = zok && (((w ^ bits[r0 + last * P]) >> 22) & 1u) == 0u;
+  else zok = zok && ((w >> 22) & 1u) != 0u;
+  if (!zok) atomicOr(bad, 2);
 }
 
 void launch_cdia_geo_check(const uint32_t* bits, int64_t r0, int64_t r1, int64_t P, int* bad,

@@ -680,6 +680,11 @@ struct BoxGeom {
   uint32_t stage_bytes;
   int sep = 0;        // separable plane sums (fast kinds, NEG1, geometric class)
   double dp1 = 0.0;   // centre value + 1 (separable: y = dp1 * x_c - sum of present x)
+  // separable on a class with plane-uniform z face bits (CdiaClass::zuni): no
+  // participation-word stream -- x / y face bits from one plane per column
+  // segment, z bits from the plane index (the launch's first plane lacks its
+  // lower neighbour iff !zl_first, its last plane its upper one iff !zu_last)
+  int nobits = 0, zl_first = 1, zu_last = 1;
 };
 
 // a block's stage sequence: items [i0, i1) (item = column * nplanes + plane)
@@ -719,7 +724,7 @@ __device__ __forceinline__ void box_issue(const BoxGeom& b, const SellView& a, c
   const uint32_t bx = xhi > xlo ? static_cast<uint32_t>((xhi - xlo) * 8) : 0u;
   bytes += bx;
   int64_t nb = 0, rb = cb + k * b.P;
-  if (k < m1) {
+  if (k < m1 && !b.nobits) {
     nb = b.R1 - rb < width ? b.R1 - rb : width;
     nb = nb > 0 ? (nb + 3) & ~int64_t{3} : 0;
   }
@@ -846,6 +851,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
   __syncthreads();
   double ap[R], ap2[R], cen2[R];  // running sums of planes k-1, k-2; centre of plane k-2
   uint32_t bp[R], bp2[R];         // participation words of planes k-1, k-2
+  uint32_t fxy[R];                // nobits: the x / y face bits of this column's positions
   double dotv = 0.0;
   const int R0 = static_cast<int>(b.R0), R1 = static_cast<int>(b.R1), P = static_cast<int>(b.P);
   const int L = static_cast<int>(b.L);
@@ -877,6 +883,9 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
       for (int j = 0; j < R; ++j) {
         ap[j] = ap2[j] = cen2[j] = 0.0;
         bp[j] = bp2[j] = 0u;
+        const int i = threadIdx.x + j * CS_BOX_THREADS;
+        const int r = cb + m0 * P + i;  // plane-invariant on a geometric class
+        fxy[j] = b.nobits && i < width && r < R1 ? __ldg(a.pbits + r) : 0u;
       }
     }
     // rows of planes k (new sums), k-1 and k-2 (complete) held by this column
@@ -889,14 +898,18 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     uint32_t bk[R], mk[R];
     double acc0[R], acc1[R], acc2[R], cen[R];
     if (kSepKind && b.sep) {
+      const bool zl = k > 0 || b.zl_first, zu = k - 2 < b.nplanes - 1 || b.zu_last;  // nobits
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int i = threadIdx.x + j * CS_BOX_THREADS;
-        bk[j] = i < lim_k ? bs[i] : 0u;
+        bk[j] = !b.nobits && i < lim_k ? bs[i] : 0u;
         acc1[j] = ap[j];
         acc2[j] = ap2[j];
-        box_terms_sep(xs + i, L, bk[j] | bp[j] | bp2[j], (bk[j] >> 4) & 1u, (bp2[j] >> 22) & 1u,
-                      acc0[j], acc1[j], acc2[j], cen[j]);
+        if (b.nobits)
+          box_terms_sep(xs + i, L, fxy[j], zl, zu, acc0[j], acc1[j], acc2[j], cen[j]);
+        else
+          box_terms_sep(xs + i, L, bk[j] | bp[j] | bp2[j], (bk[j] >> 4) & 1u, (bp2[j] >> 22) & 1u,
+                        acc0[j], acc1[j], acc2[j], cen[j]);
         acc2[j] = fma(b.dp1, cen2[j], -acc2[j]);  // (a_ii + 1) x_c - S, completed rows only
       }
       goto epilogue;
@@ -1046,6 +1059,18 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
     b.sep = sep_env && neg1 && cl.geo &&
             (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kDot || KIND == kResidF);
     b.dp1 = t.v[13] + 1.0;
+    {
+      const int64_t cr0 = cl.s0 * kSliceRows;
+      const int64_t cr1 = std::min(cl.s1 * kSliceRows, a.n_local);
+      const char* nb_e = std::getenv("CS_BOX_NOBITS");
+      const bool nb_env = nb_e == nullptr || std::atoi(nb_e) != 0;
+      if (b.sep && cl.zuni && nb_env && (b.R0 - cr0) % b.P == 0 && std::min(b.R1, a.n_local) <= cr1) {
+        const int64_t d = (b.R0 - cr0) / b.P, clast = (cr1 - cr0 - 1) / b.P;
+        b.nobits = 1;
+        b.zl_first = d > 0 || cl.zl0;
+        b.zu_last = d + b.nplanes - 1 < clast || cl.zuN;
+      }
+    }
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(items, 148 * per_sm)));

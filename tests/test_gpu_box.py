@@ -17,12 +17,14 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(64, 64, 40), (70, 50, 13), (40, 36, 30), (5, 4, 7), (128, 96, 9), (33, 20, 11)]
 
 
-def _solve(cs, p, lam, box, sep=True):
-    env = {"CS_SPMV_BOX": "1" if box else "0", "CS_BOX_SEP": "1" if sep else "0"}
+def _solve(cs, p, lam, box, sep=True, nobits=True, variant=0):
+    env = {"CS_SPMV_BOX": "1" if box else "0", "CS_BOX_SEP": "1" if sep else "0",
+           "CS_BOX_NOBITS": "1" if nobits else "0"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
-        r = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=3000, spectrum=lam))
+        r = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=3000, spectrum=lam,
+                                              variant=variant))
         y = p.spmv(np.arange(p.n_local, dtype=np.float64) % 7 - 3.0)
         return r.x, r.report.outer_iters, y.tobytes()
     finally:
@@ -55,5 +57,12 @@ def test_box_spmv_bitwise_and_solve_identical(cs, port, dims):
         assert sep[2] == off[2]  # plain SpMV stays in the exact order
         assert abs(sep[1] - off[1]) <= max(2, off[1] // 20), (sep[1], off[1])
         assert np.linalg.norm(sep[0] - off[0]) / np.linalg.norm(off[0]) <= 1e-8
+        # face bits from the plane index and one plane per column (no participation
+        # stream) vs from the stream: the same arithmetic, bit for bit -- in both
+        # residual schedules (the true residual runs its b - A x through the kernel)
+        for variant in (256, 128):
+            a = _solve(cs, p, lam, True, nobits=True, variant=variant)
+            b = _solve(cs, p, lam, True, nobits=False, variant=variant)
+            assert a[1] == b[1] and a[0].tobytes() == b[0].tobytes(), (variant, a[1], b[1])
     finally:
         p.close()

@@ -138,19 +138,23 @@ def nnz_of(stencil, nx, ny, nz):
 
 
 def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=True,
-                   diag_stream=True, pz=False):
+                   diag_stream=True, pz=False, tr=False, mat_fast=None):
     """Algorithmic bytes of every SpMV-phase kernel of one solve:
     the matrix in the format actually stored (SELL-32P: FP64 value slots +
-    per-slice column/pattern/meta bytes) read once, x read once, each output
-    written once, plus the epilogue vectors of each MPK step."""
+    per-slice column/pattern/meta bytes; CDIA: 32-bit participation words) read
+    once, x read once, each output written once, plus the epilogue vectors of
+    each MPK step. mat_fast: the matrix bytes of the fast kinds (separable box
+    SpMV on planar classes: no participation words, 0), default mat_bytes.
+    tr: the true-residual schedule's r = b - A x, z_0 = M^-1 r once per outer."""
+    mf = mat_bytes if mat_fast is None else mat_fast
     v = 8 * n
     b_spmv = mat_bytes + 2 * v                       # y = A x
     b_resid = mat_bytes + 3 * v                      # r = b - A x
-    b_dot = mat_bytes + 2 * v                        # Lanczos t = A v (+ v.t)
+    b_dot = mf + 2 * v                               # Lanczos t = A v (+ v.t)
     j = v if jacobi and diag_stream else 0          # D^-1 read by the epilogue
     if mode == "fast":                               # z_q = 2a D^-1 p_q - 2s z_{q-1} - z_{q-2}
-        b_first = mat_bytes + 3 * v + j              # x, p, z (+ D^-1)
-        b_mid = mat_bytes + 4 * v + j                # x, p, z_{q-2}, z (+ D^-1)
+        b_first = mf + 3 * v + j                     # x, p, z (+ D^-1)
+        b_mid = mf + 4 * v + j                       # x, p, z_{q-2}, z (+ D^-1)
     else:                                            # reference zp recurrence (+ D^-1 vector)
         b_first = mat_bytes + 2 * v + v + j + (v if jacobi else 0) + v
         b_mid = mat_bytes + 2 * v + 2 * v + j + (v if jacobi else 0) + v
@@ -159,23 +163,38 @@ def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=Tr
     setup_mpk = per_mpk  # the setup MPK always stores P (it becomes AQ_1)
     if pz and mode == "fast":  # no p_q written; the last step writes z_s (a mid-type step)
         per_mpk = (b_first - v) if s == 1 else (b_first - v) + (s - 1) * (b_mid - v)
+    if tr and mode == "fast":  # x, b read; r, z_0 written (+ D^-1)
+        per_mpk += mf + 4 * v + j
     # setup MPK + one (speculative) MPK per outer iteration (fast algebra)
     return b_resid + lanczos_steps * b_dot + outer * per_mpk + setup_mpk, b_spmv
 
 
-def outer_bytes_format(mat_bytes, n, s, diag_stream=True, pz=False):
+def update_vectors(s, pz, tr, diag_stream):
+    """Vectors the fast update pass moves per row. Recursive
+    residual: Q, Z, AQ, P (PZ: z_s, + D^-1 unless uniform), x, r read; Q, AQ,
+    x, r, z_0 written. True residual: Q, Z, x read; Q, x written."""
+    if tr:
+        return 3 * s + 2
+    return (5 if pz else 6) * s + (6 if diag_stream else 5)
+
+
+def outer_bytes_format(mat_bytes, n, s, diag_stream=True, pz=False, tr=False, mat_fast=None):
     """Per-outer algorithmic bytes of the fast schedule in the stored format:
     s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+6).
     PZ schedule (P derived from Z): MPK steps write no p (the last writes z_s),
-    pack 8n(2s+2), update 8n(5s+6)."""
+    pack 8n(2s+2), update 8n(5s+6). True residual: update 8n(3s+2) + one
+    residual SpMV (x, b read; r, z_0 written)."""
+    mf = mat_bytes if mat_fast is None else mat_fast
     v = 8 * n
     j = v if diag_stream else 0
     if pz:
-        mpk = (mat_bytes + 2 * v + j) + (s - 1) * (mat_bytes + 3 * v + j)
-        return mpk + v * (2 * s + 2) + v * (5 * s + (6 if diag_stream else 5))
-    mpk = (mat_bytes + 3 * v + j) + (s - 2) * (mat_bytes + 4 * v + j) + (mat_bytes + 2 * v) \
+        mpk = (mf + 2 * v + j) + (s - 1) * (mf + 3 * v + j)
+        if tr:
+            mpk += mf + 4 * v + j
+        return mpk + v * (2 * s + 2) + v * update_vectors(s, pz, tr, diag_stream)
+    mpk = (mf + 3 * v + j) + (s - 2) * (mf + 4 * v + j) + (mat_bytes + 2 * v) \
         if s > 1 else mat_bytes + 2 * v
-    return mpk + v * (3 * s + 1) + v * (6 * s + (6 if diag_stream else 5))
+    return mpk + v * (3 * s + 1) + v * update_vectors(s, pz, False, diag_stream)
 
 
 def outer_bytes(nnz, n, s):
@@ -362,16 +381,21 @@ def run_ours(args):
     mat = 4 * 32 * prob.slices if prob.cdia_classes > 0 else prob.device_bytes
     dstream = not prob.cdia_uniform_diag  # CDIA: 1/a_ii is a kernel constant
     pz = bool(rep.schedule & 1)  # CS_SCHED_P_FROM_Z
+    tr = bool(rep.schedule & 4)  # CS_SCHED_TRUE_R
+    # planar CDIA classes: the separable fast kinds read no participation words
+    mat_f = 0 if (prob.cdia_planar and args.mode == "fast") else mat
     alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode,
-                                 diag_stream=dstream, pz=pz)
+                                 diag_stream=dstream, pz=pz, tr=tr, mat_fast=mat_f)
     v8 = 8 * nl
     outers_t = sum(r.outer_iters for r in reps_t)
-    upd_vec = (5 if pz else 6) * args.s + (6 if dstream else 5)
+    upd_vec = update_vectors(args.s, pz, tr, dstream)
     alg_phase = {
         "spmv": sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps,
-                                   args.mode, diag_stream=dstream, pz=pz)[0] for r in reps_t),
-        # Q, Z, AQ, P (PZ: Z + z_s instead of P), x, r (+ D^-1 unless uniform) read;
-        # Q, AQ, x, r, z_0 written
+                                   args.mode, diag_stream=dstream, pz=pz, tr=tr,
+                                   mat_fast=mat_f)[0] for r in reps_t),
+        # recursive residual: Q, Z, AQ, P (PZ: Z + z_s instead of P), x, r (+ D^-1
+        # unless uniform) read; Q, AQ, x, r, z_0 written. True residual: Q, Z, x
+        # read; Q, x written
         "update": outers_t * v8 * upd_vec,
         # Q, Z, P, r read once (PZ: Q, Z, z_s, r); one launch per outer + the setup one
         "reduce": outers_t * v8 * ((2 * args.s + 2) if pz else (3 * args.s + 1))
@@ -380,17 +404,18 @@ def run_ours(args):
     names = {"spmv": "sell_box_kernel<kMpk*> (plane-streaming FP64 SpMV over the 3x3x3 constant-"
                      "diagonal class: bulk-copied plane stages, fused MPK epilogue; gather "
                      "kernels for other classes)",
-             "update": "update_kernel<s,beta,xr,z0> (Q, AQ, x, r, z_0 update pass)",
+             "update": ("update_tr_kernel<s,beta> (Q, x update pass; r from the residual SpMV)"
+                        if tr else "update_kernel<s,beta,xr,z0> (Q, AQ, x, r, z_0 update pass)"),
              "reduce": "pack_kernel<s> (packed Gram/projection block, DMMA)"}
     peak, peak_src = measured_peak()
-    tr = ncu_traffic() or {}
+    trf = ncu_traffic() or {}
     kern = {}
     for ph, byts in alg_phase.items():
         ms = phases[ph][0]
         if ms <= 0:
             continue
         ach = byts / (ms / 1e3) / 1e9
-        t = tr.get(ph) or {}
+        t = trf.get(ph) or {}
         kern[ph] = {"kernel": names[ph], "ms_per_solve": ms / len(reps_t),
                     "share_of_step": ms / t_inst if t_inst > 0 else None,
                     "achieved": ach, "frac": ach / peak,
@@ -412,7 +437,7 @@ def run_ours(args):
             "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}
     # whole-solve bandwidth against B_outer
     solve_outer_ms = rep.t_solve_ms / max(rep.outer_iters, 1)
-    b_out = outer_bytes_format(mat, nl, args.s, dstream, pz)
+    b_out = outer_bytes_format(mat, nl, args.s, dstream, pz, tr, mat_f)
     b_survey = outer_bytes(nnz_l, nl, args.s)
     solve_level = {"t_outer_ms": solve_outer_ms, "B_outer_GB": b_out / 1e9,
                    "achieved_GBps": b_out / (solve_outer_ms / 1e3) / 1e9,

@@ -121,8 +121,9 @@ typedef struct {
                                  the default wherever it applies; the bit is accepted */
 #define CS_VAR_P_STORED 64    /* fast: the stored-P schedule (round-1 default) */
 #define CS_VAR_TRUE_R 128     /* fast, PZ schedule: r_{k+1} = b - A x_{k+1} from one residual
-                                 SpMV instead of r_k - AQ alpha (no AQ block) */
-#define CS_VAR_RECUR_R 256    /* fast: force the recursive residual (AQ block) */
+                                 SpMV instead of r_k - AQ alpha (no AQ block) --
+                                 the default wherever the PZ schedule runs; the bit is accepted */
+#define CS_VAR_RECUR_R 256    /* fast: the recursive residual r_k - AQ alpha (AQ block kept) */
 
 typedef struct {
   /* SolveReport (solver.hpp:39-68), reference semantics */
@@ -252,8 +253,9 @@ int cs_problem_read_mm(cs_ctx* ctx, const char* path, int require_spd, cs_proble
 int cs_problem_destroy(cs_problem* p);
 /* info12: n_global, n_local, nnz_local, row_begin, n_ghost, device bytes of the
  * SELL arrays, slices, pattern-compressed slices, uniform-value slices, pattern
- * table entries, constant-diagonal (CDIA) classes, 1 if every CDIA class has a
- * uniform diagonal (format) */
+ * table entries, constant-diagonal (CDIA) classes, CDIA flags: bit 0 every class
+ * has a uniform diagonal, bit 1 every class is a geometric box with plane-uniform
+ * z faces (the separable SpMV reads no participation words) */
 int cs_problem_info(cs_problem* p, int64_t* info12);
 /* Local rows back as CSR with GLOBAL column indices (bit-exact assembly check). */
 int cs_problem_download_csr(cs_problem* p, int64_t* rowptr, int64_t* col, double* val);

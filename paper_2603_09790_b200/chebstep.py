@@ -250,7 +250,9 @@ class DeviceProblem:
         _check(lib.cs_problem_info(handle, info))
         (self.n_global, self.n_local, self.nnz_local, self.row_begin, self.n_ghost,
          self.device_bytes, self.slices, self.pattern_slices, self.uniform_slices,
-         self.pattern_entries, self.cdia_classes, self.cdia_uniform_diag) = (int(v) for v in info)
+         self.pattern_entries, self.cdia_classes, cdia_flags) = (int(v) for v in info)
+        self.cdia_uniform_diag = cdia_flags & 1
+        self.cdia_planar = (cdia_flags >> 1) & 1  # separable SpMV without participation words
         self.precond = "identity"
 
     @property

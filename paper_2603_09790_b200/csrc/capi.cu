@@ -348,9 +348,12 @@ int cs_problem_info(cs_problem* p, int64_t* info) {
     info[8] = p->uniform_slices;
     info[9] = p->pattern_entries;
     info[10] = static_cast<int64_t>(p->cdia.size());
-    bool ud = !p->cdia.empty();
-    for (const auto& k : p->cdia) ud = ud && k.t.diag != 0.0;
-    info[11] = ud ? 1 : 0;
+    bool ud = !p->cdia.empty(), zu = !p->cdia.empty();
+    for (const auto& k : p->cdia) {
+      ud = ud && k.t.diag != 0.0;
+      zu = zu && k.zuni;
+    }
+    info[11] = (ud ? 1 : 0) | (zu ? 2 : 0);
   });
 }
 

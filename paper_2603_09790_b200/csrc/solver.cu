@@ -732,8 +732,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
                      update_gram_supported(s) && (var & CS_VAR_P_STORED) == 0;
   // true-residual schedule: r_{k+1} = b - A x_{k+1} (+ z_0) in one residual SpMV,
   // the update pass keeps only Q and x (no AQ block, no recursive r)
-  const bool tr_on = pz_on && !explicit_w && (var & CS_VAR_TRUE_R) != 0 &&
-                     (var & CS_VAR_RECUR_R) == 0;
+  // (the default of the fast PZ schedule; CS_VAR_RECUR_R keeps the recursive r)
+  const bool tr_on = pz_on && !explicit_w && (var & CS_VAR_RECUR_R) == 0;
   PzArgs pz;
   if (pz_on) {
     const double alpha = 2.0 / (hi - lo), sigma = (hi + lo) / (hi - lo);  // mpk.hpp:22-25

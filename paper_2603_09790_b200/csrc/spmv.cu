@@ -711,7 +711,9 @@ struct BoxIter {
   }
 };
 
-template <bool E2>
+// E2: one row-aligned epilogue stream of plane k-2 is staged too -- z_{q-2}
+// (kMpkMidF) or b (kResidF, B_SRC)
+template <bool E2, bool B_SRC = false>
 __device__ __forceinline__ void box_issue(const BoxGeom& b, const SellView& a, const SpmvArgs& g,
                                           unsigned char* stage, uint64_t* bar, int64_t c,
                                           int64_t k, int64_t m1) {
@@ -742,7 +744,7 @@ __device__ __forceinline__ void box_issue(const BoxGeom& b, const SellView& a, c
   if (bx) bulk_g2s(xs + (xlo - E), g.x + xlo, bx, bar);
   if (nb) bulk_g2s(stage + 8 * b.xs + 8 * kBoxT, a.pbits + rb, static_cast<uint32_t>(nb * 4), bar);
   if constexpr (E2)
-    if (nz) bulk_g2s(stage + 8 * b.xs, g.zp2 + rz, static_cast<uint32_t>(nz * 8), bar);
+    if (nz) bulk_g2s(stage + 8 * b.xs, (B_SRC ? g.b : g.zp2) + rz, static_cast<uint32_t>(nz * 8), bar);
 }
 
 // One row position of a stage: its nine x values (3 lines x 3) feed group 0 of
@@ -830,7 +832,8 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
     __syncthreads();
   }
-  constexpr bool kE2 = KIND == kMpkMidF;
+  constexpr bool kE2 = KIND == kMpkMidF || KIND == kResidF;
+  constexpr bool kBsrc = KIND == kResidF;  // the staged stream is b, not z_{q-2}
   constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF;
   constexpr int R = CS_BOX_ROWS;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     for (int sl = 0; sl < b.ns; ++sl) mbar_init(&full[sl], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (; psl < b.ns - 1 && pre.valid; ++psl, pre.next(b))
-      box_issue<kE2>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
+      box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
   }
   __syncthreads();
   double ap[R], ap2[R], cen2[R];  // running sums of planes k-1, k-2; centre of plane k-2
@@ -861,7 +864,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
   for (; cur.valid; cur.next(b)) {
     if (threadIdx.x == 0 && pre.valid) {  // refill the slot consumed last iteration
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      box_issue<kE2>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
+      box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
       pre.next(b);
       psl = psl + 1 == b.ns ? 0 : psl + 1;
     }
@@ -962,8 +965,9 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
         EpiOps eo;
         eo.exd = cen2[j];
         eo.einv = JAC ? t.inv : 1.0;
-        if constexpr (kE2) eo.e2 = zs[i];
-        if constexpr (KIND == kResid || KIND == kResidF) eo.e1 = g.b[r2];
+        if constexpr (kE2 && !kBsrc) eo.e2 = zs[i];
+        if constexpr (kBsrc) eo.e1 = zs[i];
+        if constexpr (KIND == kResid) eo.e1 = g.b[r2];
         double zv = 0.0;
         epi_store<KIND, JAC>(g, r2, acc2[j], eo, dotv, zv);
         if constexpr (kPush)
@@ -1030,7 +1034,8 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
   } else {
     if (!box_enabled() || cl.boxL == 0 || a.pbits == nullptr) return false;
     const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
-    if (!al16(g.x) || (KIND == kMpkMidF && !al16(g.zp2))) return false;
+    if (!al16(g.x) || (KIND == kMpkMidF && !al16(g.zp2)) || (KIND == kResidF && !al16(g.b)))
+      return false;
     BoxGeom b{};
     b.R0 = lo * kSliceRows;
     b.R1 = hi * kSliceRows;

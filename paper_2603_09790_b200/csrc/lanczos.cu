@@ -9,6 +9,9 @@
 //    stored vector, exactly the reference operation sequence;
 //  * fast: classical Gram-Schmidt -- all projections g_i . r from one pass,
 //    the correction from a second pass fused with the r.gr reduction.
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "lanczos.cuh"
 
@@ -131,7 +134,23 @@ __global__ void __launch_bounds__(kThreads)
 // once, each g_i once; every thread keeps m accumulators over a grid-stride
 // row sweep (fixed grid: deterministic), then a fixed warp/block tree and
 // last-block finalisation in block order.
-constexpr int kProjBlocks = 296;  // 2 x 148 SMs x 8 warps, up to 40 loads per lane in flight
+// Grid: one wave of resident blocks at the kernel's occupancy (a fixed 296-block
+// grid left the 60-80-register instances at 16 warps/SM with too few loads in
+// flight: 1.7 TB/s at m = 12..20, profiles/r02h_launches_head_256_summary.txt).
+// Fixed per device and kernel, so the reduction order is run-to-run identical.
+constexpr int kProjBlocks = 296;      // legacy fixed grid (CS_LZ_GRID=0)
+constexpr int kProjMaxBlocks = 148 * 8;
+
+template <typename K>
+int proj_grid(K kern) {
+  static const bool fixed = [] {
+    const char* e = std::getenv("CS_LZ_GRID");
+    return e != nullptr && std::atoi(e) == 0;
+  }();
+  if (fixed) return kProjBlocks;
+  const int per_sm = kernel_setup(reinterpret_cast<const void*>(kern), kThreads, 0);
+  return std::min(148 * per_sm, kProjMaxBlocks);
+}
 
 template <int MB>
 __global__ void __launch_bounds__(kThreads)
@@ -377,9 +396,9 @@ void lz_cgs(int64_t n, int64_t ld, int m, const double* V, const double* G, doub
 void lz2_resid_proj(int64_t n, int64_t ld, int m, const double* t, const double* G,
                     const double* dinv, double dconst, double* gr, const LanczosScalars* sc, int j,
                     double* proj, double* partial, unsigned* ticket, DevState* st, cudaStream_t s) {
-#define CSG_RP(MB)                                                                             \
-  lz2_resid_proj_kernel<MB><<<kProjBlocks, kThreads, 0, s>>>(n, ld, m, t, G, dinv, dconst, gr, \
-                                                             sc, j, proj, partial, ticket, st)
+#define CSG_RP(MB)                                                                          \
+  lz2_resid_proj_kernel<MB><<<proj_grid(lz2_resid_proj_kernel<MB>), kThreads, 0, s>>>(      \
+      n, ld, m, t, G, dinv, dconst, gr, sc, j, proj, partial, ticket, st)
   if (m <= 8) CSG_RP(8);
   else if (m <= 16) CSG_RP(16);
   else if (m <= 24) CSG_RP(24);
@@ -406,12 +425,13 @@ void lz2_scale(int64_t n, const double* gr, const double* dinv, double dconst, d
 
 bool lz_proj_supported(int m) { return m >= 1 && m <= 40; }
 
-size_t lz_proj_partial_doubles(int m) { return static_cast<size_t>(kProjBlocks) * m; }
+size_t lz_proj_partial_doubles(int m) { return static_cast<size_t>(kProjMaxBlocks) * m; }
 
 void lz_proj(int64_t n, int64_t ld, int m, const double* G, const double* r, double* proj,
              double* partial, unsigned* ticket, DevState* st, cudaStream_t s) {
-#define CSG_PROJ(MB) \
-  proj_kernel<MB><<<kProjBlocks, kThreads, 0, s>>>(n, ld, m, G, r, proj, partial, ticket, st)
+#define CSG_PROJ(MB)                                                               \
+  proj_kernel<MB><<<proj_grid(proj_kernel<MB>), kThreads, 0, s>>>(n, ld, m, G, r, proj, \
+                                                                  partial, ticket, st)
   if (m <= 8) CSG_PROJ(8);
   else if (m <= 16) CSG_PROJ(16);
   else if (m <= 24) CSG_PROJ(24);

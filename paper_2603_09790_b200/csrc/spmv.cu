@@ -685,7 +685,12 @@ struct BoxGeom {
   // segment, z bits from the plane index (the launch's first plane lacks its
   // lower neighbour iff !zl_first, its last plane its upper one iff !zu_last)
   int nobits = 0, zl_first = 1, zu_last = 1;
+  int vstrip = 0;     // separable path with vertical row strips (L divides the block size)
 };
+
+__device__ __forceinline__ uint32_t bk_of(const uint32_t* bs, int i, int lim) {
+  return i < lim ? bs[i] : 0u;
+}
 
 // a block's stage sequence: items [i0, i1) (item = column * nplanes + plane)
 // split into column segments of planes [m0, m1); a segment streams stages
@@ -855,6 +860,16 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
   double ap[R], ap2[R], cen2[R];  // running sums of planes k-1, k-2; centre of plane k-2
   uint32_t bp[R], bp2[R];         // participation words of planes k-1, k-2
   uint32_t fxy[R];                // nobits: the x / y face bits of this column's positions
+  // rows of a column held by this thread: i = tid + j * threads, or (vertical
+  // strips, separable path) R consecutive lines at one x position, so the R + 2
+  // three-point line sums of the strip are formed once and shared by its rows
+  int ii[R];
+  const int vx = b.vstrip ? static_cast<int>(threadIdx.x % b.L) : 0;
+  const int vg = b.vstrip ? static_cast<int>(threadIdx.x / b.L) : 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    ii[j] = b.vstrip ? (vg * R + j) * static_cast<int>(b.L) + vx
+                     : static_cast<int>(threadIdx.x) + j * CS_BOX_THREADS;
   double dotv = 0.0;
   const int R0 = static_cast<int>(b.R0), R1 = static_cast<int>(b.R1), P = static_cast<int>(b.P);
   const int L = static_cast<int>(b.L);
@@ -886,7 +901,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
       for (int j = 0; j < R; ++j) {
         ap[j] = ap2[j] = cen2[j] = 0.0;
         bp[j] = bp2[j] = 0u;
-        const int i = threadIdx.x + j * CS_BOX_THREADS;
+        const int i = ii[j];
         const int r = cb + m0 * P + i;  // plane-invariant on a geometric class
         fxy[j] = b.nobits && i < width && r < R1 ? __ldg(a.pbits + r) : 0u;
       }
@@ -902,9 +917,43 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     double acc0[R], acc1[R], acc2[R], cen[R];
     if (kSepKind && b.sep) {
       const bool zl = k > 0 || b.zl_first, zu = k - 2 < b.nplanes - 1 || b.zu_last;  // nobits
+      if (b.vstrip) {
+        // line sums of lines vg*R - 1 .. vg*R + R at x = vx (xs index of (line l,
+        // x + dx) is (l + 1) L + x + dx + 1); each row adds its own line, then the
+        // one below and the one above -- the order of box_terms_sep
+        uint32_t fx = 0u;
+#pragma unroll
+        for (int j = 0; j < R; ++j) fx |= b.nobits ? fxy[j] : bk_of(bs, ii[j], lim_k) | bp[j] | bp2[j];
+        const bool xl = (fx >> 12) & 1u, xr = (fx >> 14) & 1u;
+        double ls[R + 2], cm[R + 2];
+        const double* xb = xs + vg * R * L + vx;
+#pragma unroll
+        for (int l = 0; l < R + 2; ++l) {
+          const double a = xb[l * L], m = xb[l * L + 1], c = xb[l * L + 2];
+          cm[l] = m;
+          const double t = xl ? a + m : m;
+          ls[l] = xr ? t + c : t;
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          bk[j] = !b.nobits && ii[j] < lim_k ? bs[ii[j]] : 0u;
+          const uint32_t f = b.nobits ? fxy[j] : bk[j] | bp[j] | bp2[j];
+          const bool zlj = b.nobits ? zl : ((bk[j] >> 4) & 1u) != 0u;
+          const bool zuj = b.nobits ? zu : ((bp2[j] >> 22) & 1u) != 0u;
+          double bsum = ls[j + 1];
+          if ((f >> 10) & 1u) bsum += ls[j];
+          if ((f >> 16) & 1u) bsum += ls[j + 2];
+          cen[j] = cm[j + 1];
+          acc0[j] = zlj ? bsum : 0.0;
+          acc1[j] = ap[j] + bsum;
+          acc2[j] = zuj ? ap2[j] + bsum : ap2[j];
+          acc2[j] = fma(b.dp1, cen2[j], -acc2[j]);  // (a_ii + 1) x_c - S, completed rows only
+        }
+        goto epilogue;
+      }
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const int i = threadIdx.x + j * CS_BOX_THREADS;
+        const int i = ii[j];
         bk[j] = !b.nobits && i < lim_k ? bs[i] : 0u;
         acc1[j] = ap[j];
         acc2[j] = ap2[j];
@@ -921,7 +970,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     bool agree = true, full = true;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      const int i = threadIdx.x + j * CS_BOX_THREADS;
+      const int i = ii[j];
       bk[j] = i < lim_k ? bs[i] : 0u;
       // the 9-entry sub-pattern each live row uses from this stage (rows outside
       // the column/segment are never stored, so they do not constrain it)
@@ -942,24 +991,24 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     if (all_agree && __all_sync(0xffffffffu, full)) {  // interior: all 27 entries
 #pragma unroll
       for (int j = 0; j < R; ++j)
-        box_terms<0, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
+        box_terms<0, NEG1>(t, xs + ii[j], L, bk[j], bp[j], bp2[j],
                            mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
     } else if (all_agree) {  // x / y faces: one sub-pattern per row position
 #pragma unroll
       for (int j = 0; j < R; ++j)
-        box_terms<1, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
+        box_terms<1, NEG1>(t, xs + ii[j], L, bk[j], bp[j], bp2[j],
                            mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
     } else {
 #pragma unroll
       for (int j = 0; j < R; ++j)
-        box_terms<2, NEG1>(t, xs + threadIdx.x + j * CS_BOX_THREADS, L, bk[j], bp[j], bp2[j],
+        box_terms<2, NEG1>(t, xs + ii[j], L, bk[j], bp[j], bp2[j],
                            mk[j], acc0[j], acc1[j], acc2[j], cen[j]);
     }
     }
   epilogue:
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      const int i = threadIdx.x + j * CS_BOX_THREADS;
+      const int i = ii[j];
       if (i < lim_2) {  // plane k-2 row complete
         const int64_t r2 = rb2 + i;
         EpiOps eo;
@@ -1075,6 +1124,11 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
         b.zl_first = d > 0 || cl.zl0;
         b.zu_last = d + b.nplanes - 1 < clast || cl.zuN;
       }
+    }
+    {
+      const char* vs_e = std::getenv("CS_BOX_VSTRIP");
+      const bool vs_env = vs_e == nullptr || std::atoi(vs_e) != 0;
+      b.vstrip = vs_env && b.sep && b.L <= CS_BOX_THREADS && CS_BOX_THREADS % b.L == 0;
     }
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(

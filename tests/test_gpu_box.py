@@ -14,12 +14,13 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(64, 64, 40), (70, 50, 13), (40, 36, 30), (5, 4, 7), (128, 96, 9), (33, 20, 11)]
+SHAPES = [(64, 64, 40), (70, 50, 13), (40, 36, 30), (5, 4, 7), (128, 96, 9), (33, 20, 11),
+          (16, 40, 12), (256, 9, 7)]
 
 
-def _solve(cs, p, lam, box, sep=True, nobits=True, variant=0):
+def _solve(cs, p, lam, box, sep=True, nobits=True, variant=0, vstrip=True):
     env = {"CS_SPMV_BOX": "1" if box else "0", "CS_BOX_SEP": "1" if sep else "0",
-           "CS_BOX_NOBITS": "1" if nobits else "0"}
+           "CS_BOX_NOBITS": "1" if nobits else "0", "CS_BOX_VSTRIP": "1" if vstrip else "0"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -60,9 +61,15 @@ def test_box_spmv_bitwise_and_solve_identical(cs, port, dims):
         # face bits from the plane index and one plane per column (no participation
         # stream) vs from the stream: the same arithmetic, bit for bit -- in both
         # residual schedules (the true residual runs its b - A x through the kernel)
+        # and the vertical-strip row mapping (line sums shared by a thread's R
+        # consecutive lines, where the line length divides the block) vs the
+        # strided mapping: the same sums in the same order
         for variant in (256, 128):
             a = _solve(cs, p, lam, True, nobits=True, variant=variant)
             b = _solve(cs, p, lam, True, nobits=False, variant=variant)
             assert a[1] == b[1] and a[0].tobytes() == b[0].tobytes(), (variant, a[1], b[1])
+            for nb in (True, False):
+                c = _solve(cs, p, lam, True, nobits=nb, variant=variant, vstrip=False)
+                assert c[1] == a[1] and c[0].tobytes() == a[0].tobytes(), (variant, nb)
     finally:
         p.close()

@@ -685,6 +685,7 @@ struct BoxGeom {
   // segment, z bits from the plane index (the launch's first plane lacks its
   // lower neighbour iff !zl_first, its last plane its upper one iff !zu_last)
   int nobits = 0, zl_first = 1, zu_last = 1;
+  int zplast = 0;     // nobits: the launch plane holding its last real row (R1 may be slice-padded)
   int vstrip = 0;     // separable path with vertical row strips (L divides the block size)
 };
 
@@ -916,7 +917,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, CS_BOX_MINB)
     uint32_t bk[R], mk[R];
     double acc0[R], acc1[R], acc2[R], cen[R];
     if (kSepKind && b.sep) {
-      const bool zl = k > 0 || b.zl_first, zu = k - 2 < b.nplanes - 1 || b.zu_last;  // nobits
+      const bool zl = k > 0 || b.zl_first, zu = k - 2 < b.zplast || b.zu_last;  // nobits
       if (b.vstrip) {
         // line sums of lines vg*R - 1 .. vg*R + R at x = vx (xs index of (line l,
         // x + dx) is (l + 1) L + x + dx + 1); each row adds its own line, then the
@@ -1121,8 +1122,9 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
       if (b.sep && cl.zuni && nb_env && (b.R0 - cr0) % b.P == 0 && std::min(b.R1, a.n_local) <= cr1) {
         const int64_t d = (b.R0 - cr0) / b.P, clast = (cr1 - cr0 - 1) / b.P;
         b.nobits = 1;
+        b.zplast = static_cast<int>((std::min(b.R1, a.n_local) - 1 - b.R0) / b.P);
         b.zl_first = d > 0 || cl.zl0;
-        b.zu_last = d + b.nplanes - 1 < clast || cl.zuN;
+        b.zu_last = d + b.zplast < clast || cl.zuN;
       }
     }
     {

@@ -34,7 +34,7 @@ def golden_lambda(kind, n, s):
         g = json.load(f)
     key = f"{'p27' if kind == 'poisson27' else 'p7'}_{n}x{n}x{n}_s{s}_nu30_jacobi_1e-08"
     if key in g:
-        return g[key]["lambda_min"], g[key]["lambda_max"], g[key]["outer_iters"], g[key]["x_norm"]
+        return g[key]["lambda_min"], g[key]["lambda_max"], g[key]["outer_iters"], g[key].get("x_norm")
     return None
 
 

@@ -25,9 +25,16 @@ for step in "$@"; do
       timeout 1800 python tools/count_band.py --tree-band --cases p27:512:8 --out $out/${tag}_band512.json > $out/${tag}_band512.log 2>&1 ;;
     bandpz)
       timeout 1500 python tools/count_band.py --skip-ref --variants 0,1,32,33 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4,p27:256:8,p27:512:8 --out $out/${tag}_bandpz.json > $out/${tag}_bandpz.log 2>&1 ;;
+    tests_quick)
+      timeout 1200 python -m pytest tests/test_gpu_box.py tests/test_gpu_solver.py tests/test_gpu_kernels.py -q -x -m "gpu and not slow" > $out/${tag}_tests_quick.log 2>&1 ;;
+    ncu_boxlz)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sell_box_kernel<7" -s 20 -c 1 \
+        -o $out/${tag}_box python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_box.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lz2_resid_proj_kernel<24" -s 2 -c 1 \
+        -o $out/${tag}_lz python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_lz.log 2>&1 ;;
     trband)
-      timeout 2400 python tools/count_band.py --ref-only --variants 0,128 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4 --out $out/${tag}_trband.json > $out/${tag}_trband.log 2>&1
-      timeout 1800 python tools/count_band.py --skip-ref --variants 0,128 --cases p27:256:8,p27:512:8 --out $out/${tag}_trband.json >> $out/${tag}_trband.log 2>&1 ;;
+      timeout 2400 python tools/count_band.py --ref-only --variants 0,256 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4 --out $out/${tag}_trband.json > $out/${tag}_trband.log 2>&1
+      timeout 1800 python tools/count_band.py --skip-ref --variants 0,256 --cases p27:256:8,p27:512:8 --out $out/${tag}_trband.json >> $out/${tag}_trband.log 2>&1 ;;
     e2etrace)
       CS_TRACE=1 timeout 1200 python tools/e2e_trace.py 512 > $out/${tag}_e2etrace.log 2>&1 ;;
     ncu_pz)

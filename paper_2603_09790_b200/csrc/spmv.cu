@@ -826,6 +826,173 @@ __device__ __forceinline__ void box_terms_sep(const double* xs, int L, uint32_t 
   if (zu) acc2 += bsum;
 }
 
+// Separable box SpMV, compile-time specialised (sell_boxsep_kernel): the fast
+// kinds on a planar class (geometric box, every off-centre value -1, plane-
+// uniform z faces: no participation-word stream) whose line length divides the
+// block (vertical strips). The same sums in the same order as the separable
+// path of sell_box_kernel -- bitwise the same z -- with the per-row overhead
+// gone: face flags are decoded once per column segment (a warp whose lanes are
+// all interior adds without selects), z faces are per-stage uniform, the
+// finite check is one flag reported at the end (same error word), and the
+// push test is per stage. ncu on the general kernel: 107 instructions per row,
+// ALU pipe 56 %, issue-bound at 58 % of HBM (profiles/r02h_ncu_box_*.txt).
+template <int KIND, bool JAC>
+__global__ void __launch_bounds__(CS_BOX_THREADS, 1)
+    sell_boxsep_kernel(SellView a, SpmvArgs g, BoxGeom b, const __grid_constant__ CdiaTable t) {
+  if (g.st != nullptr && *(volatile int*)&g.st->done) return;
+  halo_release(g);
+  if (g.wait_ctr != nullptr) {
+    if (threadIdx.x == 0) halo_wait(g.wait_ctr, g.want_lo, g.want_hi, g.st);
+    __syncthreads();
+  }
+  constexpr bool kE2 = KIND == kMpkMidF || KIND == kResidF;
+  constexpr bool kBsrc = KIND == kResidF;
+  constexpr bool kPush = KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF;
+  constexpr int R = CS_BOX_ROWS;
+  const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
+  extern __shared__ __align__(128) unsigned char box_smem[];
+  __shared__ __align__(8) uint64_t full[CS_BOX_NS];
+  const int64_t items = b.ncols * b.nplanes;
+  const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+  BoxIter cur{i0, i1}, pre{i0, i1};
+  cur.seg(b);
+  pre.seg(b);
+  int psl = 0;
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < b.ns; ++sl) mbar_init(&full[sl], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (; psl < b.ns - 1 && pre.valid; ++psl, pre.next(b))
+      box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
+  }
+  __syncthreads();
+  const int R0 = static_cast<int>(b.R0), R1 = static_cast<int>(b.R1), P = static_cast<int>(b.P);
+  const int L = static_cast<int>(b.L);
+  const int end2 = static_cast<int>(b.R1 < b.n_local ? b.R1 : b.n_local);
+  const int vx = static_cast<int>(threadIdx.x) % L, vg = static_cast<int>(threadIdx.x) / L;
+  const int ib = vg * R * L + vx;  // column row of this thread's line j: ib + j L
+  const double ca = g.ca, cb = g.cb, cc = g.cc, einv = JAC ? t.inv : 1.0, dp1 = b.dp1;
+  double ap[R], ap2[R], cen2[R];
+  bool xl = false, xr = false, inner = false;
+  uint32_t ydm = 0u, yum = 0u;  // bit j: row j has its lower / upper line
+  bool bad = false;
+  double dotv = 0.0;
+  int sl = 0;
+  uint32_t phase = 0;
+  for (; cur.valid; cur.next(b)) {
+    if (threadIdx.x == 0 && pre.valid) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
+      pre.next(b);
+      psl = psl + 1 == b.ns ? 0 : psl + 1;
+    }
+    const int c = cur.c, k = cur.k, m0 = cur.m0;
+    const int cbase = R0 + c * kBoxT;
+    const int width = min(P - c * kBoxT, kBoxT);
+    if (k == m0) {  // new column segment: face flags of the thread's positions
+      uint32_t fx = 0u;
+      ydm = yum = 0u;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        ap[j] = ap2[j] = cen2[j] = 0.0;
+        const int i = ib + j * L, r = cbase + m0 * P + i;
+        const uint32_t w = i < width && r < R1 ? __ldg(a.pbits + r) : 0u;
+        fx |= w;
+        ydm |= ((w >> 10) & 1u) << j;
+        yum |= ((w >> 16) & 1u) << j;
+      }
+      xl = (fx >> 12) & 1u;
+      xr = (fx >> 14) & 1u;
+      inner = __all_sync(0xffffffffu, xl && xr && ydm == (1u << R) - 1u && yum == (1u << R) - 1u);
+    }
+    mbar_wait(&full[sl], phase);
+    const unsigned char* stage = box_smem + sl * b.stage_bytes;
+    if (++sl == b.ns) {
+      sl = 0;
+      phase ^= 1u;
+    }
+    const int S = cbase + (k - 1) * P - L - 1;
+    const double* xb = reinterpret_cast<const double*>(stage) + (S & 1) + vg * R * L + vx;
+    const double* es = reinterpret_cast<const double*>(stage + 8 * b.xs);
+    const bool zl = k > 0 || b.zl_first, zu = k - 2 < b.zplast || b.zu_last;
+    double ls[R + 2], cm[R + 2];
+    if (inner) {
+#pragma unroll
+      for (int l = 0; l < R + 2; ++l) {
+        const double x0 = xb[l * L], x1 = xb[l * L + 1], x2 = xb[l * L + 2];
+        cm[l] = x1;
+        ls[l] = (x0 + x1) + x2;
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < R + 2; ++l) {
+        const double x0 = xb[l * L], x1 = xb[l * L + 1], x2 = xb[l * L + 2];
+        cm[l] = x1;
+        const double tt = xl ? x0 + x1 : x1;
+        ls[l] = xr ? tt + x2 : tt;
+      }
+    }
+    double acc0[R], acc1[R], acc2[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double bs = ls[j + 1];
+      if (inner) {
+        bs += ls[j];
+        bs += ls[j + 2];
+      } else {
+        if ((ydm >> j) & 1u) bs += ls[j];
+        if ((yum >> j) & 1u) bs += ls[j + 2];
+      }
+      acc0[j] = bs;
+      acc1[j] = ap[j] + bs;
+      acc2[j] = ap2[j] + bs;
+    }
+    if (!zl)  // the launch's first plane has no lower neighbour plane
+#pragma unroll
+      for (int j = 0; j < R; ++j) acc0[j] = 0.0;
+    if (!zu)  // the plane k-2 row has no upper neighbour plane
+#pragma unroll
+      for (int j = 0; j < R; ++j) acc2[j] = ap2[j];
+    // epilogue: rows of plane k-2 complete
+    const int rb2 = cbase + (k - 2) * P;
+    const int lim_2 = k - 2 >= m0 ? max(0, min(width, end2 - rb2)) : 0;
+    const bool edge = push && (rb2 < g.send_lo || rb2 + width > g.hi_begin);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int i = ib + j * L;
+      const double y = fma(dp1, cen2[j], -acc2[j]);  // (a_ii + 1) x_c - S
+      if (i < lim_2) {
+        const int64_t row = rb2 + i;
+        if constexpr (KIND == kDot) {
+          g.y[row] = y;
+          dotv += cen2[j] * y;
+        } else {
+          double z;
+          if constexpr (KIND == kResidF) {
+            const double r = es[i] - y;
+            g.y[row] = r;
+            z = JAC ? r * einv : r;
+          } else {
+            if (g.y) g.y[row] = y;
+            const double dp = JAC ? y * einv : y;
+            z = fma(cb, cen2[j], ca * dp);
+            if constexpr (KIND == kMpkMidF) z = fma(cc, es[i], z);
+          }
+          g.zout[row] = z;
+          bad |= !isfinite(z);
+          if constexpr (kPush)
+            if (edge) halo_push_row(g, row, z);
+        }
+      }
+      ap2[j] = acc1[j];
+      cen2[j] = cm[j + 1];
+      ap[j] = acc0[j];
+    }
+    __syncthreads();
+  }
+  if (bad) report(g, g.col);
+  if constexpr (KIND == kDot) dot_finish<CS_BOX_THREADS / 32>(g, dotv);
+}
+
 #ifndef CS_BOX_MINB
 #define CS_BOX_MINB 1
 #endif
@@ -1135,6 +1302,18 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(items, 148 * per_sm)));
+    if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF || KIND == kDot) {
+      const char* sk_e = std::getenv("CS_BOX_SEPK");
+      const bool sk_env = sk_e == nullptr || std::atoi(sk_e) != 0;
+      if (sk_env && b.sep && b.nobits && b.vstrip) {
+        auto sk = jac ? sell_boxsep_kernel<KIND, true> : sell_boxsep_kernel<KIND, false>;
+        const int per = kernel_setup(reinterpret_cast<const void*>(sk), CS_BOX_THREADS, smem);
+        const unsigned sgrid = static_cast<unsigned>(
+            std::max<int64_t>(1, std::min<int64_t>(items, 148 * per)));
+        sk<<<sgrid, CS_BOX_THREADS, smem, st>>>(a, g, b, t);
+        return true;
+      }
+    }
     kern<<<grid, CS_BOX_THREADS, smem, st>>>(a, g, b, t);
     return true;
   }

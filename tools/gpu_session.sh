@@ -28,10 +28,13 @@ for step in "$@"; do
     tests_quick)
       timeout 1200 python -m pytest tests/test_gpu_box.py tests/test_gpu_solver.py tests/test_gpu_kernels.py -q -x -m "gpu and not slow" > $out/${tag}_tests_quick.log 2>&1 ;;
     ncu_boxlz)
-      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"sell_box_kernel<7" -s 20 -c 1 \
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"sell_box_kernel<.int.7" -s 20 -c 1 \
         -o $out/${tag}_box python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_box.log 2>&1
-      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"lz2_resid_proj_kernel<24" -s 2 -c 1 \
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"lz2_resid_proj_kernel<.int.24" -s 2 -c 1 \
         -o $out/${tag}_lz python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_lz.log 2>&1 ;;
+    ncu_sep)
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"sell_boxsep_kernel<.int.7" -s 20 -c 1 \
+        -o $out/${tag}_sep python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_sep.log 2>&1 ;;
     trband)
       timeout 2400 python tools/count_band.py --ref-only --variants 0,256 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4 --out $out/${tag}_trband.json > $out/${tag}_trband.log 2>&1
       timeout 1800 python tools/count_band.py --skip-ref --variants 0,256 --cases p27:256:8,p27:512:8 --out $out/${tag}_trband.json >> $out/${tag}_trband.log 2>&1 ;;

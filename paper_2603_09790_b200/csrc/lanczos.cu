@@ -165,10 +165,13 @@ __global__ void __launch_bounds__(kThreads)
   for (int c = 0; c < MB; ++c) acc[c] = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    double gg[MB];  // every load of the row in flight before the FMA chain
+#pragma unroll
+    for (int c = 0; c < MB; ++c) gg[c] = c < m ? __ldcs(G + c * ld + i) : 0.0;
     const double rv = __ldcs(r + i);
 #pragma unroll
     for (int c = 0; c < MB; ++c)
-      if (c < m) acc[c] = fma(__ldcs(G + c * ld + i), rv, acc[c]);
+      if (c < m) acc[c] = fma(gg[c], rv, acc[c]);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -220,13 +223,22 @@ __global__ void __launch_bounds__(kThreads)
   for (int c = 0; c < MB; ++c) acc[c] = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
-    double gv = fma(-a, __ldg(G + j * ld + i), __ldcs(t + i));
-    if (j > 0) gv = fma(-b, __ldg(G + (j - 1) * ld + i), gv);
+    // every basis load of the row first (ncu: with the loads interleaved into
+    // the FMA chain one load was in flight per thread, 2.2 TB/s)
+    double gg[MB];
+    const double* gi = G + i;
+#pragma unroll
+    for (int c = 0; c < MB; ++c) gg[c] = c < m ? __ldcs(gi + c * ld) : 0.0;
+    const double tv = __ldcs(t + i);
+    const double di = dinv ? __ldg(dinv + i) : dconst;
+    const double gj = __ldg(gi + j * ld), gj1 = j > 0 ? __ldg(gi + (j - 1) * ld) : 0.0;
+    double gv = fma(-a, gj, tv);
+    if (j > 0) gv = fma(-b, gj1, gv);
     gr[i] = gv;
-    const double rv = gv * (dinv ? __ldg(dinv + i) : dconst);
+    const double rv = gv * di;
 #pragma unroll
     for (int c = 0; c < MB; ++c)
-      if (c < m) acc[c] = fma(__ldcs(G + c * ld + i), rv, acc[c]);
+      if (c < m) acc[c] = fma(gg[c], rv, acc[c]);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll

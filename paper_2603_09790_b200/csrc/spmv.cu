@@ -538,6 +538,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -836,8 +839,12 @@ __device__ __forceinline__ void box_terms_sep(const double* xs, int L, uint32_t 
 // finite check is one flag reported at the end (same error word), and the
 // push test is per stage. ncu on the general kernel: 107 instructions per row,
 // ALU pipe 56 %, issue-bound at 58 % of HBM (profiles/r02h_ncu_box_*.txt).
-template <int KIND, bool JAC>
-__global__ void __launch_bounds__(CS_BOX_THREADS, 1)
+// WS: warp-specialised ring -- one extra producer warp issues the bulk copies
+// as soon as every consumer warp has released the slot (an "empty" mbarrier per
+// slot, one arrive per consumer warp) instead of thread 0 issuing them between
+// block-wide barriers (ncu: barrier stalls and warp 0 lagging every stage).
+template <int KIND, bool JAC, bool WS>
+__global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
     sell_boxsep_kernel(SellView a, SpmvArgs g, BoxGeom b, const __grid_constant__ CdiaTable t) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
   halo_release(g);
@@ -852,6 +859,8 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
   extern __shared__ __align__(128) unsigned char box_smem[];
   __shared__ __align__(8) uint64_t full[CS_BOX_NS];
+  __shared__ __align__(8) uint64_t empty[WS ? CS_BOX_NS : 1];
+  constexpr int kCW = CS_BOX_THREADS / 32;  // consumer warps
   const int64_t items = b.ncols * b.nplanes;
   const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
   BoxIter cur{i0, i1}, pre{i0, i1};
@@ -859,12 +868,37 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
   pre.seg(b);
   int psl = 0;
   if (threadIdx.x == 0) {
-    for (int sl = 0; sl < b.ns; ++sl) mbar_init(&full[sl], 1);
+    for (int sl = 0; sl < b.ns; ++sl) {
+      mbar_init(&full[sl], 1);
+      if constexpr (WS) mbar_init(&empty[sl], kCW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (; psl < b.ns - 1 && pre.valid; ++psl, pre.next(b))
-      box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
+    if constexpr (!WS)
+      for (; psl < b.ns - 1 && pre.valid; ++psl, pre.next(b))
+        box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
   }
   __syncthreads();
+  double dotv = 0.0;
+  if constexpr (WS) {
+    if (threadIdx.x >= CS_BOX_THREADS) {  // producer warp: lane 0 streams every stage
+      if (threadIdx.x == CS_BOX_THREADS) {
+        int slot = 0;
+        uint32_t eph = 0;
+        for (int n = 0; pre.valid; pre.next(b), ++n) {
+          if (n >= b.ns) mbar_wait(&empty[slot], eph);  // all consumers left this slot
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          box_issue<kE2, kBsrc>(b, a, g, box_smem + slot * b.stage_bytes, &full[slot], pre.c, pre.k,
+                                pre.m1);
+          if (++slot == b.ns) {
+            slot = 0;
+            if (n >= b.ns) eph ^= 1u;
+          }
+        }
+      }
+      if constexpr (KIND == kDot) dot_finish<kCW + 1>(g, dotv);
+      return;
+    }
+  }
   const int R0 = static_cast<int>(b.R0), R1 = static_cast<int>(b.R1), P = static_cast<int>(b.P);
   const int L = static_cast<int>(b.L);
   const int end2 = static_cast<int>(b.R1 < b.n_local ? b.R1 : b.n_local);
@@ -875,11 +909,10 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
   bool xl = false, xr = false, inner = false;
   uint32_t ydm = 0u, yum = 0u;  // bit j: row j has its lower / upper line
   bool bad = false;
-  double dotv = 0.0;
   int sl = 0;
   uint32_t phase = 0;
   for (; cur.valid; cur.next(b)) {
-    if (threadIdx.x == 0 && pre.valid) {
+    if (!WS && threadIdx.x == 0 && pre.valid) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       box_issue<kE2, kBsrc>(b, a, g, box_smem + psl * b.stage_bytes, &full[psl], pre.c, pre.k, pre.m1);
       pre.next(b);
@@ -906,6 +939,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
     }
     mbar_wait(&full[sl], phase);
     const unsigned char* stage = box_smem + sl * b.stage_bytes;
+    const int slot = sl;
     if (++sl == b.ns) {
       sl = 0;
       phase ^= 1u;
@@ -987,10 +1021,16 @@ __global__ void __launch_bounds__(CS_BOX_THREADS, 1)
       cen2[j] = cm[j + 1];
       ap[j] = acc0[j];
     }
-    __syncthreads();
+    if constexpr (WS) {  // this warp's reads of the slot are done (arrive = release)
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+    } else {
+      (void)slot;
+      __syncthreads();
+    }
   }
   if (bad) report(g, g.col);
-  if constexpr (KIND == kDot) dot_finish<CS_BOX_THREADS / 32>(g, dotv);
+  if constexpr (KIND == kDot) dot_finish<kCW + (WS ? 1 : 0)>(g, dotv);
 }
 
 #ifndef CS_BOX_MINB
@@ -1306,11 +1346,15 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
       const char* sk_e = std::getenv("CS_BOX_SEPK");
       const bool sk_env = sk_e == nullptr || std::atoi(sk_e) != 0;
       if (sk_env && b.sep && b.nobits && b.vstrip) {
-        auto sk = jac ? sell_boxsep_kernel<KIND, true> : sell_boxsep_kernel<KIND, false>;
-        const int per = kernel_setup(reinterpret_cast<const void*>(sk), CS_BOX_THREADS, smem);
+        const char* ws_e = std::getenv("CS_BOX_WS");
+        const bool ws = ws_e == nullptr || std::atoi(ws_e) != 0;
+        auto sk = ws ? (jac ? sell_boxsep_kernel<KIND, true, true> : sell_boxsep_kernel<KIND, false, true>)
+                     : (jac ? sell_boxsep_kernel<KIND, true, false> : sell_boxsep_kernel<KIND, false, false>);
+        const int nthr = CS_BOX_THREADS + (ws ? 32 : 0);
+        const int per = kernel_setup(reinterpret_cast<const void*>(sk), nthr, smem);
         const unsigned sgrid = static_cast<unsigned>(
             std::max<int64_t>(1, std::min<int64_t>(items, 148 * per)));
-        sk<<<sgrid, CS_BOX_THREADS, smem, st>>>(a, g, b, t);
+        sk<<<sgrid, nthr, smem, st>>>(a, g, b, t);
         return true;
       }
     }

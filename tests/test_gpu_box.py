@@ -18,9 +18,10 @@ SHAPES = [(64, 64, 40), (70, 50, 13), (40, 36, 30), (5, 4, 7), (128, 96, 9), (33
           (16, 40, 12), (256, 9, 7)]
 
 
-def _solve(cs, p, lam, box, sep=True, nobits=True, variant=0, vstrip=True):
+def _solve(cs, p, lam, box, sep=True, nobits=True, variant=0, vstrip=True, sepk=True, ws=True):
     env = {"CS_SPMV_BOX": "1" if box else "0", "CS_BOX_SEP": "1" if sep else "0",
-           "CS_BOX_NOBITS": "1" if nobits else "0", "CS_BOX_VSTRIP": "1" if vstrip else "0"}
+           "CS_BOX_NOBITS": "1" if nobits else "0", "CS_BOX_VSTRIP": "1" if vstrip else "0",
+           "CS_BOX_SEPK": "1" if sepk else "0", "CS_BOX_WS": "1" if ws else "0"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -71,5 +72,10 @@ def test_box_spmv_bitwise_and_solve_identical(cs, port, dims):
             for nb in (True, False):
                 c = _solve(cs, p, lam, True, nobits=nb, variant=variant, vstrip=False)
                 assert c[1] == a[1] and c[0].tobytes() == a[0].tobytes(), (variant, nb)
+            # the compile-time specialised planar kernel (with and without its
+            # producer warp) vs the general kernel's separable path
+            for sepk, ws in ((False, True), (True, False)):
+                c = _solve(cs, p, lam, True, variant=variant, sepk=sepk, ws=ws)
+                assert c[1] == a[1] and c[0].tobytes() == a[0].tobytes(), (variant, sepk, ws)
     finally:
         p.close()

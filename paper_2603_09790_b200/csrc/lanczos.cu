@@ -323,7 +323,9 @@ __global__ void lz2_scale_kernel(int64_t n, const double* __restrict__ gr,
   if (halted(st)) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double gv = __ddiv_rn(gr[i], sc->denom);
+  // one reciprocal per step, not a division per row (fast mode only; the
+  // reference-order Lanczos keeps its divisions)
+  const double gv = gr[i] * sc->rdenom;
   g[i] = gv;
   v[i] = gv * (dinv ? dinv[i] : dconst);
 }
@@ -341,6 +343,7 @@ __global__ void scalar_kernel(int which, int j, int steps, LanczosScalars* sc, D
       return;
     }
     sc->denom = nrm;
+    sc->rdenom = 1.0 / nrm;
   } else if (which == 1) {
     if (!isfinite(d)) {
       atomicCAS(&st->err, 0ull, make_err(9 | (2 << 8), j));
@@ -363,6 +366,7 @@ __global__ void scalar_kernel(int which, int j, int steps, LanczosScalars* sc, D
     if (j + 1 < steps) {
       sc->beta[j] = bj;
       sc->denom = bj;
+      sc->rdenom = 1.0 / bj;
     } else {
       st->done = 1;
     }

@@ -12,6 +12,7 @@ struct LanczosScalars {
   double proj[kLanczosMax];
   double dot;    // last reduced scalar
   double denom;  // normaliser of the next basis pair
+  double rdenom; // 1 / denom (the fast G-only scale multiplies)
   int count;     // completed alpha entries
 };
 

@@ -35,6 +35,8 @@ for step in "$@"; do
     ncu_sep)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"sell_boxsep_kernel<.int.7" -s 20 -c 1 \
         -o $out/${tag}_sep python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_sep.log 2>&1 ;;
+    abws)
+      timeout 1500 bash tools/ab_env.sh "CS_BOX_WS=0" "CS_BOX_WS=1" "CS_BOX_WS=0" "CS_BOX_WS=1" > $out/${tag}_abws.txt 2>&1 ;;
     trband)
       timeout 2400 python tools/count_band.py --ref-only --variants 0,256 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4 --out $out/${tag}_trband.json > $out/${tag}_trband.log 2>&1
       timeout 1800 python tools/count_band.py --skip-ref --variants 0,256 --cases p27:256:8,p27:512:8 --out $out/${tag}_trband.json >> $out/${tag}_trband.log 2>&1 ;;

@@ -843,7 +843,9 @@ __device__ __forceinline__ void box_terms_sep(const double* xs, int L, uint32_t 
 // as soon as every consumer warp has released the slot (an "empty" mbarrier per
 // slot, one arrive per consumer warp) instead of thread 0 issuing them between
 // block-wide barriers (ncu: barrier stalls and warp 0 lagging every stage).
-template <int KIND, bool JAC, bool WS>
+// LC > 0: the line length as a compile-time constant (256, 512: the row offsets
+// of a strip become immediate address offsets)
+template <int KIND, bool JAC, bool WS, int LC>
 __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
     sell_boxsep_kernel(SellView a, SpmvArgs g, BoxGeom b, const __grid_constant__ CdiaTable t) {
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
@@ -900,7 +902,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
     }
   }
   const int R0 = static_cast<int>(b.R0), R1 = static_cast<int>(b.R1), P = static_cast<int>(b.P);
-  const int L = static_cast<int>(b.L);
+  const int L = LC > 0 ? LC : static_cast<int>(b.L);
   const int end2 = static_cast<int>(b.R1 < b.n_local ? b.R1 : b.n_local);
   const int vx = static_cast<int>(threadIdx.x) % L, vg = static_cast<int>(threadIdx.x) / L;
   const int ib = vg * R * L + vx;  // column row of this thread's line j: ib + j L
@@ -990,11 +992,15 @@ __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
     const int rb2 = cbase + (k - 2) * P;
     const int lim_2 = k - 2 >= m0 ? max(0, min(width, end2 - rb2)) : 0;
     const bool edge = push && (rb2 < g.send_lo || rb2 + width > g.hi_begin);
+    // a full column of live rows (the common case): no per-row bound test
+    const int lim = lim_2 == kBoxT ? 0x7fffffff : lim_2;
+    double* const ybase = g.y != nullptr ? g.y + rb2 : nullptr;
+    double* const zbase = g.zout + rb2;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int i = ib + j * L;
       const double y = fma(dp1, cen2[j], -acc2[j]);  // (a_ii + 1) x_c - S
-      if (i < lim_2) {
+      if (i < lim) {
         const int64_t row = rb2 + i;
         if constexpr (KIND == kDot) {
           g.y[row] = y;
@@ -1003,15 +1009,15 @@ __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
           double z;
           if constexpr (KIND == kResidF) {
             const double r = es[i] - y;
-            g.y[row] = r;
+            ybase[i] = r;
             z = JAC ? r * einv : r;
           } else {
-            if (g.y) g.y[row] = y;
+            if (ybase) ybase[i] = y;
             const double dp = JAC ? y * einv : y;
             z = fma(cb, cen2[j], ca * dp);
             if constexpr (KIND == kMpkMidF) z = fma(cc, es[i], z);
           }
-          g.zout[row] = z;
+          zbase[i] = z;
           bad |= !isfinite(z);
           if constexpr (kPush)
             if (edge) halo_push_row(g, row, z);
@@ -1348,8 +1354,12 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
       if (sk_env && b.sep && b.nobits && b.vstrip) {
         const char* ws_e = std::getenv("CS_BOX_WS");
         const bool ws = ws_e == nullptr || std::atoi(ws_e) != 0;
-        auto sk = ws ? (jac ? sell_boxsep_kernel<KIND, true, true> : sell_boxsep_kernel<KIND, false, true>)
-                     : (jac ? sell_boxsep_kernel<KIND, true, false> : sell_boxsep_kernel<KIND, false, false>);
+        const int lc = b.L == 512 ? 512 : b.L == 256 ? 256 : 0;
+#define CSG_SK(W, LCV)                                                                 \
+  (jac ? sell_boxsep_kernel<KIND, true, W, LCV> : sell_boxsep_kernel<KIND, false, W, LCV>)
+        auto sk = ws ? (lc == 512 ? CSG_SK(true, 512) : lc == 256 ? CSG_SK(true, 256) : CSG_SK(true, 0))
+                     : (lc == 512 ? CSG_SK(false, 512) : lc == 256 ? CSG_SK(false, 256) : CSG_SK(false, 0));
+#undef CSG_SK
         const int nthr = CS_BOX_THREADS + (ws ? 32 : 0);
         const int per = kernel_setup(reinterpret_cast<const void*>(sk), nthr, smem);
         const unsigned sgrid = static_cast<unsigned>(

@@ -401,9 +401,12 @@ def run_ours(args):
         "reduce": outers_t * v8 * ((2 * args.s + 2) if pz else (3 * args.s + 1))
         + len(reps_t) * v8 * (3 * args.s + 1),
     }
-    names = {"spmv": "sell_box_kernel<kMpk*> (plane-streaming FP64 SpMV over the 3x3x3 constant-"
-                     "diagonal class: bulk-copied plane stages, fused MPK epilogue; gather "
-                     "kernels for other classes)",
+    names = {"spmv": ("sell_boxsep_kernel<kMpk*/kResidF> (planar 27-point class: separable plane "
+                      "sums over bulk-copied plane stages, producer warp + mbarrier ring, fused "
+                      "MPK / residual epilogue)" if prob.cdia_planar and args.mode == "fast" else
+                      "sell_box_kernel<kMpk*> (plane-streaming FP64 SpMV over the 3x3x3 constant-"
+                      "diagonal class: bulk-copied plane stages, fused MPK epilogue; gather "
+                      "kernels for other classes)"),
              "update": ("update_tr_kernel<s,beta> (Q, x update pass; r from the residual SpMV)"
                         if tr else "update_kernel<s,beta,xr,z0> (Q, AQ, x, r, z_0 update pass)"),
              "reduce": "pack_kernel<s> (packed Gram/projection block, DMMA)"}

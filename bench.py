@@ -138,7 +138,7 @@ def nnz_of(stencil, nx, ny, nz):
 
 
 def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=True,
-                   diag_stream=True, pz=False, tr=False, mat_fast=None):
+                   diag_stream=True, pz=False, tr=False, mat_fast=None, rz=False):
     """Algorithmic bytes of every SpMV-phase kernel of one solve:
     the matrix in the format actually stored (SELL-32P: FP64 value slots +
     per-slice column/pattern/meta bytes; CDIA: 32-bit participation words) read
@@ -163,8 +163,8 @@ def spmv_alg_bytes(mat_bytes, n, s, outer, lanczos_steps, mode="fast", jacobi=Tr
     setup_mpk = per_mpk  # the setup MPK always stores P (it becomes AQ_1)
     if pz and mode == "fast":  # no p_q written; the last step writes z_s (a mid-type step)
         per_mpk = (b_first - v) if s == 1 else (b_first - v) + (s - 1) * (b_mid - v)
-    if tr and mode == "fast":  # x, b read; r, z_0 written (+ D^-1)
-        per_mpk += mf + 4 * v + j
+    if tr and mode == "fast":  # x, b read; r (unless formed from z_0 by the pack), z_0 written
+        per_mpk += mf + (3 if rz else 4) * v + j
     # setup MPK + one (speculative) MPK per outer iteration (fast algebra)
     return b_resid + lanczos_steps * b_dot + outer * per_mpk + setup_mpk, b_spmv
 
@@ -178,7 +178,8 @@ def update_vectors(s, pz, tr, diag_stream):
     return (5 if pz else 6) * s + (6 if diag_stream else 5)
 
 
-def outer_bytes_format(mat_bytes, n, s, diag_stream=True, pz=False, tr=False, mat_fast=None):
+def outer_bytes_format(mat_bytes, n, s, diag_stream=True, pz=False, tr=False, mat_fast=None,
+                       rz=False):
     """Per-outer algorithmic bytes of the fast schedule in the stored format:
     s SpMV/MPK steps + packed reduction 8n(3s+1) + update pass 8n(6s+6).
     PZ schedule (P derived from Z): MPK steps write no p (the last writes z_s),
@@ -190,8 +191,8 @@ def outer_bytes_format(mat_bytes, n, s, diag_stream=True, pz=False, tr=False, ma
     if pz:
         mpk = (mf + 2 * v + j) + (s - 1) * (mf + 3 * v + j)
         if tr:
-            mpk += mf + 4 * v + j
-        return mpk + v * (2 * s + 2) + v * update_vectors(s, pz, tr, diag_stream)
+            mpk += mf + (3 if rz else 4) * v + j
+        return mpk + v * (2 * s + (1 if rz else 2)) + v * update_vectors(s, pz, tr, diag_stream)
     mpk = (mf + 3 * v + j) + (s - 2) * (mf + 4 * v + j) + (mat_bytes + 2 * v) \
         if s > 1 else mat_bytes + 2 * v
     return mpk + v * (3 * s + 1) + v * update_vectors(s, pz, False, diag_stream)
@@ -382,23 +383,24 @@ def run_ours(args):
     dstream = not prob.cdia_uniform_diag  # CDIA: 1/a_ii is a kernel constant
     pz = bool(rep.schedule & 1)  # CS_SCHED_P_FROM_Z
     tr = bool(rep.schedule & 4)  # CS_SCHED_TRUE_R
+    rz = bool(rep.schedule & 8)  # CS_SCHED_R_FROM_Z0
     # planar CDIA classes: the separable fast kinds read no participation words
     mat_f = 0 if (prob.cdia_planar and args.mode == "fast") else mat
     alg, b_spmv = spmv_alg_bytes(mat, nl, args.s, rep.outer_iters, cfg.lanczos_steps, args.mode,
-                                 diag_stream=dstream, pz=pz, tr=tr, mat_fast=mat_f)
+                                 diag_stream=dstream, pz=pz, tr=tr, mat_fast=mat_f, rz=rz)
     v8 = 8 * nl
     outers_t = sum(r.outer_iters for r in reps_t)
     upd_vec = update_vectors(args.s, pz, tr, dstream)
     alg_phase = {
         "spmv": sum(spmv_alg_bytes(mat, nl, args.s, r.outer_iters, cfg.lanczos_steps,
                                    args.mode, diag_stream=dstream, pz=pz, tr=tr,
-                                   mat_fast=mat_f)[0] for r in reps_t),
+                                   mat_fast=mat_f, rz=rz)[0] for r in reps_t),
         # recursive residual: Q, Z, AQ, P (PZ: Z + z_s instead of P), x, r (+ D^-1
         # unless uniform) read; Q, AQ, x, r, z_0 written. True residual: Q, Z, x
         # read; Q, x written
         "update": outers_t * v8 * upd_vec,
         # Q, Z, P, r read once (PZ: Q, Z, z_s, r); one launch per outer + the setup one
-        "reduce": outers_t * v8 * ((2 * args.s + 2) if pz else (3 * args.s + 1))
+        "reduce": outers_t * v8 * ((2 * args.s + (1 if rz else 2)) if pz else (3 * args.s + 1))
         + len(reps_t) * v8 * (3 * args.s + 1),
     }
     names = {"spmv": ("sell_boxsep_kernel<kMpk*/kResidF> (planar 27-point class: separable plane "
@@ -440,7 +442,7 @@ def run_ours(args):
             "survey_B_spmv_12B_per_nnz": 12 * nnz_l + 16 * nl}
     # whole-solve bandwidth against B_outer
     solve_outer_ms = rep.t_solve_ms / max(rep.outer_iters, 1)
-    b_out = outer_bytes_format(mat, nl, args.s, dstream, pz, tr, mat_f)
+    b_out = outer_bytes_format(mat, nl, args.s, dstream, pz, tr, mat_f, rz)
     b_survey = outer_bytes(nnz_l, nl, args.s)
     solve_level = {"t_outer_ms": solve_outer_ms, "B_outer_GB": b_out / 1e9,
                    "achieved_GBps": b_out / (solve_outer_ms / 1e3) / 1e9,

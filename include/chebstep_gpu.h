@@ -124,6 +124,7 @@ typedef struct {
                                  SpMV instead of r_k - AQ alpha (no AQ block) --
                                  the default wherever the PZ schedule runs; the bit is accepted */
 #define CS_VAR_RECUR_R 256    /* fast: the recursive residual r_k - AQ alpha (AQ block kept) */
+#define CS_VAR_STORED_R 512   /* fast, true residual: store r (default: the pack forms r = D z_0) */
 
 typedef struct {
   /* SolveReport (solver.hpp:39-68), reference semantics */
@@ -156,6 +157,7 @@ typedef struct {
 #define CS_SCHED_P_FROM_Z 1   /* P derived from Z (no P stream) */
 #define CS_SCHED_EXPLICIT_W 2 /* W_k reduced from the vectors each outer */
 #define CS_SCHED_TRUE_R 4     /* r from b - A x each outer (no AQ block) */
+#define CS_SCHED_R_FROM_Z0 8  /* r not stored: the pack forms r = D z_0 */
 
 /* ------------------------------------------------------------ errors / info */
 const char* cs_last_error(int* payload);

@@ -35,7 +35,7 @@ CS_GEN_POISSON27, CS_GEN_STENCIL7 = 0, 1
 CS_GRAM_FGS, CS_GRAM_CHOLESKY = 0, 1
 CS_MODE_FAST, CS_MODE_REFERENCE = 0, 1
 CS_VAR_EXPLICIT_W, CS_VAR_RECUR_W, CS_VAR_REF_FGS, CS_VAR_REF_MPK, CS_VAR_TREE = 1, 2, 4, 8, 16
-CS_VAR_P_FROM_Z, CS_VAR_P_STORED, CS_VAR_TRUE_R, CS_VAR_RECUR_R = 32, 64, 128, 256
+CS_VAR_P_FROM_Z, CS_VAR_P_STORED, CS_VAR_TRUE_R, CS_VAR_RECUR_R, CS_VAR_STORED_R = 32, 64, 128, 256, 512
 PHASES = ("spmv", "reduce", "small", "update", "lanczos", "comm", "other")
 
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")

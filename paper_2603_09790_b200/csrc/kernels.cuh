@@ -174,6 +174,9 @@ struct PzArgs {
   double k1 = 0.0, k2 = 0.0;      // 1/alpha, 1/(2 alpha)
   double dconst = 1.0;            // the uniform diagonal a_ii (Jacobi), 1 (identity)
   const double* diag = nullptr;   // non-uniform Jacobi: the diagonal a_ii (else nullptr)
+  // true-residual schedule: the pack forms r = D z_0 (z_0 = D^-1 r, Z column 0)
+  // instead of reading r, which the residual SpMV then does not store
+  int r_from_z0 = 0;
 };
 #ifdef __CUDACC__
 // zz[0..S] = z_0 .. z_S of one row; p[j] = column j of P; the same arithmetic

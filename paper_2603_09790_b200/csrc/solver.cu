@@ -830,6 +830,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   ua.p = bk.P;
   if (pz_on) {  // after the setup MPK the P block is free: it holds z_s from now on
     pz.zs = bk.P;
+    // true residual: r is not stored, the pack forms it as D z_0 (CS_VAR_STORED_R keeps it)
+    pz.r_from_z0 = tr_on && (var & CS_VAR_STORED_R) == 0 ? 1 : 0;
     ua.pz = pz;
   }
   if (mode == CS_MODE_FAST) {
@@ -851,7 +853,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   auto residual_z0 = [&](bool peer) {
     SpmvArgs g;
     g.x = bk.x;
-    g.y = bk.r;
+    g.y = pz.r_from_z0 ? nullptr : bk.r;
     g.b = bk.b;
     g.zout = bk.Z;
     g.col = 0;
@@ -1027,7 +1029,7 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   rep->t_lanczos_ms = t_lz;
   rep->t_solve_ms = t_solve;
   rep->schedule = (pz_on ? CS_SCHED_P_FROM_Z : 0) | (explicit_w ? CS_SCHED_EXPLICIT_W : 0) |
-                  (tr_on ? CS_SCHED_TRUE_R : 0);
+                  (tr_on ? CS_SCHED_TRUE_R : 0) | (pz.r_from_z0 ? CS_SCHED_R_FROM_Z0 : 0);
   trace.mark("report");
 }
 

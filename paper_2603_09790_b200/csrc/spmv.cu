@@ -244,7 +244,7 @@ __device__ __forceinline__ void epi_store(const SpmvArgs& g, int64_t row, double
     g.y[row] = __dsub_rn(e.e1, acc);
   } else if constexpr (KIND == kResidF) {
     const double r = e.e1 - acc;
-    g.y[row] = r;
+    if (g.y) g.y[row] = r;  // nullptr: the pack forms r = D z_0
     const double z = JAC ? r * e.einv : r;
     g.zout[row] = z;
     zv = z;
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
           double z;
           if constexpr (KIND == kResidF) {
             const double r = es[i] - y;
-            ybase[i] = r;
+            if (ybase) ybase[i] = r;  // nullptr: the pack forms r = D z_0
             z = JAC ? r * einv : r;
           } else {
             if (ybase) ybase[i] = y;

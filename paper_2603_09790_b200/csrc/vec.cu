@@ -323,7 +323,13 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
         pv[i] = ok ? __ldcs(P + i * ld + row) : 0.0;
       }
     }
-    const double rv = ok ? __ldcs(r + row) : 0.0;
+    double rv;
+    if constexpr (PZ) {
+      const double di = pz.diag ? (ok ? __ldg(pz.diag + row) : 1.0) : pz.dconst;
+      rv = pz.r_from_z0 ? (ok ? zv[0] * di : 0.0) : (ok ? __ldcs(r + row) : 0.0);
+    } else {
+      rv = ok ? __ldcs(r + row) : 0.0;
+    }
     rr = fma(rv, rv, rr);
 #pragma unroll
     for (int i = 0; i < S; ++i) {

@@ -94,7 +94,7 @@ FAST_CASES = [
 
 # fast schedules: the recursive residual r_k - AQ alpha (AQ block kept) and the
 # true residual b - A x_k from one SpMV per outer (no AQ block)
-VARIANTS = [("recursive_r", 256), ("true_r", 128)]
+VARIANTS = [("recursive_r", 256), ("true_r", 128), ("true_r_stored", 128 | 512)]
 
 
 @pytest.mark.parametrize("variant", [v[1] for v in VARIANTS], ids=[v[0] for v in VARIANTS])
@@ -280,7 +280,8 @@ def test_fast_mode_vs_golden_counts(cs, case, stencil, n, s, variant):
     p = cs.DeviceProblem.generate("poisson27" if stencil == 27 else "poisson7", n, n, n)
     p.set_precond("jacobi")
     res = p.pcg_s_solve(cfg=cs.SolverConfig(s=s, tol=1e-8, max_outer=5000, variant=variant))
-    assert bool(res.report.schedule & 4) == (variant == 128)  # CS_SCHED_TRUE_R
+    assert bool(res.report.schedule & 4) == bool(variant & 128)  # CS_SCHED_TRUE_R
+    assert bool(res.report.schedule & 8) == (variant == 128)  # CS_SCHED_R_FROM_Z0
     rep = res.report
     assert rep.converged
     if lo == hi:

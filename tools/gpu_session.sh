@@ -37,6 +37,13 @@ for step in "$@"; do
         -o $out/${tag}_sep python bench.py --grid 256 --steps 1 --warmup 0 --no-e2e --no-cpu --no-pcg > $out/${tag}_ncu_sep.log 2>&1 ;;
     abws)
       timeout 1500 bash tools/ab_env.sh "CS_BOX_WS=0" "CS_BOX_WS=1" "CS_BOX_WS=0" "CS_BOX_WS=1" > $out/${tag}_abws.txt 2>&1 ;;
+    abrz)
+      for v in 512 0 512 0; do
+        timeout 600 python bench.py --grid 256 --steps 3 --warmup 3 --no-e2e --no-cpu --no-pcg --variant $v 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['solve_roofline']
+print('variant $v', 'outer', d['config']['outer_iters'], 'ms/outer %.4f' % s['t_outer_ms'], 'lz %.1f' % s['t_lanczos_ms'], 'value %.5f' % d['value'], 'mhz', d['clocks']['sm_mhz'], d['phases_ms'])"
+      done > $out/${tag}_abrz.txt 2>&1 ;;
     trband)
       timeout 2400 python tools/count_band.py --ref-only --variants 0,256 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4 --out $out/${tag}_trband.json > $out/${tag}_trband.log 2>&1
       timeout 1800 python tools/count_band.py --skip-ref --variants 0,256 --cases p27:256:8,p27:512:8 --out $out/${tag}_trband.json >> $out/${tag}_trband.log 2>&1 ;;

@@ -14,7 +14,8 @@ import re
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HOT = ("sell_box_kernel", "sell_kernel", "sell_zb_kernel", "update_kernel", "update_gram_kernel",
+HOT = ("sell_boxsep_kernel", "update_tr_kernel", "lz2_resid_proj_kernel", "lz2_cgs_kernel",
+       "lz2_scale_kernel", "sell_box_kernel", "sell_kernel", "sell_zb_kernel", "update_kernel", "update_gram_kernel",
        "pack_kernel", "fast_step_kernel", "fast_setup_kernel", "proj_kernel", "cgs_kernel",
        "tree_gram_kernel", "resid_kernel", "bj_apply_kernel", "pcg_vec_kernel", "csr_fill_kernel")
 KEYS = ("DMMA", "DFMA", "DADD", "DMUL", "UBLKCP", "UTMALDG", "SYNCS", "LDG.E.128", "LDG.E.64",

@@ -843,6 +843,9 @@ __device__ __forceinline__ void box_terms_sep(const double* xs, int L, uint32_t 
 // as soon as every consumer warp has released the slot (an "empty" mbarrier per
 // slot, one arrive per consumer warp) instead of thread 0 issuing them between
 // block-wide barriers (ncu: barrier stalls and warp 0 lagging every stage).
+// ring slots of the planar kernel: its stages carry no participation words, so
+// up to kSepNS fit (CS_BOXSEP_NS, default 6; 4 for 512-line planes at T = 2048)
+constexpr int kSepNS = 8;
 // LC > 0: the line length as a compile-time constant (256, 512: the row offsets
 // of a strip become immediate address offsets)
 template <int KIND, bool JAC, bool WS, int LC>
@@ -860,8 +863,8 @@ __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
   constexpr int R = CS_BOX_ROWS;
   const bool push = kPush && (g.push_lo != nullptr || g.push_hi != nullptr);
   extern __shared__ __align__(128) unsigned char box_smem[];
-  __shared__ __align__(8) uint64_t full[CS_BOX_NS];
-  __shared__ __align__(8) uint64_t empty[WS ? CS_BOX_NS : 1];
+  __shared__ __align__(8) uint64_t full[kSepNS];
+  __shared__ __align__(8) uint64_t empty[WS ? kSepNS : 1];
   constexpr int kCW = CS_BOX_THREADS / 32;  // consumer warps
   const int64_t items = b.ncols * b.nplanes;
   const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
@@ -1361,10 +1364,16 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
                      : (lc == 512 ? CSG_SK(false, 512) : lc == 256 ? CSG_SK(false, 256) : CSG_SK(false, 0));
 #undef CSG_SK
         const int nthr = CS_BOX_THREADS + (ws ? 32 : 0);
-        const int per = kernel_setup(reinterpret_cast<const void*>(sk), nthr, smem);
+        // stage = x slice + the epilogue stream (no participation words): more slots
+        const char* ns_e = std::getenv("CS_BOXSEP_NS");
+        const int ns_want = std::min(kSepNS, std::max(2, ns_e ? std::atoi(ns_e) : 6));
+        b.stage_bytes = static_cast<uint32_t>(round_up(8 * b.xs + 8 * kBoxT, 128));
+        b.ns = std::min<int>(ns_want, kSmemMax / static_cast<int>(b.stage_bytes));
+        const int ssmem = b.ns * static_cast<int>(b.stage_bytes);
+        const int per = kernel_setup(reinterpret_cast<const void*>(sk), nthr, ssmem);
         const unsigned sgrid = static_cast<unsigned>(
             std::max<int64_t>(1, std::min<int64_t>(items, 148 * per)));
-        sk<<<sgrid, nthr, smem, st>>>(a, g, b, t);
+        sk<<<sgrid, nthr, ssmem, st>>>(a, g, b, t);
         return true;
       }
     }

@@ -844,7 +844,8 @@ __device__ __forceinline__ void box_terms_sep(const double* xs, int L, uint32_t 
 // slot, one arrive per consumer warp) instead of thread 0 issuing them between
 // block-wide barriers (ncu: barrier stalls and warp 0 lagging every stage).
 // ring slots of the planar kernel: its stages carry no participation words, so
-// up to kSepNS fit (CS_BOXSEP_NS, default 6; 4 for 512-line planes at T = 2048)
+// up to kSepNS fit (CS_BOXSEP_NS); measured at 256^3: 4 slots 312 ms of SpMV per
+// solve, 5: 317, 6: 328 (profiles/r02h_ab_ring_depth_256.txt) -- default 4
 constexpr int kSepNS = 8;
 // LC > 0: the line length as a compile-time constant (256, 512: the row offsets
 // of a strip become immediate address offsets)
@@ -1366,7 +1367,7 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
         const int nthr = CS_BOX_THREADS + (ws ? 32 : 0);
         // stage = x slice + the epilogue stream (no participation words): more slots
         const char* ns_e = std::getenv("CS_BOXSEP_NS");
-        const int ns_want = std::min(kSepNS, std::max(2, ns_e ? std::atoi(ns_e) : 6));
+        const int ns_want = std::min(kSepNS, std::max(2, ns_e ? std::atoi(ns_e) : 4));
         b.stage_bytes = static_cast<uint32_t>(round_up(8 * b.xs + 8 * kBoxT, 128));
         b.ns = std::min<int>(ns_want, kSmemMax / static_cast<int>(b.stage_bytes));
         const int ssmem = b.ns * static_cast<int>(b.stage_bytes);

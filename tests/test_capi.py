@@ -108,3 +108,15 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "cs_oracle" not in txt and "libchebstep_ref" not in txt, f
+
+
+def test_python_constants_match_header():
+    """Every CS_VAR_* / CS_MODE_* / CS_PRECOND_* value the Python mirror uses is
+    the header's (the schedule bits are checked by the GPU solver tests)."""
+    import re
+    from paper_2603_09790_b200 import _lib as L
+    hdr = open(os.path.join(ROOT, "include", "chebstep_gpu.h")).read()
+    defs = dict(re.findall(r"#define\s+(CS_VAR_\w+)\s+(\d+)", hdr))
+    assert defs, "no CS_VAR_* in the header"
+    for name, val in defs.items():
+        assert getattr(L, name) == int(val), name

@@ -37,7 +37,7 @@ if pinned_mode:
 b, x0 = np.ones(a.n), np.zeros(a.n)
 cfg = cs.SolverConfig(s=8, tol=1e-8, max_outer=50000)
 m = cs.JacobiPreconditioner(a)
-for i in range(3):
+for i in range(5):
     t0 = time.perf_counter()
     r = cs.pcg_s_solve(a, b, x0, m, cfg)
     print(f"e2e {time.perf_counter()-t0:.3f} s outer {r.report.outer_iters} "

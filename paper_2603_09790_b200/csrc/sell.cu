@@ -415,7 +415,11 @@ __global__ void compress_plan_kernel(int64_t nslices, const int64_t* __restrict_
         ok = uni = false;
         break;
       }
-      uni = uni && u && U <= kUniformMaxSlots;
+      // a uniform table is walked entry by entry (one masked gather per entry),
+      // so it only pays while it is not much longer than the slice's slot count:
+      // a reordered operator whose 32 rows share few offsets has U >> W (a
+      // shuffled 27-point slice: U ~ 800, W = 27) and stays explicit SELL-32
+      uni = uni && u && U <= kUniformMaxSlots && 2 * U <= 3 * W;
       if (uni)
         h = mix64(mix64(mix64(mix64(h, static_cast<unsigned>(off)), mask), vb),
                   static_cast<unsigned long long>(gk));

@@ -73,3 +73,27 @@ def test_formats_spmv_and_solve_bitwise(cs, port, kind, dims, coef, monkeypatch)
     ref = sols["cdia"]
     for name, v in sols.items():
         assert v == ref, f"{name} differs from the CDIA solve"
+
+
+def test_shuffled_operator_stays_explicit(cs, port):
+    """A reordered operator (rows shuffled inside windows, columns renumbered)
+    has slices whose 32 rows share few relative offsets: the conversion must keep
+    them as explicit SELL-32 (a uniform table would be ~800 entries walked one by
+    one per warp: 5x slower, profiles/r02h_irregular_spmv_128.txt) -- and the
+    SpMV stays bitwise the oracle's."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from irregular_bench import permuted
+    o = port.poisson27(24, 24, 24)
+    a = cs.CsrMatrix(o.n, o.rowptr, o.col, o.val)
+    rp, col, val = permuted(a, 4096)
+    p = cs.DeviceProblem.from_csr(cs.CsrMatrix(o.n, rp, col, val))
+    try:
+        assert p.uniform_slices == 0 and p.cdia_classes == 0, (p.uniform_slices, p.cdia_classes)
+        assert p.device_bytes / p.nnz_local < 13.0  # explicit: 8 B value + 4 B column (+ padding)
+        from oracle.oracle import Csr
+        q = Csr(o.n, rp, col, val)
+        x = np.random.default_rng(5).standard_normal(o.n)
+        assert p.spmv(x).tobytes() == port.spmv(q, x).tobytes()
+    finally:
+        p.close()

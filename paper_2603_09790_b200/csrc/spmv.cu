@@ -689,6 +689,7 @@ struct BoxGeom {
   // lower neighbour iff !zl_first, its last plane its upper one iff !zu_last)
   int nobits = 0, zl_first = 1, zu_last = 1;
   int zplast = 0;     // nobits: the launch plane holding its last real row (R1 may be slice-padded)
+  int64_t lseg = 1;   // planes per band of the item order (BoxIter)
   int vstrip = 0;     // separable path with vertical row strips (L divides the block size)
 };
 
@@ -703,13 +704,26 @@ struct BoxIter {
   int64_t it, i1;
   int c = 0, k = 0, m0 = 0, m1 = 0;
   bool valid = false;
+  // items in plane-band-major order: band s (planes [s*lseg, s*lseg + ls)),
+  // then column, then plane. With lseg ~ one block's share, blocks on
+  // neighbouring columns walk the same planes at the same time, so the halo
+  // lines a column stages from its neighbours are L2 hits (column-major order:
+  // +26 % DRAM reads at 512^3, profiles/r02h_ncu_sep512_*.txt)
   __device__ __forceinline__ void seg(const BoxGeom& b) {
     valid = it < i1;
     if (!valid) return;
-    const int64_t cc = it / b.nplanes;
+    const int64_t band_items = b.ncols * b.lseg;
+    const int64_t nb = (b.nplanes + b.lseg - 1) / b.lseg;
+    int64_t s = it / band_items;
+    if (s > nb - 1) s = nb - 1;
+    const int64_t rem = it - s * band_items;
+    const int64_t p0 = s * b.lseg;
+    const int64_t ls = b.nplanes - p0 < b.lseg ? b.nplanes - p0 : b.lseg;
+    const int64_t cc = rem / ls;
     c = static_cast<int>(cc);
-    m0 = static_cast<int>(it - cc * b.nplanes);
-    m1 = static_cast<int>(m0 + (i1 - it) < b.nplanes ? m0 + (i1 - it) : b.nplanes);
+    m0 = static_cast<int>(p0 + (rem - cc * ls));
+    const int64_t end = p0 + ls;  // this column's band ends here
+    m1 = static_cast<int>(m0 + (i1 - it) < end ? m0 + (i1 - it) : end);
     k = m0;
   }
   __device__ __forceinline__ void next(const BoxGeom& b) {
@@ -1352,6 +1366,12 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
     const int64_t items = b.ncols * b.nplanes;
     const unsigned grid = static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(items, 148 * per_sm)));
+    {  // band length ~ one block's share of the items (CS_BOX_BANDS=0: column-major)
+      const char* bd_e = std::getenv("CS_BOX_BANDS");
+      const bool bands = bd_e == nullptr || std::atoi(bd_e) != 0;
+      const int64_t share = (items + grid - 1) / grid;
+      b.lseg = bands ? std::max<int64_t>(1, std::min<int64_t>(b.nplanes, share)) : b.nplanes;
+    }
     if constexpr (KIND == kMpkFirstF || KIND == kMpkMidF || KIND == kResidF || KIND == kDot) {
       const char* sk_e = std::getenv("CS_BOX_SEPK");
       const bool sk_env = sk_e == nullptr || std::atoi(sk_e) != 0;
@@ -1374,6 +1394,8 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
         const int per = kernel_setup(reinterpret_cast<const void*>(sk), nthr, ssmem);
         const unsigned sgrid = static_cast<unsigned>(
             std::max<int64_t>(1, std::min<int64_t>(items, 148 * per)));
+        if (b.lseg != b.nplanes || std::getenv("CS_BOX_BANDS") == nullptr)
+          b.lseg = std::max<int64_t>(1, std::min<int64_t>(b.nplanes, (items + sgrid - 1) / sgrid));
         sk<<<sgrid, nthr, ssmem, st>>>(a, g, b, t);
         return true;
       }

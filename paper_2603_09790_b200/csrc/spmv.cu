@@ -1394,7 +1394,8 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
         const int per = kernel_setup(reinterpret_cast<const void*>(sk), nthr, ssmem);
         const unsigned sgrid = static_cast<unsigned>(
             std::max<int64_t>(1, std::min<int64_t>(items, 148 * per)));
-        if (b.lseg != b.nplanes || std::getenv("CS_BOX_BANDS") == nullptr)
+        const char* bd_e = std::getenv("CS_BOX_BANDS");
+        if (bd_e == nullptr || std::atoi(bd_e) != 0)  // bands sized for this kernel's grid
           b.lseg = std::max<int64_t>(1, std::min<int64_t>(b.nplanes, (items + sgrid - 1) / sgrid));
         sk<<<sgrid, nthr, ssmem, st>>>(a, g, b, t);
         return true;

@@ -258,13 +258,10 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// The r products ride on the tensor cores too: r is column S of the P tile, so
-// [Q | Z]^T [P | r] gives G1, G2 and c2 = Q^T r, c1 = Z^T r in one DMMA chain
-// (no 2s per-lane FMA accumulators: 32 registers fewer, more warps resident).
 template <int S>
 struct PackShape {
   static constexpr int MT = (2 * S + 7) / 8;
-  static constexpr int NT = (S + 1 + 7) / 8;
+  static constexpr int NT = (S + 7) / 8;
   static constexpr int UC = MT * 8;
   static constexpr int PC = NT * 8;
   static constexpr int NOUT = 2 * S * S + 2 * S + 1;
@@ -289,14 +286,16 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
   double* sU = smem + warp * Sh::smem_warp;
   double* sP = sU + Sh::UC * kPackStride;
   for (int c = 2 * S; c < Sh::UC; ++c) sU[c * kPackStride + lane] = 0.0;
-  for (int c = S + 1; c < Sh::PC; ++c) sP[c * kPackStride + lane] = 0.0;
+  for (int c = S; c < Sh::PC; ++c) sP[c * kPackStride + lane] = 0.0;
 
   double acc[Sh::MT][Sh::NT][2];
 #pragma unroll
   for (int m = 0; m < Sh::MT; ++m)
 #pragma unroll
     for (int q = 0; q < Sh::NT; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
-  double rr = 0.0;
+  double c1[S], c2[S], rr = 0.0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) c1[i] = c2[i] = 0.0;
 
   const int64_t nchunks = (n + 31) / 32;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kPackWarps;
@@ -334,11 +333,12 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     rr = fma(rv, rv, rr);
 #pragma unroll
     for (int i = 0; i < S; ++i) {
+      c2[i] = fma(qv[i], rv, c2[i]);
+      c1[i] = fma(zv[i], rv, c1[i]);
       sU[i * kPackStride + lane] = qv[i];
       sU[(S + i) * kPackStride + lane] = zv[i];
       sP[i * kPackStride + lane] = pv[i];
     }
-    sP[S * kPackStride + lane] = rv;
     __syncwarp();
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
@@ -354,9 +354,16 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     }
     __syncwarp();
   }
-  // warp-level: rr by shuffle tree
+  // warp-level: plain accumulators by shuffle tree
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) rr += __shfl_down_sync(0xffffffffu, rr, off);
+  for (int off = 16; off > 0; off >>= 1) {
+    rr += __shfl_down_sync(0xffffffffu, rr, off);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      c1[i] += __shfl_down_sync(0xffffffffu, c1[i], off);
+      c2[i] += __shfl_down_sync(0xffffffffu, c2[i], off);
+    }
+  }
   __syncthreads();  // tiles are dead; reuse smem as [warp][NOUT]
   double* out = smem + warp * Sh::NOUT;
 #pragma unroll
@@ -366,12 +373,17 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = m * 8 + g;       // U column: Q_i (i < S) or Z_{i-S}
-        const int j = q * 8 + 2 * t + e;  // P column (j == S: r)
+        const int j = q * 8 + 2 * t + e;  // P column
         if (i < 2 * S && j < S) out[(i < S ? 0 : S * S) + (i % S) + j * S] = acc[m][q][e];
-        if (i < 2 * S && j == S)  // Q_i^T r -> c2, Z_{i-S}^T r -> c1
-          out[2 * S * S + (i < S ? S + i : i - S)] = acc[m][q][e];
       }
-  if (lane == 0) out[2 * S * S + 2 * S] = rr;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      out[2 * S * S + i] = c1[i];
+      out[2 * S * S + S + i] = c2[i];
+    }
+    out[2 * S * S + 2 * S] = rr;
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < Sh::NOUT; e += kPackWarps * 32) {
     double s = 0.0;

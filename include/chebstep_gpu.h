@@ -158,6 +158,8 @@ typedef struct {
 #define CS_SCHED_EXPLICIT_W 2 /* W_k reduced from the vectors each outer */
 #define CS_SCHED_TRUE_R 4     /* r from b - A x each outer (no AQ block) */
 #define CS_SCHED_R_FROM_Z0 8  /* r not stored: the pack forms r = D z_0 */
+#define CS_SCHED_P2P_ALLREDUCE 16 /* multi-GPU: the packed block's allreduce fused into the
+                                     pack over NVLink peer memory (no NCCL call per outer) */
 
 /* ------------------------------------------------------------ errors / info */
 const char* cs_last_error(int* payload);

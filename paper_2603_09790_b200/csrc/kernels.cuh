@@ -193,6 +193,21 @@ __device__ __forceinline__ void p_from_z(const double (&zz)[S + 1], const PzArgs
   }
 }
 #endif
+// Fused NVLink allreduce of the packed block (multi-GPU fast algebra, DESIGN.md
+// 7): the pack's last block stores its rank-local block into slot [epoch & 1]
+// [rank] of EVERY rank's exchange buffer (peer memory mapped by CUDA IPC),
+// releases a per-source flag in each, waits for all flags of this epoch and sums
+// the slots in rank order 0..N-1 -- the same bits on every rank, no NCCL call.
+constexpr int kXredMaxRanks = 8;
+constexpr int kXredSlot = 1024;  // doubles per slot (>= the packed block for s <= 16)
+struct XredArgs {
+  int nranks = 0, rank = 0, npack = 0;
+  unsigned long long epoch = 0;
+  double* slots = nullptr;              // mine: [2][nranks][kXredSlot]
+  unsigned long long* flags = nullptr;  // mine: [nranks] (flag r written by rank r)
+  double* peer_slots[kXredMaxRanks] = {};
+  unsigned long long* peer_flags[kXredMaxRanks] = {};
+};
 // fast packed reduction {Q^T P, Z^T P, Z^T r, Q^T r, r^T r} (2s^2+2s+1 doubles)
 bool pack_supported(int s);
 // flags (multi-rank, or nullptr): s rank-local basis-breakdown column flags
@@ -200,7 +215,8 @@ bool pack_supported(int s);
 // derived from Z (p unused).
 void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket,
-                 DevState* st, double* flags, cudaStream_t strm, const PzArgs& pz = PzArgs{});
+                 DevState* st, double* flags, cudaStream_t strm, const PzArgs& pz = PzArgs{},
+                 const XredArgs& xr = XredArgs{});
 // flags[j] = 1.0 iff this rank's pending basis breakdown is in column j
 void launch_pending_flags(int s, const DevState* st, double* flags, cudaStream_t strm);
 size_t pack_partial_doubles(int s, int64_t n);

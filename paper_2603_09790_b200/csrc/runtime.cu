@@ -230,8 +230,99 @@ void p2p_teardown(cs_problem* p) {
     if (m.sig) cudaIpcCloseMemHandle(m.sig);
     m = cs_problem::PeerMap{};
   }
+  for (auto& x : p->xpeer) {
+    if (x) cudaIpcCloseMemHandle(x);
+    x = nullptr;
+  }
   cudaGetLastError();
   p->p2p = false;
+  p->xred_ok = false;
+}
+
+namespace {
+size_t xred_bytes(int nranks) {
+  return sizeof(double) * 2 * static_cast<size_t>(nranks) * kXredSlot +
+         sizeof(unsigned long long) * kXredMaxRanks;
+}
+
+// Collective (every rank, after the neighbour mapping): map every rank's
+// exchange buffer; flags restart at 0 for this solve (the all-gather orders the
+// reset before any peer's first store). false on every rank if any rank cannot.
+bool xred_setup(cs_problem* p, bool ok_in) {
+  cs_ctx* c = p->ctx;
+  const int N = c->nranks, me = c->rank;
+  const char* env = std::getenv("CS_P2P_ALLREDUCE");
+  int ok = ok_in && N <= kXredMaxRanks && (env == nullptr || std::atoi(env) != 0);
+  if (ok && p->xred.p == nullptr) {
+    StreamBind plain(nullptr);  // IPC export needs a cudaMalloc allocation
+    p->xred.alloc(xred_bytes(N));
+  }
+  if (ok) {
+    CS_CUDA(cudaMemsetAsync(p->xred.p, 0, xred_bytes(N), c->stream));
+    if (!p->xred_exported) {
+      p->xred_exported = cudaIpcGetMemHandle(&p->ipc_xred, p->xred.p) == cudaSuccess;
+      cudaGetLastError();
+    }
+    ok = p->xred_exported;
+  }
+  struct XInfo {
+    cudaIpcMemHandle_t h;
+    unsigned char uuid[16];
+    int32_t ok, pad;
+  };
+  XInfo mine{};
+  mine.h = p->ipc_xred;
+  std::memcpy(mine.uuid, c->uuid, 16);
+  mine.ok = ok;
+  DBuf dev(sizeof(XInfo) * (N + 1));
+  XInfo* d = dev.as<XInfo>();
+  CS_CUDA(cudaMemcpyAsync(d + N, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+  CS_NCCL(ncclAllGather(d + N, d, sizeof(XInfo), ncclChar, c->comm, c->stream));
+  std::vector<XInfo> all(N);
+  CS_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(XInfo) * N, cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < N && ok; ++r) {
+    if (r == me) continue;
+    // ranks sharing a GPU must not spin on each other: the NCCL allreduce instead
+    if (!all[r].ok || std::memcmp(all[r].uuid, mine.uuid, 16) == 0) {
+      ok = 0;
+      break;
+    }
+    if (p->xpeer[r] == nullptr &&
+        cudaIpcOpenMemHandle(&p->xpeer[r], all[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      p->xpeer[r] = nullptr;
+      ok = 0;
+    }
+  }
+  DBuf e(sizeof(int));
+  CS_CUDA(cudaMemcpyAsync(e.p, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CS_NCCL(ncclAllReduce(e.p, e.p, 1, ncclInt32, ncclMin, c->comm, c->stream));
+  int all_ok = 0;
+  CS_CUDA(cudaMemcpyAsync(&all_ok, e.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CS_CUDA(cudaStreamSynchronize(c->stream));
+  p->xred_epoch = 0;
+  return all_ok != 0;
+}
+}  // namespace
+
+XredArgs xred_next(cs_problem* p, int npack) {
+  XredArgs x;
+  if (!p->xred_ok || npack > kXredSlot) return x;
+  cs_ctx* c = p->ctx;
+  x.nranks = c->nranks;
+  x.rank = c->rank;
+  x.npack = npack;
+  x.epoch = ++p->xred_epoch;
+  x.slots = p->xred.as<double>();
+  x.flags = reinterpret_cast<unsigned long long*>(x.slots + 2 * static_cast<size_t>(x.nranks) * kXredSlot);
+  for (int r = 0; r < x.nranks; ++r) {
+    if (r == x.rank) continue;
+    x.peer_slots[r] = static_cast<double*>(p->xpeer[r]);
+    x.peer_flags[r] = reinterpret_cast<unsigned long long*>(
+        x.peer_slots[r] + 2 * static_cast<size_t>(x.nranks) * kXredSlot);
+  }
+  return x;
 }
 
 bool p2p_setup(cs_problem* p, double* Z) {
@@ -324,6 +415,8 @@ bool p2p_setup(cs_problem* p, double* Z) {
   CS_CUDA(cudaMemcpyAsync(&all, e.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CS_CUDA(cudaStreamSynchronize(c->stream));
   p->p2p = all != 0;
+  // the packed-block allreduce over peer memory (collective on every rank)
+  p->xred_ok = xred_setup(p, p->p2p);
   return p->p2p;
 }
 
@@ -393,6 +486,8 @@ std::string format_device_error(unsigned long long word, int) {
                ": cholesky: non-positive pivot (basis breakdown)";
       return "pcg: non-positive curvature at iteration " + k;
     case CS_ERR_NCCL:
+      if (sub == 1 || payload == 1)
+        return "allreduce: a peer's packed block did not arrive (peer-memory allreduce timeout)";
       return "halo exchange: peer ghost planes did not arrive (peer-memory halo timeout)";
     case CS_ERR_GENERIC:
       if (sub == 1) return "estimate_interval: degenerate start vector";

@@ -187,6 +187,14 @@ struct cs_problem {
   cudaIpcMemHandle_t ipc_ws{}, ipc_sig{};
   unsigned long long p2p_epoch = 0; // halo exchanges consumed in the current solve
   bool p2p_pending = false;         // the last kernel pushed rows not yet released
+  // fused NVLink allreduce of the packed block (csg::XredArgs): my exchange
+  // buffer [2][nranks][kXredSlot] doubles + [nranks] flags, every rank's mapped
+  csg::DBuf xred;
+  cudaIpcMemHandle_t ipc_xred{};
+  bool xred_exported = false;
+  void* xpeer[csg::kXredMaxRanks] = {};
+  bool xred_ok = false;
+  unsigned long long xred_epoch = 0;
   csg::SellView view() const {
     csg::SellView v;
     v.n_local = n_local;
@@ -251,6 +259,8 @@ void problem_set_precond_fn(cs_problem* p, cs_precond_fn fn, void* user);
 // every rank calls it once per solve after its workspace is final). Returns
 // whether the peer-memory path is on for this solve (all ranks agree).
 bool p2p_setup(cs_problem* p, double* Z);
+// arguments of the fused allreduce for the next pack (advances the epoch)
+csg::XredArgs xred_next(cs_problem* p, int npack);
 void p2p_teardown(cs_problem* p);
 // SpMV of the fast MPK through the peer-memory halo: interior slices, then the
 // boundary slices after this exchange's ghost planes arrived; push_col (or

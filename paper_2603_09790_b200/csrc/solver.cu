@@ -755,6 +755,14 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   };
   // packed one-allreduce block {Q^T P, Z^T P, Z^T r, Q^T r, r^T r}
   auto packed_reduce = [&](const double* Qm, const double* Zm, const PzArgs& pza = PzArgs{}) {
+    if (use_pack && p->xred_ok && pza.zs != nullptr && npack <= kXredSlot) {
+      // the allreduce fused into the pack over NVLink peer memory (no NCCL call)
+      ++c->allreduces;
+      Launch L(c, CS_PHASE_REDUCE);
+      launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, flags, c->stream,
+                  pza, xred_next(p, npack));
+      return;
+    }
     if (use_pack) {
       Launch L(c, CS_PHASE_REDUCE);
       launch_pack(s, n, ld, Qm, Zm, bk.P, bk.r, raw, partial, ticket + 1, st, flags, c->stream,
@@ -1029,7 +1037,8 @@ void pcgs_solve_dev(cs_problem* p, const double* b_dev, const double* x0_dev,
   rep->t_lanczos_ms = t_lz;
   rep->t_solve_ms = t_solve;
   rep->schedule = (pz_on ? CS_SCHED_P_FROM_Z : 0) | (explicit_w ? CS_SCHED_EXPLICIT_W : 0) |
-                  (tr_on ? CS_SCHED_TRUE_R : 0) | (pz.r_from_z0 ? CS_SCHED_R_FROM_Z0 : 0);
+                  (tr_on ? CS_SCHED_TRUE_R : 0) | (pz.r_from_z0 ? CS_SCHED_R_FROM_Z0 : 0) |
+                  (p2p && p->xred_ok ? CS_SCHED_P2P_ALLREDUCE : 0);
   trace.mark("report");
 }
 

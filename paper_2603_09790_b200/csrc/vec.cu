@@ -272,11 +272,59 @@ struct PackShape {
 #ifndef CS_PACK_MINB
 #define CS_PACK_MINB 2
 #endif
+__device__ __forceinline__ unsigned long long xr_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void xr_st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// the last block of the pack: exchange + fixed-order sum (see XredArgs)
+__device__ __noinline__ void xred_exchange(const XredArgs& x, double* packed, DevState* st) {
+  const int N = x.nranks, me = x.rank, par = static_cast<int>(x.epoch & 1ull);
+  for (int r = 0; r < N; ++r) {
+    double* dst = (r == me ? x.slots : x.peer_slots[r]) +
+                  (static_cast<int64_t>(par) * N + me) * kXredSlot;
+    for (int e = threadIdx.x; e < x.npack; e += blockDim.x) dst[e] = packed[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < N && static_cast<int>(threadIdx.x) != me)
+    xr_st_release(x.peer_flags[threadIdx.x] + me, x.epoch);
+  if (threadIdx.x == 0) {  // every source's block of this epoch (bounded: no hung GPU)
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int r = 0; r < N; ++r) {
+      if (r == me) continue;
+      while (xr_ld_acquire(x.flags + r) < x.epoch) {
+        __nanosleep(64);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20ull * 1000000000ull) {
+          atomicCAS(&st->err, 0ull, make_err(11 /*CS_ERR_NCCL*/, 1));
+          st->done = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < x.npack; e += blockDim.x) {
+    double sum = 0.0;
+    for (int r = 0; r < N; ++r)
+      sum += __ldcg(x.slots + (static_cast<int64_t>(par) * N + r) * kXredSlot + e);
+    packed[e] = sum;
+  }
+}
+
 template <int S, bool PZ>
 __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     pack_kernel(int64_t n, int64_t ld, const double* __restrict__ Q, const double* __restrict__ Z,
                 const double* __restrict__ P, const double* __restrict__ r, double* packed,
-                double* partial, unsigned* ticket, DevState* st, double* flags, PzArgs pz) {
+                double* partial, unsigned* ticket, DevState* st, double* flags, PzArgs pz,
+                const __grid_constant__ XredArgs xr) {
   using Sh = PackShape<S>;
   if (halted(st)) return;
   extern __shared__ double smem[];
@@ -401,6 +449,10 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
   finalize_partials(partial, gridDim.x, Sh::NOUT, packed);
   if (flags) write_pending_flags(S, st, flags);
   if (threadIdx.x == 0) *ticket = 0u;
+  if (xr.nranks > 1) {  // fused NVLink allreduce of packed[0, npack)
+    __syncthreads();
+    xred_exchange(xr, packed, st);
+  }
 }
 
 int pack_grid(int64_t n) {
@@ -413,7 +465,7 @@ int pack_grid(int64_t n) {
 template <int S>
 void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
-                 double* flags, cudaStream_t strm, const PzArgs& pz) {
+                 double* flags, cudaStream_t strm, const PzArgs& pz, const XredArgs& xr) {
   using Sh = PackShape<S>;
   const bool pzm = pz.zs != nullptr;
   auto kern = pzm ? pack_kernel<S, true> : pack_kernel<S, false>;
@@ -424,7 +476,7 @@ void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const 
   const int64_t want = pack_grid(n);
   const int grid = static_cast<int>(std::min<int64_t>(want, 148 * per_sm));
   kern<<<grid, kPackWarps * 32, Sh::smem_bytes, strm>>>(n, ld, q, z, p, r, packed, partial, ticket,
-                                                        st, flags, pz);
+                                                        st, flags, pz, xr);
   CS_CUDA(cudaGetLastError());
 }
 
@@ -987,8 +1039,9 @@ size_t pack_partial_doubles(int s, int64_t n) {
 
 void launch_pack(int s, int64_t n, int64_t ld, const double* q, const double* z, const double* p,
                  const double* r, double* packed, double* partial, unsigned* ticket, DevState* st,
-                 double* flags, cudaStream_t strm, const PzArgs& pz) {
-#define CSG_PACK(SV) pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, flags, strm, pz)
+                 double* flags, cudaStream_t strm, const PzArgs& pz, const XredArgs& xr) {
+#define CSG_PACK(SV) \
+  pack_launch<SV>(n, ld, q, z, p, r, packed, partial, ticket, st, flags, strm, pz, xr)
   switch (s) {
     case 1: CSG_PACK(1); break;
     case 2: CSG_PACK(2); break;

@@ -49,7 +49,13 @@ def test_multi_gpu_parity(stencil, n, nz, mm, variant, tmp_path):
             assert r["n_ghost"] > 0, r
         assert r["outer_ok"], r
         assert r["transport_bitwise"], r
+        assert r["fused_allreduce_x_rel"] <= 1e-8, r
+        assert abs(r["fused_allreduce_outer"][0] - r["fused_allreduce_outer"][1]) <= 1, r
         assert r["halo_mode"] == ("nccl" if mm else "nvlink-p2p"), r
+        # PZ schedules over the peer halo: the per-outer allreduce runs inside the
+        # pack over peer memory (CS_SCHED_P2P_ALLREDUCE), off with CS_P2P_ALLREDUCE=0
+        if not mm:
+            assert bool(r["schedule"] & 16) and not r["schedule_nccl_allreduce"] & 16, r
         assert r["halo_mode_off"] == "nccl", r
         assert r["x_rel"] <= 1e-8, r
         assert abs(r["pcg_iters"][0] - r["pcg_iters"][1]) <= 1 and r["pcg_x_rel"] <= 1e-8, r

@@ -117,15 +117,25 @@ def main():
     res["allreduces"] = sol.report.device_allreduces
     res["halo_mode"] = p.halo_mode
     res["schedule"] = sol.report.schedule
-    # the same solve with the NCCL halo: the transport must not change a bit
+    # the same solve with the peer halo but the NCCL allreduce, and with the NCCL
+    # halo: the halo transport must not change a bit; the fused peer-memory
+    # allreduce (rank-order sums) is another rounding of the same block -> x to 1e-8
+    spec = sol.report.spectrum_used
+    os.environ["CS_P2P_ALLREDUCE"] = "0"
+    sol_a = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000, spectrum=spec,
+                                              variant=a.variant))
+    res["schedule_nccl_allreduce"] = sol_a.report.schedule
     os.environ["CS_P2P_HALO"] = "0"
-    sol_n = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000,
-                                              spectrum=sol.report.spectrum_used,
+    sol_n = p.pcg_s_solve(cfg=cs.SolverConfig(s=a.s, tol=1e-8, max_outer=5000, spectrum=spec,
                                               variant=a.variant))
     os.environ.pop("CS_P2P_HALO")
+    os.environ.pop("CS_P2P_ALLREDUCE")
     res["halo_mode_off"] = p.halo_mode
-    res["transport_bitwise"] = bool(sol_n.x.tobytes() == sol.x.tobytes()
-                                    and sol_n.report.outer_iters == sol.report.outer_iters)
+    res["transport_bitwise"] = bool(sol_n.x.tobytes() == sol_a.x.tobytes()
+                                    and sol_n.report.outer_iters == sol_a.report.outer_iters)
+    res["fused_allreduce_x_rel"] = float(np.linalg.norm(sol.x - sol_a.x) /
+                                         max(np.linalg.norm(sol_a.x), 1e-300))
+    res["fused_allreduce_outer"] = [sol.report.outer_iters, sol_a.report.outer_iters]
     res["lambda_rel"] = abs(sol.report.spectrum_used.lambda_min / r_o.lambda_min - 1)
     pc = p.pcg_solve(tol=1e-8, max_iter=5000)
     xp, rpcg = port.pcg_solve(o, tol=1e-8, max_iter=5000)

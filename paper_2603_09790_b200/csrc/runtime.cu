@@ -302,6 +302,9 @@ bool xred_setup(cs_problem* p, bool ok_in) {
   CS_CUDA(cudaMemcpyAsync(&all_ok, e.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CS_CUDA(cudaStreamSynchronize(c->stream));
   p->xred_epoch = 0;
+  if (std::getenv("CS_TRACE"))
+    std::fprintf(stderr, "[cs-trace] rank %d xred_setup ok_in %d local %d all %d exported %d\n", me,
+                 static_cast<int>(ok_in), ok, all_ok, static_cast<int>(p->xred_exported));
   return all_ok != 0;
 }
 }  // namespace

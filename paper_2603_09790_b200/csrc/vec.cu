@@ -284,29 +284,30 @@ __device__ __forceinline__ void xr_st_release(unsigned long long* p, unsigned lo
 // the last block of the pack: exchange + fixed-order sum (see XredArgs)
 __device__ __noinline__ void xred_exchange(const XredArgs& x, double* packed, DevState* st) {
   const int N = x.nranks, me = x.rank, par = static_cast<int>(x.epoch & 1ull);
-  for (int r = 0; r < N; ++r) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp r (< N) stores the block into rank r's slot, then its lane 0 fences once
+  // (one MEMBAR.SYS per peer, not per thread) and releases the flag
+  if (warp < N) {
+    const int r = warp;
     double* dst = (r == me ? x.slots : x.peer_slots[r]) +
                   (static_cast<int64_t>(par) * N + me) * kXredSlot;
-    for (int e = threadIdx.x; e < x.npack; e += blockDim.x) dst[e] = packed[e];
+    for (int e = lane; e < x.npack; e += 32) dst[e] = packed[e];
+    __syncwarp();
+    if (lane == 0 && r != me) {
+      __threadfence_system();
+      xr_st_release(x.peer_flags[r] + me, x.epoch);
+    }
   }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x < N && static_cast<int>(threadIdx.x) != me)
-    xr_st_release(x.peer_flags[threadIdx.x] + me, x.epoch);
-  if (threadIdx.x == 0) {  // every source's block of this epoch (bounded: no hung GPU)
+  if (warp == (N < 8 ? N : 0) && lane < N && lane != me) {  // wait for every source (bounded)
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (int r = 0; r < N; ++r) {
-      if (r == me) continue;
-      while (xr_ld_acquire(x.flags + r) < x.epoch) {
-        __nanosleep(64);
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 20ull * 1000000000ull) {
-          atomicCAS(&st->err, 0ull, make_err(11 /*CS_ERR_NCCL*/, 1));
-          st->done = 1;
-          break;
-        }
+    while (xr_ld_acquire(x.flags + lane) < x.epoch) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20ull * 1000000000ull) {
+        atomicCAS(&st->err, 0ull, make_err(11 /*CS_ERR_NCCL*/, 1));
+        st->done = 1;
+        break;
       }
     }
   }

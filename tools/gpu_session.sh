@@ -44,6 +44,14 @@ import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['solve_roofline']
 print('variant $v', 'outer', d['config']['outer_iters'], 'ms/outer %.4f' % s['t_outer_ms'], 'lz %.1f' % s['t_lanczos_ms'], 'value %.5f' % d['value'], 'mhz', d['clocks']['sm_mhz'], d['phases_ms'])"
       done > $out/${tag}_abrz.txt 2>&1 ;;
+    ab4xr)
+      for g in 256 512; do for v in 0 1 0 1; do
+        CS_P2P_ALLREDUCE=$v timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+          --master-port $((29700 + v)) bench.py --gpus 4 --grid $g --no-cpu --no-e2e --no-pcg --steps 3 --warmup 3 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['solve_roofline']
+print('grid $g xred $v', 'outer', d['config']['outer_iters'], 'ms/outer %.4f' % s['t_outer_ms'], 'value %.5f' % d['value'], 'mhz', d['clocks']['sm_mhz'], d['phases_ms'])"
+      done; done > $out/${tag}_ab4xr.txt 2>&1 ;;
     trband)
       timeout 2400 python tools/count_band.py --ref-only --variants 0,256 --cases p27:96:8,p27:128:8,p27:128:4,p7:256:4 --out $out/${tag}_trband.json > $out/${tag}_trband.log 2>&1
       timeout 1800 python tools/count_band.py --skip-ref --variants 0,256 --cases p27:256:8,p27:512:8 --out $out/${tag}_trband.json >> $out/${tag}_trband.log 2>&1 ;;

@@ -3,7 +3,7 @@
 # environment setting, ms per outer iteration and the solve time printed per run.
 #   bash tools/ab_env.sh "CS_BOX_WS=0" "CS_BOX_WS=1" ...
 for envs in "$@"; do
-  env $envs timeout 600 python bench.py --grid 256 --steps 3 --warmup 3 --no-e2e --no-cpu --no-pcg 2>/dev/null |
+  env $envs timeout 900 python bench.py --grid ${AB_GRID:-256} --steps ${AB_STEPS:-3} --warmup 3 --no-e2e --no-cpu --no-pcg 2>/dev/null |
     python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['solve_roofline']

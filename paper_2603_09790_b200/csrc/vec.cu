@@ -320,7 +320,9 @@ __device__ __noinline__ void xred_exchange(const XredArgs& x, double* packed, De
   }
 }
 
-template <int S, bool PZ>
+// XR: the multi-GPU instance with the fused allreduce (the single-GPU instance
+// carries no exchange code: measured 35 % slower with it compiled in)
+template <int S, bool PZ, bool XR>
 __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
     pack_kernel(int64_t n, int64_t ld, const double* __restrict__ Q, const double* __restrict__ Z,
                 const double* __restrict__ P, const double* __restrict__ r, double* packed,
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kPackWarps * 32, CS_PACK_MINB)
   finalize_partials(partial, gridDim.x, Sh::NOUT, packed);
   if (flags) write_pending_flags(S, st, flags);
   if (threadIdx.x == 0) *ticket = 0u;
-  if (xr.nranks > 1) {  // fused NVLink allreduce of packed[0, npack)
+  if constexpr (XR) {  // fused NVLink allreduce of packed[0, npack)
     __syncthreads();
     xred_exchange(xr, packed, st);
   }
@@ -469,7 +471,8 @@ void pack_launch(int64_t n, int64_t ld, const double* q, const double* z, const 
                  double* flags, cudaStream_t strm, const PzArgs& pz, const XredArgs& xr) {
   using Sh = PackShape<S>;
   const bool pzm = pz.zs != nullptr;
-  auto kern = pzm ? pack_kernel<S, true> : pack_kernel<S, false>;
+  auto kern = xr.nranks > 1 ? (pzm ? pack_kernel<S, true, true> : pack_kernel<S, false, true>)
+                            : (pzm ? pack_kernel<S, true, false> : pack_kernel<S, false, false>);
   // one wave of resident blocks (a grid past the resident count leaves a
   // half-occupied second wave: 444 blocks at 2 per SM measured 0.64 ms at 256^3)
   const int per_sm = kernel_setup(reinterpret_cast<const void*>(kern), kPackWarps * 32,

@@ -826,79 +826,6 @@ __global__ void __launch_bounds__(kThreads) update_tr_kernel(UpdateArgs a, Cols<
   if (a.push_hi != nullptr && i >= a.hi_begin) a.push_hi[i - a.hi_begin] = acc;
 }
 
-// The same pass on row PAIRS: 16-byte loads and stores (half the memory
-// instructions, 512 contiguous bytes per warp per column); bitwise the same
-// arithmetic per row. Needs 16-byte aligned columns (the workspace's are).
-template <int S, bool BETA>
-__global__ void __launch_bounds__(kThreads) update_tr2_kernel(UpdateArgs a, Cols<S> c) {
-  if (halted(a.st)) return;
-  __shared__ double sh_alpha[S];
-  __shared__ double sh_beta[BETA ? S * S : 1];
-  for (int t = threadIdx.x; t < S; t += blockDim.x) sh_alpha[t] = a.alpha[t];
-  if constexpr (BETA)
-    for (int t = threadIdx.x; t < S * S; t += blockDim.x) sh_beta[t] = a.beta[t];
-  __syncthreads();
-  const int64_t i = 2 * (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x);
-  if (i >= a.n) return;
-  if (i + 1 >= a.n) {  // odd tail row
-    double acc = a.x[i];
-    double lo[S], hi[S];
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-      lo[q] = c.q[q][i];
-      if constexpr (BETA) hi[q] = c.z[q][i];
-    }
-    if constexpr (BETA) {
-#pragma unroll
-      for (int q = 0; q < S; ++q)
-#pragma unroll
-        for (int j = 0; j < S; ++j) hi[j] = __dadd_rn(hi[j], __dmul_rn(sh_beta[q + j * S], lo[q]));
-#pragma unroll
-      for (int j = 0; j < S; ++j) c.q[j][i] = hi[j];
-    }
-#pragma unroll
-    for (int j = 0; j < S; ++j) acc = __dadd_rn(acc, __dmul_rn(sh_alpha[j], BETA ? hi[j] : lo[j]));
-    a.x[i] = acc;
-    if (a.push_lo != nullptr && i < a.send_lo) a.push_lo[i] = acc;
-    if (a.push_hi != nullptr && i >= a.hi_begin) a.push_hi[i - a.hi_begin] = acc;
-    return;
-  }
-  double2 acc = *reinterpret_cast<const double2*>(a.x + i);
-  double2 lo[S], hi[S];
-#pragma unroll
-  for (int q = 0; q < S; ++q) {
-    lo[q] = *reinterpret_cast<const double2*>(c.q[q] + i);
-    if constexpr (BETA) hi[q] = *reinterpret_cast<const double2*>(c.z[q] + i);
-  }
-  if constexpr (BETA) {
-#pragma unroll
-    for (int q = 0; q < S; ++q)
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        const double bqj = sh_beta[q + j * S];
-        hi[j].x = __dadd_rn(hi[j].x, __dmul_rn(bqj, lo[q].x));
-        hi[j].y = __dadd_rn(hi[j].y, __dmul_rn(bqj, lo[q].y));
-      }
-#pragma unroll
-    for (int j = 0; j < S; ++j) *reinterpret_cast<double2*>(c.q[j] + i) = hi[j];
-  }
-#pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const double aj = sh_alpha[j];
-    acc.x = __dadd_rn(acc.x, __dmul_rn(aj, BETA ? hi[j].x : lo[j].x));
-    acc.y = __dadd_rn(acc.y, __dmul_rn(aj, BETA ? hi[j].y : lo[j].y));
-  }
-  *reinterpret_cast<double2*>(a.x + i) = acc;
-  if (a.push_lo != nullptr) {
-    if (i < a.send_lo) a.push_lo[i] = acc.x;
-    if (i + 1 < a.send_lo) a.push_lo[i + 1] = acc.y;
-  }
-  if (a.push_hi != nullptr) {
-    if (i >= a.hi_begin) a.push_hi[i - a.hi_begin] = acc.x;
-    if (i + 1 >= a.hi_begin) a.push_hi[i + 1 - a.hi_begin] = acc.y;
-  }
-}
-
 template <int S>
 Cols<S> make_cols(const UpdateArgs& a) {
   Cols<S> c{};
@@ -1194,18 +1121,11 @@ void launch_fast_update(const UpdateArgs& a, cudaStream_t s) {
 
 bool launch_fast_update_tr(const UpdateArgs& a, cudaStream_t st) {
   if (a.n == 0) return true;
-  const char* pe = std::getenv("CS_UPD_PAIRS");  // per launch, like CS_SPMV_BOX (A/B, tests)
-  const bool pairs_env = pe == nullptr || std::atoi(pe) != 0;
-  const auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  const bool pairs = pairs_env && al16(a.x) && al16(a.q) && al16(a.z) && (a.ld & 1) == 0;
-  const unsigned grid = pairs ? grid_for((a.n + 1) / 2) : grid_for(a.n);
+  // one row per thread (a row-pair variant with 16-byte accesses measured 25 %
+  // slower at 256^3: profiles/r02h_ab_update_pairs_256.txt)
+  const unsigned grid = grid_for(a.n);
 #define CSG_TR(SV)                                                                          \
   case SV:                                                                                  \
-    if (pairs) {                                                                            \
-      if (a.beta) update_tr2_kernel<SV, true><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a)); \
-      else update_tr2_kernel<SV, false><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a));       \
-      break;                                                                                \
-    }                                                                                       \
     if (a.beta) update_tr_kernel<SV, true><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a)); \
     else update_tr_kernel<SV, false><<<grid, kThreads, 0, st>>>(a, make_cols<SV>(a));       \
     break

@@ -351,21 +351,3 @@ def test_analysis_hooks_reference_mode(cs, port, ref):
     assert pr.report.a_norm_error.tobytes() == hp["aerr"].tobytes()
     assert len(pr.report.iterates) == len(hp["iter"])
 
-
-def test_update_row_pairs_bitwise(cs):
-    """The true-residual update pass on row pairs (16-byte accesses) is the same
-    arithmetic per row as the one-row pass: bitwise the same solve (odd n: the
-    tail row takes the scalar path)."""
-    import os
-    for dims in ((33, 17, 9), (40, 40, 40)):
-        p = cs.DeviceProblem.generate("poisson27", *dims).set_precond("jacobi")
-        out = []
-        for v in ("1", "0"):
-            os.environ["CS_UPD_PAIRS"] = v
-            try:
-                r = p.pcg_s_solve(cfg=cs.SolverConfig(s=8, tol=1e-8, max_outer=3000))
-            finally:
-                os.environ.pop("CS_UPD_PAIRS", None)
-            out.append((r.report.outer_iters, r.x.tobytes()))
-        assert out[0] == out[1], dims
-        p.close()

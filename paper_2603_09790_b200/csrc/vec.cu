@@ -282,7 +282,7 @@ __device__ __forceinline__ void xr_st_release(unsigned long long* p, unsigned lo
 }
 
 // the last block of the pack: exchange + fixed-order sum (see XredArgs)
-__device__ __noinline__ void xred_exchange(const XredArgs& x, double* packed, DevState* st) {
+__device__ __forceinline__ void xred_exchange(const XredArgs& x, double* packed, DevState* st) {
   const int N = x.nranks, me = x.rank, par = static_cast<int>(x.epoch & 1ull);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warp r (< N) stores the block into rank r's slot, then its lane 0 fences once

@@ -321,13 +321,16 @@ __global__ void lz2_scale_kernel(int64_t n, const double* __restrict__ gr,
                                  const double* __restrict__ dinv, double dconst, double* g,
                                  double* v, const LanczosScalars* sc, DevState* st) {
   if (halted(st)) return;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
   // one reciprocal per step, not a division per row (fast mode only; the
-  // reference-order Lanczos keeps its divisions)
-  const double gv = gr[i] * sc->rdenom;
-  g[i] = gv;
-  v[i] = gv * (dinv ? dinv[i] : dconst);
+  // reference-order Lanczos keeps its divisions); a grid-stride sweep so the
+  // state and scalar loads are paid once per thread, not once per row
+  const double rd = sc->rdenom;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double gv = gr[i] * rd;
+    g[i] = gv;
+    v[i] = gv * (dinv ? dinv[i] : dconst);
+  }
 }
 
 // scalar steps: 0 normalise start (nrm = sqrt(v.g) > 0), 1 alpha_j (finite),
@@ -435,7 +438,8 @@ void lz2_cgs(int64_t n, int64_t ld, int m, const double* G, const double* dinv, 
 void lz2_scale(int64_t n, const double* gr, const double* dinv, double dconst, double* g, double* v,
                const LanczosScalars* sc, DevState* st, cudaStream_t s) {
   if (n == 0) return;
-  lz2_scale_kernel<<<grid_for(n), kThreads, 0, s>>>(n, gr, dinv, dconst, g, v, sc, st);
+  const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
+  lz2_scale_kernel<<<grid, kThreads, 0, s>>>(n, gr, dinv, dconst, g, v, sc, st);
   CS_CUDA(cudaGetLastError());
 }
 

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads)
     if constexpr (MB > 0) {
       // chunks of 8 pairs: 16 loads in flight per thread at a register count
       // that keeps several blocks resident (all 2m at once needed ~200 registers)
-      constexpr int kC = 16;  // loads in flight per thread (8: 0.71 of HBM at 256^3)
+      constexpr int kC = 8;  // 16 measured slower (Lanczos 59.5 -> 75.5 ms at 256^3)
 #pragma unroll 1
       for (int c0 = 0; c0 < MB; c0 += kC) {
         if (c0 >= m) break;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-// gr -= sum_i proj_i g_i (16-column chunks), fused with the dot (D^-1 gr) . gr
+// gr -= sum_i proj_i g_i (8-column chunks), fused with the dot (D^-1 gr) . gr
 __global__ void __launch_bounds__(kThreads)
     lz2_cgs_kernel(int64_t n, int64_t ld, int m, const double* __restrict__ G,
                    const double* __restrict__ dinv, double dconst, double* gr, const double* proj,
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kThreads)
   double d = 0.0;
   if (i < n) {
     double gv = gr[i];
-    constexpr int kC = 16;  // loads in flight per thread (8: 0.71 of HBM at 256^3)
+    constexpr int kC = 8;  // 16 measured slower (Lanczos 59.5 -> 75.5 ms at 256^3)
 #pragma unroll 1
     for (int c0 = 0; c0 < m; c0 += kC) {
       double gg[kC];

@@ -866,13 +866,6 @@ constexpr int kSepNS = 8;
 template <int KIND, bool JAC, bool WS, int LC>
 __global__ void __launch_bounds__(CS_BOX_THREADS + (WS ? 32 : 0), 1)
     sell_boxsep_kernel(SellView a, SpmvArgs g, BoxGeom b, const __grid_constant__ CdiaTable t) {
-  // Programmatic dependent launch (CS_PDL): this grid may be scheduled while the
-  // previous kernel drains; nothing it reads is touched before the previous
-  // grid has completed and flushed (griddepcontrol.wait; a no-op without PDL).
-  // Its own dependents may be scheduled at once: they occupy SMs only as these
-  // blocks exit (one resident block per SM) and wait the same way.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (g.st != nullptr && *(volatile int*)&g.st->done) return;
   halo_release(g);
   if (g.wait_ctr != nullptr) {
@@ -1404,22 +1397,7 @@ bool box_launch(bool jac, const SellView& a, const SpmvArgs& g, const CdiaClass&
         const char* bd_e = std::getenv("CS_BOX_BANDS");
         if (bd_e == nullptr || std::atoi(bd_e) != 0)  // bands sized for this kernel's grid
           b.lseg = std::max<int64_t>(1, std::min<int64_t>(b.nplanes, (items + sgrid - 1) / sgrid));
-        const char* pdl_e = std::getenv("CS_PDL");
-        if (pdl_e == nullptr || std::atoi(pdl_e) != 0) {
-          cudaLaunchConfig_t lc{};
-          lc.gridDim = dim3(sgrid);
-          lc.blockDim = dim3(nthr);
-          lc.dynamicSmemBytes = static_cast<size_t>(ssmem);
-          lc.stream = st;
-          cudaLaunchAttribute at[1];
-          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-          at[0].val.programmaticStreamSerializationAllowed = 1;
-          lc.attrs = at;
-          lc.numAttrs = 1;
-          CS_CUDA(cudaLaunchKernelEx(&lc, sk, a, g, b, t));
-        } else {
-          sk<<<sgrid, nthr, ssmem, st>>>(a, g, b, t);
-        }
+        sk<<<sgrid, nthr, ssmem, st>>>(a, g, b, t);
         return true;
       }
     }
